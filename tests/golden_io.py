@@ -1,0 +1,44 @@
+"""Loaders for the committed golden fixtures (generated from the reference by
+tests/golden/make_golden.py)."""
+import gzip
+import json
+import os
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def _load(name):
+    with gzip.open(os.path.join(GOLDEN, name), "rt") as fh:
+        return json.load(fh)
+
+
+def _ints(hexlist):
+    return [int(x, 16) for x in hexlist]
+
+
+def ks_cases():
+    out = []
+    for c in _load("ks_golden.json.gz"):
+        out.append((c["tag"], _ints(c["f"]), _ints(c["g"]), c["b"], _ints(c["h"])))
+    return out
+
+
+def pack_cases():
+    out = []
+    for c in _load("pack_golden.json.gz"):
+        out.append((_ints(c["c"]), c["b"], c["w"], int(c["pack"]), int(c["rev"]),
+                    int(c["neg"]), int(c["nrev"])))
+    return out
+
+
+def recon_cases():
+    return [(_ints(c["fwd"]), _ints(c["rev"]), c["w"], _ints(c["h"]))
+            for c in _load("recon_golden.json.gz")]
+
+
+def bivar_cases():
+    return [(c["tag"], c["f"], c["g"], c["h"]) for c in _load("bivar_golden.json.gz")]
+
+
+def signed_cases():
+    return [(c["f"], c["g"], [int(v) for v in c["h"]]) for c in _load("signed_golden.json.gz")]
