@@ -1,0 +1,143 @@
+/*
+ * kmx.h -- C ABI of the B200-native multipoint Kronecker substitution path.
+ *
+ * The reference package (kronmul, pure Python) has no FFI; these entry points
+ * are the batched native equivalents of its Python multiply entry points, and
+ * are what a ctypes / cffi binding of the reference would bind:
+ *
+ *   kmx_ks_mul        <- kronmul.ksint.ks1_mul / ks2_mul / ks3_mul / ks4_mul
+ *                        (pkg/src/kronmul/ksint.py:219-348), batched over pairs
+ *   kmx_ks_mul_host   <- the same, host buffers in/out (the drop-in path)
+ *   kmx_reconstruct   <- kronmul.ksint.reconstruct_overlapped
+ *                        (pkg/src/kronmul/ksint.py:137-195)
+ *   kmx_bks_mul       <- kronmul.bipoly.bks_standard / bks_reciprocal /
+ *                        bks_negated / bks_four with ring_z()
+ *                        (pkg/src/kronmul/bipoly.py:177-278)
+ *   kmx_ks_params     <- kronmul.ksint.derive_params (ksint.py:82-98)
+ *
+ * Conventions
+ *   - Plain pointers and sizes; no torch types.  Device entry points take
+ *     device pointers and a cudaStream_t passed as void*; they are
+ *     stream-ordered and asynchronous.  Device-side consistency errors
+ *     (ReconstructionError, inexact halving/shift, coefficient out of range)
+ *     are latched in a flag inside the caller-owned workspace; read it with
+ *     kmx_ws_status() (synchronises the stream).
+ *   - Coefficients are little-endian 32-bit words: f is [batch][len_f][in_words],
+ *     g is [batch][len_g][in_words], h is [batch][len_f+len_g-1][out_words]
+ *     with out_words >= kmx_ks_out_words(...).
+ *   - Variant numbering follows the reference names (ksint.py:8-12):
+ *     1 = standard (2^N), 2 = reciprocal (2^N, 2^-N), 3 = negated (+-2^N),
+ *     4 = four-point (+-2^N, +-2^-N).
+ *   - KMX_SIGNED: coefficients are two's-complement coeff_bits-bit integers
+ *     (coeff_bits <= 32, in_words == 1); the product coefficients are written
+ *     in two's complement.  The reference rejects negative coefficients
+ *     (pack.py:44-46); the signed path is the bias lift of SURVEY.md §8(c).
+ *
+ * Return codes map to the reference's exceptions:
+ *   KMX_OK 0; KMX_EINVAL -1 -> ValueError (pack.py:39-59, ksint.py:84-87);
+ *   KMX_ERECON -2 -> ReconstructionError (ksint.py:44-45, :157-177);
+ *   KMX_EINEXACT -3 -> ValueError (bignat.py:265-269, :310-317, :446-447);
+ *   KMX_ECUDA -4; KMX_ENOMEM -5.
+ */
+#ifndef KMX_H
+#define KMX_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define KMX_OK 0
+#define KMX_EINVAL (-1)
+#define KMX_ERECON (-2)
+#define KMX_EINEXACT (-3)
+#define KMX_ECUDA (-4)
+#define KMX_ENOMEM (-5)
+
+/* flags */
+#define KMX_SIGNED 1u          /* two's-complement input coefficients        */
+#define KMX_NO_VALIDATE 2u     /* skip the 0 <= c < 2^b range check           */
+
+/* Derived parameters (ksint.py:82-98).  out[0..7] = e, N1, N2, N4,
+ * four_point_safe, out_len, limbs of the packed f operand, limbs of the
+ * packed g operand for `variant` (after any KS4 -> KS1 fallback). */
+int kmx_ks_params(int variant, int len_f, int len_g, int coeff_bits, unsigned flags,
+                  int64_t* out8);
+
+/* Minimum out_words for h: ceil(N1 / 32) (the reference's out_bound_bits =
+ * 2b+e, ksint.py:74-79). */
+int kmx_ks_out_words(int len_f, int len_g, int coeff_bits, unsigned flags);
+
+/* Bytes of device workspace needed by kmx_ks_mul for this problem. */
+size_t kmx_ks_workspace_bytes(int variant, int batch, int len_f, int len_g, int coeff_bits,
+                              unsigned flags);
+
+/* Batched KS product on the device (asynchronous on `stream`). */
+int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits,
+               const uint32_t* f, const uint32_t* g, int in_words,
+               uint32_t* h, int out_words,
+               void* workspace, size_t ws_bytes, unsigned flags, void* stream);
+
+/* Read and clear the workspace's latched device error (synchronises stream). */
+int kmx_ws_status(void* workspace, void* stream);
+
+/* Per-operand statistics of the last kmx_ks_mul on this workspace
+ * (synchronises stream): the reference's MulStats.limb_products under
+ * classical multiplication, i.e. the sum over sub-products of
+ * limbs64(x) * limbs64(y) on the normalized packed operands
+ * (bignat.py:327-330).  Written to *limb_products64 as a batch total. */
+int kmx_ws_limb_products(void* workspace, int variant, int batch, int len_f, int len_g,
+                         int coeff_bits, unsigned flags, uint64_t* limb_products64,
+                         void* stream);
+
+/* Host-buffer entry point: copies f, g to the device, runs kmx_ks_mul,
+ * copies h back and checks the device error flag.  Thread-safe (per-device
+ * cached buffers under a mutex).  Pinned host memory gives full PCIe speed. */
+int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits,
+                    const uint32_t* f, const uint32_t* g, int in_words,
+                    uint32_t* h, int out_words, unsigned flags,
+                    uint64_t* limb_products64 /* nullable: MulStats count */);
+
+/* Overlap reconstruction of `batch` independent digit-stream pairs on the
+ * device: fwd, rev are [batch][count+1][dwords] (rev listed most significant
+ * first, ksint.py:101-109), width_bits <= 32*dwords; h is
+ * [batch][count][hwords] with hwords >= ceil(2*width_bits/32).  carries
+ * (nullable) receives [batch][2*count+1] bytes: the count+1 forward-stream
+ * carries then the count reverse-stream carries (ksint.py:182-195,
+ * with_carries=True). */
+size_t kmx_reconstruct_workspace_bytes(int batch, int count, int dwords);
+int kmx_reconstruct(int batch, int count, int width_bits, const uint32_t* fwd,
+                    const uint32_t* rev, int dwords, uint32_t* h, int hwords,
+                    void* workspace, size_t ws_bytes, uint8_t* carries, void* stream);
+int kmx_reconstruct_host(int batch, int count, int width_bits, const uint32_t* fwd,
+                         const uint32_t* rev, int dwords, uint32_t* h, int hwords,
+                         uint8_t* carries);
+
+/* Bivariate R[x,y] -> R[x] reductions over R = Z.  f, g: [batch][lx][ly]
+ * int32 (coeffs[i][j] of x^i y^j, bipoly.py:75-97); h: [batch][2lx-1][2ly-1]
+ * int64.  coeff_bits bounds |c| < 2^coeff_bits (<= 30) and must keep every
+ * univariate product coefficient inside int64 (checked -> KMX_EINVAL). */
+size_t kmx_bks_workspace_bytes(int variant, int batch, int lx, int ly);
+int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits,
+                const int32_t* f, const int32_t* g, int64_t* h,
+                void* workspace, size_t ws_bytes, void* stream);
+int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits,
+                     const int32_t* f, const int32_t* g, int64_t* h);
+
+/* Measured IMAD.WIDE.U32 throughput on device 0 (32x32->64 products per
+ * second, full chip), the roofline denominator for the multiply kernels. */
+double kmx_imad_peak(int iters);
+
+/* Human-readable message for a return code. */
+const char* kmx_error_string(int code);
+
+/* Number of kernels launched by the last kmx_ks_mul / kmx_bks_mul call on
+ * this thread (for the bench's gpu_launches count). */
+int kmx_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KMX_H */

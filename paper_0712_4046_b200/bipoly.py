@@ -1,0 +1,148 @@
+"""Drop-in bivariate reductions R[x,y] -> R[x] over R = Z, on the GPU.
+
+Mirrors pkg/src/kronmul/bipoly.py: BiPoly (:75-97), RingOps (:31-44),
+ring_z (:53-56), ring_zmod (:59-72), MissingHalveError (:26-28) and
+bks_standard / bks_reciprocal / bks_negated / bks_four (:177-278).
+
+With ring_z() and the default univariate multiplier, the whole reduction
+(evaluation, univariate products, half-sums and overlap recovery) runs in
+libkmx.so.  Other rings (ring_zmod) and custom univariate multipliers are the
+next rows of SURVEY.md §8(f) and raise NotImplementedError here -- never a
+silent CPU path.
+"""
+from __future__ import annotations
+
+import operator
+from dataclasses import dataclass
+from typing import Any, Callable, Optional, Sequence
+
+import numpy as np
+
+from . import _lib
+from ._lib import check, lib
+
+__all__ = ["RingOps", "BiPoly", "MissingHalveError", "ring_z", "ring_zmod", "bks_standard",
+           "bks_reciprocal", "bks_negated", "bks_four"]
+
+UniMul = Callable[[Sequence[Any], Sequence[Any]], list]
+
+
+class MissingHalveError(ValueError):
+    """The ring has no exact halving, so this variant cannot run
+    (bipoly.py:26-28)."""
+
+
+@dataclass(frozen=True)
+class RingOps:
+    """Operation table of a commutative ring's additive structure
+    (bipoly.py:31-44).  ``name`` identifies the rings the GPU path handles."""
+
+    zero: Any
+    add: Callable[[Any, Any], Any]
+    sub: Callable[[Any, Any], Any]
+    neg: Callable[[Any], Any]
+    eq: Callable[[Any, Any], bool]
+    halve: Optional[Callable[[Any], Any]] = None
+    name: str = ""
+
+
+def _halve_int(a: int) -> int:
+    if a & 1:
+        raise ValueError("halving an odd integer is not exact")
+    return a >> 1
+
+
+def ring_z() -> RingOps:
+    """The integers (bipoly.py:53-56)."""
+    return RingOps(zero=0, add=operator.add, sub=operator.sub, neg=operator.neg, eq=operator.eq,
+                   halve=_halve_int, name="Z")
+
+
+def ring_zmod(n: int) -> RingOps:
+    """Integers mod n; halving exists only for odd n (bipoly.py:59-72)."""
+    if n < 2:
+        raise ValueError("modulus must be >= 2")
+    halve = None
+    if n % 2 == 1:
+        inv2 = (n + 1) // 2
+        halve = lambda a: (a * inv2) % n  # noqa: E731
+    return RingOps(zero=0, add=lambda a, b: (a + b) % n, sub=lambda a, b: (a - b) % n,
+                   neg=lambda a: (-a) % n, eq=operator.eq, halve=halve, name=f"Z/{n}")
+
+
+@dataclass(frozen=True)
+class BiPoly:
+    """Dense bivariate polynomial: coeffs[i][j] is the coefficient of
+    x**i * y**j (bipoly.py:75-97)."""
+
+    coeffs: tuple
+
+    def __post_init__(self):
+        coeffs = tuple(tuple(row) for row in self.coeffs)
+        object.__setattr__(self, "coeffs", coeffs)
+        if not coeffs or not coeffs[0]:
+            raise ValueError("both lengths must be >= 1")
+        width = len(coeffs[0])
+        if any(len(row) != width for row in coeffs):
+            raise ValueError("coefficient array must be rectangular")
+
+    @property
+    def lx(self) -> int:
+        return len(self.coeffs)
+
+    @property
+    def ly(self) -> int:
+        return len(self.coeffs[0])
+
+
+def _check_shapes(f: BiPoly, g: BiPoly) -> None:
+    if f.lx != g.lx or f.ly != g.ly:
+        raise ValueError("inputs must share both lengths")
+
+
+def _bks(variant: int, f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None,
+         needs_halve: bool) -> BiPoly:
+    _check_shapes(f, g)
+    if needs_halve and ring.halve is None:
+        raise MissingHalveError("ring does not support exact halving")
+    if ring.name != "Z":
+        raise NotImplementedError("GPU bivariate path covers R = Z (ring_z); "
+                                  "Z/nZ is a next row (SURVEY.md §8(f) #4)")
+    if mul is not None:
+        raise NotImplementedError("custom univariate multipliers are not routed through the GPU path")
+    lx, ly = f.lx, f.ly
+    fa = np.asarray(f.coeffs, dtype=object)
+    ga = np.asarray(g.coeffs, dtype=object)
+    mx = max(max(abs(int(c)) for c in fa.reshape(-1)), max(abs(int(c)) for c in ga.reshape(-1)))
+    cb = max(1, mx.bit_length())
+    if cb > 30:
+        raise ValueError("coefficient magnitude beyond the GPU path's int64 accumulation bound (|c| < 2^30)")
+    f32 = np.ascontiguousarray(fa.astype(np.int64).astype(np.int32))
+    g32 = np.ascontiguousarray(ga.astype(np.int64).astype(np.int32))
+    h = np.zeros((2 * lx - 1, 2 * ly - 1), dtype=np.int64)
+    rc = lib().kmx_bks_mul_host(variant, 1, lx, ly, cb, _lib.ptr(f32), _lib.ptr(g32), _lib.ptr(h))
+    check(rc, "bks")
+    return BiPoly(tuple(tuple(int(v) for v in row) for row in h))
+
+
+def bks_standard(f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None = None) -> BiPoly:
+    """One univariate product of length 2 Lx Ly - Lx - Ly + 1 (bipoly.py:177-188)."""
+    return _bks(1, f, g, ring, mul, False)
+
+
+def bks_reciprocal(f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None = None) -> BiPoly:
+    """Two univariate products of length Lx Ly plus overlap recovery
+    (bipoly.py:191-206)."""
+    return _bks(2, f, g, ring, mul, False)
+
+
+def bks_negated(f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None = None) -> BiPoly:
+    """Two univariate products with alternating chunk signs, half-sum and
+    half-difference (bipoly.py:209-232)."""
+    return _bks(3, f, g, ring, mul, True)
+
+
+def bks_four(f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None = None) -> BiPoly:
+    """Four univariate products of length ceil(Lx/2)(Ly-1) + Lx
+    (bipoly.py:235-278)."""
+    return _bks(4, f, g, ring, mul, True)

@@ -1,0 +1,489 @@
+// C ABI (include/kmx.h): parameter derivation, workspace planning and the
+// per-variant launch sequence pack -> mul -> finish [-> recon] [-> bias].
+//
+// Variant sequences follow the reference exactly:
+//   KS1 ksint.py:219-226   pack(N1) x2, one product, unpack out_len digits
+//   KS2 ksint.py:229-247   pack/pack_reversed(N2), 2 products, out_len+1
+//                          digits per stream, reversed list, reconstruction
+//   KS3 ksint.py:257-279   pack/pack_negated(N2), 2 products, (P+-Q)/2,
+//                          odd part >> N2, unpack at 2*N2, interleave
+//   KS4 ksint.py:289-348   4 packs at N4, 4 products, even/odd half-sums,
+//                          rev part >> N4 by parity of k, 2 reconstructions
+//                          at 2*N4; KS1 fallback if not four_point_safe and
+//                          the out_len == 1 single product (:299-303).
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/kmx.h"
+#include "kmx_common.cuh"
+#include "kmx_internal.h"
+
+using namespace kmx;
+
+namespace {
+
+int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+// ---- tiny host bignum for the four-point bound (ksint.py:282-286)
+typedef std::vector<uint32_t> Big;
+Big big_from_u64(unsigned long long v) { Big r; while (v) { r.push_back((uint32_t)v); v >>= 32; } return r; }
+Big big_pow2_minus1(int b) {  // 2^b - 1
+  Big r((b + 31) / 32, 0xffffffffu);
+  if (b % 32) r.back() = (1u << (b % 32)) - 1u;
+  return r;
+}
+Big big_mul(const Big& a, const Big& b) {
+  Big r(a.size() + b.size() + 1, 0u);
+  for (size_t i = 0; i < a.size(); i++) {
+    unsigned long long c = 0;
+    for (size_t j = 0; j < b.size(); j++) {
+      unsigned long long t = (unsigned long long)a[i] * b[j] + r[i + j] + c;
+      r[i + j] = (uint32_t)t;
+      c = t >> 32;
+    }
+    size_t k = i + b.size();
+    while (c) { unsigned long long t = (unsigned long long)r[k] + c; r[k] = (uint32_t)t; c = t >> 32; k++; }
+  }
+  while (!r.empty() && r.back() == 0) r.pop_back();
+  return r;
+}
+int big_cmp(Big a, Big b) {
+  while (!a.empty() && a.back() == 0) a.pop_back();
+  while (!b.empty() && b.back() == 0) b.pop_back();
+  if (a.size() != b.size()) return a.size() < b.size() ? -1 : 1;
+  for (size_t i = a.size(); i-- > 0;) if (a[i] != b[i]) return a[i] < b[i] ? -1 : 1;
+  return 0;
+}
+
+struct KsPlan {
+  int req_variant, variant, batch, lf, lg, b, in_words;
+  unsigned flags;
+  bool sign;
+  int e, N1, N2, N4, out_len, out_words_min;
+  bool safe;
+  int N, P, kinds[4];
+  int mf, mg, mp, mfs, mgs;
+  int G, C, nbands, TI;
+  long long ps;
+  int ns;
+  Stream st[4];
+  int W, dwords, cnt_max, dslots;
+  int nrs;
+  ReconStream rs[2];
+  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, total;
+};
+
+size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_words, unsigned flags) {
+  memset(&p, 0, sizeof p);
+  if (variant < 1 || variant > 4 || batch < 0 || lf < 1 || lg < 1 || b < 1) return KMX_EINVAL;
+  p.req_variant = variant;
+  p.batch = batch; p.lf = lf; p.lg = lg; p.b = b; p.flags = flags;
+  p.sign = (flags & KMX_SIGNED) != 0;
+  if (p.sign && b > 32) return KMX_EINVAL;
+  if (in_words <= 0) in_words = (b + 31) / 32;
+  if (p.sign && in_words != 1) return KMX_EINVAL;
+  if (!p.sign && in_words < (b + 31) / 32) return KMX_EINVAL;
+  p.in_words = in_words;
+  // derive_params (ksint.py:82-98)
+  p.e = bitlen_u64((unsigned long long)std::min(lf, lg) - 1);
+  p.N1 = 2 * b + p.e;
+  p.N2 = b + (p.e + 1) / 2;
+  p.N4 = (p.N1 + 3) / 4;
+  p.out_len = lf + lg - 1;
+  p.out_words_min = (p.N1 + 31) / 32;
+  // _four_point_safe (ksint.py:282-286): min(L)(2^b-1)^2 < 2^w (2^w - 1)
+  {
+    const int w = 2 * p.N4;
+    Big t = big_pow2_minus1(b);
+    Big lhs = big_mul(big_mul(t, t), big_from_u64((unsigned long long)std::min(lf, lg)));
+    // rhs = 2^w (2^w - 1) = (2^w - 1) << w
+    Big m1 = big_pow2_minus1(w);
+    Big sh((size_t)(w / 32) + m1.size() + 1, 0u);
+    for (size_t i = 0; i < m1.size(); i++) {
+      unsigned long long v = (unsigned long long)m1[i] << (w % 32);
+      sh[i + w / 32] |= (uint32_t)v;
+      sh[i + w / 32 + 1] |= (uint32_t)(v >> 32);
+    }
+    p.safe = big_cmp(lhs, sh) < 0;
+  }
+  int v = variant;
+  if (v == 4 && (!p.safe || p.out_len == 1)) v = 1;  // ksint.py:299-303
+  p.variant = v;
+  p.N = v == 1 ? p.N1 : (v == 4 ? p.N4 : p.N2);
+  if (2 * p.N < b) return KMX_EINVAL;  // pack.py:55-59 (cannot happen for derived N)
+  switch (v) {
+    case 1: p.P = 1; p.kinds[0] = 0; break;
+    case 2: p.P = 2; p.kinds[0] = 0; p.kinds[1] = 2; break;
+    case 3: p.P = 2; p.kinds[0] = 0; p.kinds[1] = 1; break;
+    default: p.P = 4; p.kinds[0] = 0; p.kinds[1] = 1; p.kinds[2] = 2; p.kinds[3] = 3; break;
+  }
+  // packed operand limbs: N (L-1) + b bits, +1 overlapped carry bit, +1 margin
+  long long bf = (long long)p.N * (lf - 1) + b + 2;
+  long long bg = (long long)p.N * (lg - 1) + b + 2;
+  if ((bf + 31) / 32 > (1LL << 28) || (bg + 31) / 32 > (1LL << 28)) return KMX_EINVAL;
+  p.mf = (int)((bf + 31) / 32);
+  p.mg = (int)((bg + 31) / 32);
+  p.mfs = (p.mf + 3) & ~3;
+  p.mgs = (p.mg + 3) & ~3;
+  p.mp = p.mf + p.mg;
+  // multiply geometry
+  {
+    int need = (p.mp + MUL_R - 1) / MUL_R, G = 1;
+    while (G < need && G < MUL_THREADS) G <<= 1;
+    p.G = G;
+    p.C = G * MUL_R;
+    p.nbands = (p.mp + p.C - 1) / p.C;
+    int ti = (p.mf + 7) & ~7;
+    p.TI = std::min(128, std::max(8, ti));
+    p.ps = (long long)p.nbands * p.C;
+  }
+  // output streams (finish) and reconstructions
+  const int k = p.out_len, n_even = (k + 1) / 2, n_odd = k / 2;
+  auto S = [&](int i) -> Stream& { return p.st[i]; };
+  memset(p.st, 0, sizeof p.st);
+  p.nrs = 0;
+  if (v == 1) {
+    p.ns = 1; p.W = p.N1;
+    S(0) = Stream{0, 0, 0, 0, 0, p.N1, k, 0, 0, 1, 0, 0};
+  } else if (v == 2) {
+    p.ns = 2; p.W = p.N2;
+    S(0) = Stream{0, 0, 0, 0, 0, p.N2, k + 1, 1, 0, 0, 0, 0};
+    S(1) = Stream{1, 0, 0, 0, 0, p.N2, k + 1, 1, 0, 0, 1, 1};
+    p.nrs = 1;
+    p.rs[0] = ReconStream{0, 1, k, 0, 1};
+    p.cnt_max = k + 1; p.dslots = 2;
+  } else if (v == 3) {
+    p.ns = 2; p.W = 2 * p.N2;
+    S(0) = Stream{0, 1, +1, 1, 1, 2 * p.N2, n_even, 0, 0, 2, 0, 0};
+    S(1) = Stream{0, 1, -1, 1, 1 + p.N2, 2 * p.N2, n_odd, 0, 1, 2, 0, 0};
+  } else {
+    const int w = 2 * p.N4;
+    p.ns = 4; p.W = w;
+    S(0) = Stream{0, 1, +1, 1, 1, w, n_even + 1, 1, 0, 0, 0, 0};
+    S(1) = Stream{0, 1, -1, 1, 1 + p.N4, w, n_odd + 1, 1, 0, 0, 1, 0};
+    S(2) = Stream{2, 3, +1, 3, 1 + (k % 2 == 0 ? p.N4 : 0), w, n_even + 1, 1, 0, 0, 2, 1};
+    S(3) = Stream{2, 3, -1, 3, 1 + (k % 2 == 1 ? p.N4 : 0), w, n_odd + 1, 1, 0, 0, 3, 1};
+    p.nrs = n_odd ? 2 : 1;
+    p.rs[0] = ReconStream{0, 2, n_even, 0, 2};
+    p.rs[1] = ReconStream{1, 3, n_odd, 1, 2};
+    p.cnt_max = n_even + 1; p.dslots = 4;
+  }
+  if (p.W > 32 * (FIN_HALO - 1)) return KMX_EINVAL;
+  p.dwords = (p.W + 31) / 32;
+  if (p.nrs && p.dwords > 17) return KMX_EINVAL;
+  // workspace layout
+  size_t o = 0;
+  p.off_err = o; o = align256(o + 16);
+  p.off_meta = o; o = align256(o + (size_t)batch * p.P * 2 * 2 * 4);
+  p.off_opf = o; o = align256(o + (size_t)batch * p.P * p.mfs * 4);
+  p.off_opg = o; o = align256(o + (size_t)batch * p.P * p.mgs * 4);
+  p.off_prod = o; o = align256(o + (size_t)batch * p.P * p.ps * 4);
+  p.off_spill = o; o = align256(o + (size_t)batch * p.P * p.nbands * 16);
+  p.off_dbuf = o;
+  if (p.nrs) o = align256(o + (size_t)batch * p.dslots * p.cnt_max * p.dwords * 4);
+  p.off_scr = o;
+  if (p.sign) o = align256(o + (size_t)batch * (lf + lg + 2) * 8);
+  p.total = o;
+  return KMX_OK;
+}
+
+int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KMX_OK : KMX_ECUDA; }
+
+int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h, int out_words,
+             void* ws, size_t ws_bytes, cudaStream_t st) {
+  g_launches = 0;
+  if (out_words < p.out_words_min) return KMX_EINVAL;
+  if (ws_bytes < p.total || (!ws && p.total)) return KMX_EINVAL;
+  if (p.batch == 0) return KMX_OK;
+  char* w = (char*)ws;
+  uint32_t* err = (uint32_t*)(w + p.off_err);
+  uint32_t* meta = (uint32_t*)(w + p.off_meta);
+  uint32_t* opf = (uint32_t*)(w + p.off_opf);
+  uint32_t* opg = (uint32_t*)(w + p.off_opg);
+  uint32_t* prod = (uint32_t*)(w + p.off_prod);
+  unsigned long long* spill = (unsigned long long*)(w + p.off_spill);
+  uint32_t* dbuf = (uint32_t*)(w + p.off_dbuf);
+  unsigned long long* scr = (unsigned long long*)(w + p.off_scr);
+  cudaError_t e = cudaMemsetAsync(err, 0, 4, st);
+  if (e != cudaSuccess) return KMX_ECUDA;
+
+  PackArgs pa;
+  memset(&pa, 0, sizeof pa);
+  pa.nops = 2 * p.P;
+  pa.N = p.N; pa.b = p.b; pa.in_words = p.in_words; pa.bias = p.sign; pa.err = err;
+  const bool validate = !(p.flags & KMX_NO_VALIDATE);
+  for (int s = 0; s < p.P; s++) {
+    PackOp& F = pa.op[s];
+    F.coeffs = f; F.coeff_pair_stride = (long long)p.lf * p.in_words; F.len = p.lf; F.kind = p.kinds[s];
+    F.out = opf + (long long)s * p.mfs; F.out_pair_stride = (long long)p.P * p.mfs;
+    F.meta = meta + 2 * s; F.meta_pair_stride = 4LL * p.P; F.m = p.mf; F.validate = validate && s == 0;
+    PackOp& Gq = pa.op[p.P + s];
+    Gq.coeffs = g; Gq.coeff_pair_stride = (long long)p.lg * p.in_words; Gq.len = p.lg; Gq.kind = p.kinds[s];
+    Gq.out = opg + (long long)s * p.mgs; Gq.out_pair_stride = (long long)p.P * p.mgs;
+    Gq.meta = meta + 2 * (p.P + s); Gq.meta_pair_stride = 4LL * p.P; Gq.m = p.mg; Gq.validate = validate && s == 0;
+  }
+  if ((e = launch_pack(pa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+  g_launches++;
+
+  MulArgs ma;
+  ma.A = opf; ma.a_stride = p.mfs; ma.ma = p.mf;
+  ma.B = opg; ma.b_stride = p.mgs; ma.mb = p.mg;
+  ma.P = prod; ma.p_stride = p.ps; ma.spill = spill;
+  ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
+  if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  g_launches++;
+
+  FinishArgs fa;
+  memset(&fa, 0, sizeof fa);
+  for (int i = 0; i < p.ns; i++) fa.s[i] = p.st[i];
+  fa.ns = p.ns;
+  fa.P = prod; fa.p_stride = p.ps; fa.mp = p.mp; fa.nprod_pair = p.P;
+  fa.spill = spill; fa.nbands = p.nbands; fa.band_cols = p.C;
+  fa.meta = meta; fa.meta_per_pair = 4 * p.P; fa.mf_slot_stride = p.P;
+  fa.h = h; fa.out_words = out_words; fa.h_pair_stride = (long long)p.out_len * out_words;
+  fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = (long long)p.cnt_max * p.dwords;
+  fa.dslots_pair = p.dslots; fa.err = err;
+  if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+  g_launches++;
+
+  if (p.nrs) {
+    ReconArgs ra;
+    memset(&ra, 0, sizeof ra);
+    for (int i = 0; i < p.nrs; i++) ra.s[i] = p.rs[i];
+    ra.ns = p.nrs; ra.batch = p.batch; ra.W = p.W;
+    ra.dbuf = dbuf; ra.dwords = p.dwords; ra.dslot_stride = (long long)p.cnt_max * p.dwords;
+    ra.dslots_pair = p.dslots;
+    ra.h = h; ra.out_words = out_words; ra.h_pair_stride = (long long)p.out_len * out_words;
+    ra.err = err;
+    if ((e = launch_recon(ra, st)) != cudaSuccess) return KMX_ECUDA;
+    g_launches++;
+  }
+  if (p.sign) {
+    BiasArgs ba;
+    ba.f = f; ba.g = g; ba.lf = p.lf; ba.lg = p.lg; ba.b = p.b;
+    ba.h = h; ba.out_words = out_words; ba.scratch = scr; ba.batch = p.batch;
+    if ((e = launch_bias(ba, st)) != cudaSuccess) return KMX_ECUDA;
+    g_launches++;
+  }
+  return KMX_OK;
+}
+
+int status_from_flag(uint32_t fl) {
+  if (fl & ERR_INVAL) return KMX_EINVAL;
+  if (fl & ERR_RECON) return KMX_ERECON;
+  if (fl & ERR_INEXACT) return KMX_EINEXACT;
+  return KMX_OK;
+}
+
+// per-device cached buffers for the host entry points
+struct HostCtx {
+  std::mutex mu;
+  cudaStream_t st = nullptr;
+  void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
+  size_t cap[4] = {0, 0, 0, 0};
+};
+HostCtx g_ctx[16];
+
+int ensure(HostCtx& c, int i, size_t bytes) {
+  if (c.cap[i] >= bytes) return KMX_OK;
+  if (c.buf[i]) cudaFree(c.buf[i]);
+  c.buf[i] = nullptr;
+  c.cap[i] = 0;
+  size_t want = std::max(bytes, (size_t)4096);
+  if (cudaMalloc(&c.buf[i], want) != cudaSuccess) return KMX_ENOMEM;
+  c.cap[i] = want;
+  return KMX_OK;
+}
+
+HostCtx* host_ctx(int* rc) {
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) { *rc = KMX_ECUDA; return nullptr; }
+  HostCtx& c = g_ctx[dev];
+  *rc = KMX_OK;
+  return &c;
+}
+
+}  // namespace
+
+extern "C" {
+
+int kmx_ks_params(int variant, int len_f, int len_g, int coeff_bits, unsigned flags, int64_t* out8) {
+  KsPlan p;
+  int rc = make_plan(p, variant, 1, len_f, len_g, coeff_bits, 0, flags);
+  if (rc) return rc;
+  out8[0] = p.e; out8[1] = p.N1; out8[2] = p.N2; out8[3] = p.N4;
+  out8[4] = p.safe; out8[5] = p.out_len; out8[6] = p.mf; out8[7] = p.mg;
+  return KMX_OK;
+}
+
+int kmx_ks_out_words(int len_f, int len_g, int coeff_bits, unsigned flags) {
+  KsPlan p;
+  int rc = make_plan(p, 1, 1, len_f, len_g, coeff_bits, 0, flags);
+  return rc ? rc : p.out_words_min;
+}
+
+size_t kmx_ks_workspace_bytes(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags) {
+  KsPlan p;
+  if (make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags)) return 0;
+  return p.total;
+}
+
+int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits, const uint32_t* f,
+               const uint32_t* g, int in_words, uint32_t* h, int out_words, void* workspace,
+               size_t ws_bytes, unsigned flags, void* stream) {
+  KsPlan p;
+  int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, in_words, flags);
+  if (rc) return rc;
+  return run_plan(p, f, g, h, out_words, workspace, ws_bytes, (cudaStream_t)stream);
+}
+
+int kmx_ws_status(void* workspace, void* stream) {
+  uint32_t fl = 0;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (cudaMemcpyAsync(&fl, workspace, 4, cudaMemcpyDeviceToHost, st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess) return KMX_ECUDA;
+  if (fl) cudaMemsetAsync(workspace, 0, 4, st);
+  return status_from_flag(fl);
+}
+
+int kmx_ws_limb_products(void* workspace, int variant, int batch, int len_f, int len_g, int coeff_bits,
+                         unsigned flags, uint64_t* out, void* stream) {
+  KsPlan p;
+  int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);
+  if (rc) return rc;
+  std::vector<uint32_t> meta((size_t)batch * p.P * 4);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!meta.empty()) {
+    if (cudaMemcpyAsync(meta.data(), (char*)workspace + p.off_meta, meta.size() * 4, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return KMX_ECUDA;
+    if (cudaStreamSynchronize(st) != cudaSuccess) return KMX_ECUDA;
+  }
+  uint64_t tot = 0;
+  for (int pr = 0; pr < batch; pr++)
+    for (int s = 0; s < p.P; s++) {
+      const uint64_t bf = meta[(size_t)pr * 4 * p.P + 2 * s + 1];
+      const uint64_t bg = meta[(size_t)pr * 4 * p.P + 2 * (p.P + s) + 1];
+      tot += ((bf + 63) / 64) * ((bg + 63) / 64);
+    }
+  *out = tot;
+  return KMX_OK;
+}
+
+int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits, const uint32_t* f,
+                    const uint32_t* g, int in_words, uint32_t* h, int out_words, unsigned flags,
+                    uint64_t* limb_products64) {
+  KsPlan p;
+  int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, in_words, flags);
+  if (rc) return rc;
+  if (out_words < p.out_words_min) return KMX_EINVAL;
+  HostCtx* c = host_ctx(&rc);
+  if (!c) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+  const size_t fb = (size_t)batch * len_f * p.in_words * 4, gb = (size_t)batch * len_g * p.in_words * 4;
+  const size_t hb = (size_t)batch * p.out_len * out_words * 4;
+  if ((rc = ensure(*c, 0, fb + gb + 256))) return rc;
+  if ((rc = ensure(*c, 1, hb))) return rc;
+  if ((rc = ensure(*c, 2, p.total))) return rc;
+  uint32_t* df = (uint32_t*)c->buf[0];
+  uint32_t* dg = (uint32_t*)((char*)c->buf[0] + align256(fb));
+  if (batch == 0) return KMX_OK;
+  if (cudaMemcpyAsync(df, f, fb, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMemcpyAsync(dg, g, gb, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  rc = run_plan(p, df, dg, (uint32_t*)c->buf[1], out_words, c->buf[2], c->cap[2], c->st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(h, c->buf[1], hb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
+  rc = kmx_ws_status(c->buf[2], c->st);
+  if (rc == KMX_OK && limb_products64)
+    rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, coeff_bits, flags, limb_products64, c->st);
+  return rc;
+}
+
+size_t kmx_reconstruct_workspace_bytes(int batch, int count, int dwords) {
+  if (batch < 0 || count < 1 || dwords < 1) return 0;
+  return 256 + (size_t)batch * 2 * (count + 1) * dwords * 4;
+}
+
+int kmx_reconstruct(int batch, int count, int width_bits, const uint32_t* fwd, const uint32_t* rev, int dwords,
+                    uint32_t* h, int hwords, void* workspace, size_t ws_bytes, uint8_t* carries, void* stream) {
+  // The reconstruction kernel reads both streams from one digit buffer; the
+  // standalone entry takes them as two arrays, so stage them in the
+  // workspace: [batch][2][count+1][dwords] plus the error word.
+  if (batch < 0 || count < 1 || width_bits < 1 || dwords < (width_bits + 31) / 32 || dwords > 17 ||
+      hwords < (2 * width_bits + 31) / 32)
+    return KMX_EINVAL;
+  const size_t slot = (size_t)(count + 1) * dwords;
+  const size_t need = 256 + (size_t)batch * 2 * slot * 4;
+  if (ws_bytes < need) return KMX_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* err = (uint32_t*)workspace;
+  uint32_t* db = (uint32_t*)((char*)workspace + 256);
+  g_launches = 0;
+  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMemcpy2DAsync(db, 2 * slot * 4, fwd, slot * 4, slot * 4, batch, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return KMX_ECUDA;
+  if (cudaMemcpy2DAsync(db + slot, 2 * slot * 4, rev, slot * 4, slot * 4, batch, cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+    return KMX_ECUDA;
+  ReconArgs ra;
+  memset(&ra, 0, sizeof ra);
+  ra.s[0] = ReconStream{0, 1, count, 0, 1};
+  ra.ns = 1; ra.batch = batch; ra.W = width_bits;
+  ra.dbuf = db; ra.dwords = dwords; ra.dslot_stride = (long long)slot; ra.dslots_pair = 2;
+  ra.h = h; ra.out_words = hwords; ra.h_pair_stride = (long long)count * hwords; ra.err = err;
+  ra.carries = carries;
+  cudaError_t e = launch_recon(ra, st);
+  g_launches = 1;
+  return cuda_rc(e);
+}
+
+int kmx_reconstruct_host(int batch, int count, int width_bits, const uint32_t* fwd, const uint32_t* rev,
+                         int dwords, uint32_t* h, int hwords, uint8_t* carries) {
+  if (batch < 0 || count < 1 || dwords < 1 || hwords < 1) return KMX_EINVAL;
+  if (batch == 0) return KMX_OK;
+  int rc;
+  HostCtx* c = host_ctx(&rc);
+  if (!c) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+  const size_t db = (size_t)batch * (count + 1) * dwords * 4;
+  const size_t hb = (size_t)batch * count * hwords * 4;
+  const size_t cb = (size_t)batch * (2 * count + 1);
+  const size_t wsb = kmx_reconstruct_workspace_bytes(batch, count, dwords);
+  if ((rc = ensure(*c, 0, 2 * align256(db) + align256(cb)))) return rc;
+  if ((rc = ensure(*c, 1, hb))) return rc;
+  if ((rc = ensure(*c, 2, wsb))) return rc;
+  uint32_t* dfw = (uint32_t*)c->buf[0];
+  uint32_t* drv = (uint32_t*)((char*)c->buf[0] + align256(db));
+  uint8_t* dca = (uint8_t*)((char*)c->buf[0] + 2 * align256(db));
+  if (cudaMemcpyAsync(dfw, fwd, db, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMemcpyAsync(drv, rev, db, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  rc = kmx_reconstruct(batch, count, width_bits, dfw, drv, dwords, (uint32_t*)c->buf[1], hwords, c->buf[2],
+                       c->cap[2], carries ? dca : nullptr, c->st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(h, c->buf[1], hb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
+  if (carries && cudaMemcpyAsync(carries, dca, cb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
+  return kmx_ws_status(c->buf[2], c->st);
+}
+
+double kmx_imad_peak(int iters) { return measure_imad_peak(iters > 0 ? iters : 4096); }
+
+const char* kmx_error_string(int code) {
+  switch (code) {
+    case KMX_OK: return "ok";
+    case KMX_EINVAL: return "invalid argument (ValueError)";
+    case KMX_ERECON: return "overlapped digit streams are inconsistent (ReconstructionError)";
+    case KMX_EINEXACT: return "inexact halving/shift or value does not fit its digits (ValueError)";
+    case KMX_ECUDA: return "CUDA error";
+    case KMX_ENOMEM: return "device out of memory";
+    default: return "unknown error";
+  }
+}
+
+int kmx_last_launch_count(void) { return g_launches; }
+
+}  // extern "C"

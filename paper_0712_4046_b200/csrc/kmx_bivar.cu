@@ -1,0 +1,377 @@
+// Bivariate R[x,y] -> R[x] reductions over R = Z (bipoly.py:177-278).
+//
+//   k_beval    evaluation: y-chunks concatenated at a spacing, optionally in
+//              reversed chunk order and/or with alternating signs
+//              (_concat_chunks, bipoly.py:128-143)
+//   k_conv     batched univariate products in Z[x] (the UniMul plug-in,
+//              bipoly.py:23, default uni_schoolbook oracle.py:58-69): int32 x
+//              int32 -> int64 column sums, one IMAD.WIDE per product term
+//   k_brecover half-sums, exact halving and the chunk overlap recovery
+//              (_overlap_recover bipoly.py:151-174; _split_chunks :146-148)
+#include <cstring>
+
+#include "../../include/kmx.h"
+#include "kmx_common.cuh"
+#include "kmx_internal.h"
+
+namespace kmx {
+
+// point descriptors: reverse / alternate flags per univariate product
+struct BPoint { int reverse, alternate; };
+
+__device__ __forceinline__ void point_flags(int variant, int pt, int& rev, int& alt) {
+  rev = 0; alt = 0;
+  if (variant == 2) rev = pt == 1;
+  else if (variant == 3) alt = pt == 1;
+  else if (variant == 4) { alt = pt & 1; rev = (pt >> 1) & 1; }
+}
+
+// evals: [batch][P][2][Lu] int32 (f then g)
+__global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, const int32_t* g, int32_t* ev) {
+  const int lx = p.lx, ly = p.ly, Lu = p.Lu, sp = p.spacing;
+  const long long total = (long long)p.batch * p.P * 2 * Lu;
+  for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
+       id += (long long)gridDim.x * blockDim.x) {
+    const int t = (int)(id % Lu);
+    long long r = id / Lu;
+    const int side = (int)(r % 2); r /= 2;
+    const int pt = (int)(r % p.P);
+    const long long pair = r / p.P;
+    int rev, alt;
+    point_flags(p.variant, pt, rev, alt);
+    const int32_t* c = (side ? g : f) + pair * lx * ly;
+    // chunk positions q = (rev ? ly-1-k : k) with q*sp <= t < q*sp + lx
+    int qlo = t - lx + 1 <= 0 ? 0 : (t - lx + 1 + sp - 1) / sp;
+    int qhi = t / sp;
+    if (qhi > ly - 1) qhi = ly - 1;
+    long long acc = 0;
+    for (int q = qlo; q <= qhi; q++) {
+      const int k = rev ? (ly - 1 - q) : q;
+      const int i = t - q * sp;
+      const long long v = c[(long long)i * ly + k];
+      acc += (alt && (k & 1)) ? -v : v;
+    }
+    ev[id] = (int32_t)acc;
+  }
+}
+
+// ---------------------------------------------------------------- k_conv
+// Same band geometry as k_mul: G threads x 8 consecutive columns; the
+// column sums stay in int64 registers (bounds checked on the host).
+struct ConvArgs {
+  const int32_t* A; long long a_stride;
+  const int32_t* B; long long b_stride;
+  int L;                  // operand length (both)
+  int64_t* P; long long p_stride;
+  int nprod, nbands, G, TI;
+};
+
+__global__ void __launch_bounds__(MUL_THREADS) k_conv(ConvArgs a) {
+  extern __shared__ __align__(16) int32_t cs[];
+  const int G = a.G, TI = a.TI;
+  const int C = G * MUL_R;
+  const int slots = MUL_THREADS / G;
+  const int tid = threadIdx.x;
+  const int slot = tid / G, tb = tid - slot * G;
+  const int slot_words = C + 2 * TI;
+  int32_t* as_ = cs + slot * slot_words;
+  int32_t* bs_ = as_ + TI;
+  const long long band = (long long)blockIdx.x * slots + slot;
+  const bool live = band < (long long)a.nprod * a.nbands;
+  const int z = live ? (int)(band / a.nbands) : 0;
+  const int bi = live ? (int)(band - (long long)z * a.nbands) : 0;
+  const int k0 = bi * C;
+  const int32_t* A = a.A + (long long)z * a.a_stride;
+  const int32_t* B = a.B + (long long)z * a.b_stride;
+  const int L = a.L;
+  const int ilo = max(0, k0 - (L - 1));
+  const int ihi = min(L - 1, k0 + C - 1);
+  long long acc[MUL_R];
+#pragma unroll
+  for (int r = 0; r < MUL_R; r++) acc[r] = 0;
+  for (int i0 = ilo; i0 <= ihi; i0 += TI) {
+    for (int x = tb; x < TI; x += G) {
+      const int i = i0 + x;
+      as_[x] = (live && i <= ihi) ? A[i] : 0;
+    }
+    const int bbase = k0 - i0 - TI + 1;
+    for (int x = tb; x < C + TI; x += G) {
+      const int j = bbase + x;
+      bs_[x] = (live && j >= 0 && j < L) ? B[j] : 0;
+    }
+    __syncthreads();
+    const int base0 = tb * MUL_R + TI - 8;
+    int32_t w[16];
+    {
+      const int4* p = reinterpret_cast<const int4*>(bs_ + base0);
+      int4 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
+      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
+      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
+      w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
+      w[12] = q3.x; w[13] = q3.y; w[14] = q3.z; w[15] = q3.w;
+    }
+    const int nu = TI >> 3;
+    for (int u = 0; u < nu; u++) {
+      const int4* ap = reinterpret_cast<const int4*>(as_ + 8 * u);
+      const int4 a0 = ap[0], a1 = ap[1];
+      const int32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+#pragma unroll
+      for (int v = 0; v < 8; v++) {
+#pragma unroll
+        for (int r = 0; r < MUL_R; r++) acc[r] += (long long)av[v] * w[7 + r - v];
+      }
+      if (u + 1 < nu) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) w[8 + j] = w[j];
+        const int4* p = reinterpret_cast<const int4*>(bs_ + base0 - 8 * (u + 1));
+        const int4 b0 = p[0], b1 = p[1];
+        w[0] = b0.x; w[1] = b0.y; w[2] = b0.z; w[3] = b0.w;
+        w[4] = b1.x; w[5] = b1.y; w[6] = b1.z; w[7] = b1.w;
+      }
+    }
+    __syncthreads();
+  }
+  if (live) {
+    int64_t* dst = a.P + (long long)z * a.p_stride + k0 + tb * MUL_R;
+    const int kmax = 2 * L - 1;
+#pragma unroll
+    for (int r = 0; r < MUL_R; r++)
+      if (k0 + tb * MUL_R + r < kmax) dst[r] = acc[r];
+  }
+}
+
+// ------------------------------------------------------------ k_brecover
+// One CTA per pair.  prods: [pair][P][p_stride] int64 (2Lu-1 valid).
+// h: [pair][2lx-1][2ly-1] int64.
+__device__ __forceinline__ long long halve(long long v, uint32_t* err) {
+  if (v & 1) raise_err(err, ERR_INEXACT);  // bipoly.py:47-50
+  return v >> 1;
+}
+
+// lanes t < min(sp, cl): sequential over chunks, chunk k -> output column
+// y = ybase + k*ystep.  fwd(x) / rev(x) fetch the recovered-sum vectors.
+template <class FF, class RF>
+__device__ void overlap_recover(int count, int sp, int cl, int ybase, int ystep, int lx2, int ly2,
+                                int64_t* H, FF fwd, RF rev) {
+  const int low = min(sp, cl);
+  const int ov = cl > sp ? cl - sp : 0;
+  for (int t = threadIdx.x; t < low; t += blockDim.x) {
+    long long hi_prev = 0, lo_prev = 0;  // high_{k-1}[t], low_{k-1}[t]
+    for (int k = 0; k < count; k++) {
+      long long lo = fwd((long long)k * sp + t);
+      if (t < ov) lo -= hi_prev;
+      long long hi = 0;
+      if (t < ov) hi = rev((long long)(count - 1 - k) * sp + sp + t) - lo_prev;
+      const int y = ybase + k * ystep;
+      H[(long long)t * ly2 + y] = lo;
+      if (t < ov) H[(long long)(sp + t) * ly2 + y] = hi;
+      hi_prev = hi;
+      lo_prev = lo;
+    }
+  }
+  (void)lx2;
+}
+
+__global__ void __launch_bounds__(128) k_brecover(BivarPlan p, const int64_t* prods, long long p_stride,
+                                                  int64_t* h, uint32_t* err) {
+  const int pair = blockIdx.x;
+  const int lx = p.lx, ly = p.ly;
+  const int lx2 = 2 * lx - 1, ly2 = 2 * ly - 1;
+  const int64_t* pr = prods + (long long)pair * p.P * p_stride;
+  int64_t* H = h + (long long)pair * lx2 * ly2;
+  if (p.variant == 1) {  // bipoly.py:177-188: split at spacing 2lx-1
+    const int sp = 2 * lx - 1;
+    for (int id = threadIdx.x; id < lx2 * ly2; id += blockDim.x) {
+      const int i = id / ly2, j = id - i * ly2;
+      H[id] = pr[(long long)j * sp + i];
+    }
+  } else if (p.variant == 3) {  // bipoly.py:209-232
+    const int64_t* pp = pr;
+    const int64_t* pn = pr + p_stride;
+    for (int id = threadIdx.x; id < lx2 * ly2; id += blockDim.x) {
+      const int i = id / ly2, y = id - i * ly2;
+      const int j = y >> 1;
+      long long v;
+      if ((y & 1) == 0) {
+        const long long t = 2LL * lx * j + i;
+        v = halve(pp[t] + pn[t], err);
+      } else {
+        const long long t = 2LL * lx * j + i + lx;  // odd_vec = (...)[lx:]
+        v = halve(pp[t] - pn[t], err);
+      }
+      H[id] = v;
+    }
+  } else if (p.variant == 2) {  // bipoly.py:191-206
+    const int64_t* pf = pr;
+    const int64_t* pv = pr + p_stride;
+    overlap_recover(2 * ly - 1, lx, 2 * lx - 1, 0, 1, lx2, ly2, H,
+                    [&](long long x) { return (long long)pf[x]; },
+                    [&](long long x) { return (long long)pv[x]; });
+  } else {  // bipoly.py:235-278
+    const int n = p.n4;
+    const int64_t* pp = pr;
+    const int64_t* pn = pr + p_stride;
+    const int64_t* rp = pr + 2 * p_stride;
+    const int64_t* rn = pr + 3 * p_stride;
+    overlap_recover(ly, 2 * n, 2 * lx - 1, 0, 2, lx2, ly2, H,
+                    [&](long long x) { return halve(pp[x] + pn[x], err); },
+                    [&](long long x) { return halve(rp[x] + rn[x], err); });
+    if (ly > 1)
+      overlap_recover(ly - 1, 2 * n, 2 * lx - 1, 1, 2, lx2, ly2, H,
+                      [&](long long x) { return halve(pp[x + n] - pn[x + n], err); },
+                      [&](long long x) { return halve(rp[x + n] - rn[x + n], err); });
+  }
+}
+
+cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h, int32_t* evals,
+                         int64_t* prods, uint32_t* err, cudaStream_t st, int* nlaunch) {
+  *nlaunch = 0;
+  const long long ne = (long long)p.batch * p.P * 2 * p.Lu;
+  int grid = (int)std::min<long long>((ne + 255) / 256, 148LL * 32);
+  if (grid < 1) grid = 1;
+  k_beval<<<grid, 256, 0, st>>>(p, f, g, evals);
+  (*nlaunch)++;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  // convolution geometry
+  const int mp = 2 * p.Lu - 1;
+  int need = (mp + MUL_R - 1) / MUL_R, G = 1;
+  while (G < need && G < MUL_THREADS) G <<= 1;
+  const int C = G * MUL_R;
+  const int nbands = (mp + C - 1) / C;
+  int TI = (p.Lu + 7) & ~7;
+  TI = TI < 8 ? 8 : (TI > 128 ? 128 : TI);
+  const long long ps = (long long)nbands * C;
+  ConvArgs ca;
+  ca.A = evals; ca.a_stride = 2LL * p.Lu;
+  ca.B = evals + p.Lu; ca.b_stride = 2LL * p.Lu;
+  ca.L = p.Lu;
+  ca.P = prods; ca.p_stride = ps;
+  ca.nprod = p.batch * p.P; ca.nbands = nbands; ca.G = G; ca.TI = TI;
+  const int slots = MUL_THREADS / G;
+  const long long nbt = (long long)ca.nprod * nbands;
+  const int cgrid = (int)((nbt + slots - 1) / slots);
+  const size_t smem = (size_t)slots * (C + 2 * TI) * 4;
+  if (smem > 48 * 1024) {
+    e = cudaFuncSetAttribute(k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_conv<<<cgrid, MUL_THREADS, smem, st>>>(ca);
+  (*nlaunch)++;
+  if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err);
+  (*nlaunch)++;
+  return cudaGetLastError();
+}
+
+}  // namespace kmx
+
+// ------------------------------------------------------------------ C ABI
+using namespace kmx;
+
+namespace {
+int bks_plan(BivarPlan& p, int variant, int batch, int lx, int ly, int coeff_bits) {
+  if (variant < 1 || variant > 4 || batch < 0 || lx < 1 || ly < 1 || coeff_bits < 1 || coeff_bits > 30)
+    return KMX_EINVAL;
+  p.variant = variant; p.lx = lx; p.ly = ly; p.batch = batch;
+  p.n4 = (lx + 1) / 2;
+  switch (variant) {
+    case 1: p.P = 1; p.spacing = 2 * lx - 1; p.Lu = (2 * lx - 1) * (ly - 1) + lx; break;
+    case 2: p.P = 2; p.spacing = lx; p.Lu = lx * ly; break;
+    case 3: p.P = 2; p.spacing = lx; p.Lu = lx * ly; break;
+    default: p.P = 4; p.spacing = p.n4; p.Lu = p.n4 * (ly - 1) + lx; break;
+  }
+  // |eval| < 2^(cb + [four-point overlap]); every univariate product
+  // coefficient (and the half-sum numerators) must stay inside int64
+  const int eb = coeff_bits + (variant == 4 ? 1 : 0);
+  if (eb > 31) return KMX_EINVAL;
+  double bound = (double)p.Lu * (double)(1ULL << eb) * (double)(1ULL << eb) * 2.0;
+  if (bound >= 9.2e18) return KMX_EINVAL;
+  return KMX_OK;
+}
+
+size_t align256b(size_t x) { return (x + 255) & ~(size_t)255; }
+
+void bks_layout(const BivarPlan& p, size_t* off_ev, size_t* off_pr, size_t* total) {
+  const int mp = 2 * p.Lu - 1;
+  int need = (mp + MUL_R - 1) / MUL_R, G = 1;
+  while (G < need && G < MUL_THREADS) G <<= 1;
+  const int C = G * MUL_R;
+  const long long ps = (long long)((mp + C - 1) / C) * C;
+  size_t o = 256;
+  *off_ev = o;
+  o = align256b(o + (size_t)p.batch * p.P * 2 * p.Lu * 4);
+  *off_pr = o;
+  o = align256b(o + (size_t)p.batch * p.P * ps * 8);
+  *total = o;
+}
+}  // namespace
+
+extern "C" {
+
+size_t kmx_bks_workspace_bytes(int variant, int batch, int lx, int ly) {
+  BivarPlan p;
+  if (bks_plan(p, variant, batch, lx, ly, 1)) return 0;
+  size_t a, b, t;
+  bks_layout(p, &a, &b, &t);
+  return t;
+}
+
+int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits, const int32_t* f, const int32_t* g,
+                int64_t* h, void* workspace, size_t ws_bytes, void* stream) {
+  BivarPlan p;
+  int rc = bks_plan(p, variant, batch, lx, ly, coeff_bits);
+  if (rc) return rc;
+  size_t oe, op, tot;
+  bks_layout(p, &oe, &op, &tot);
+  if (ws_bytes < tot) return KMX_EINVAL;
+  if (batch == 0) return KMX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  char* w = (char*)workspace;
+  uint32_t* err = (uint32_t*)w;
+  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return KMX_ECUDA;
+  int nl = 0;
+  cudaError_t e = launch_bivar(p, f, g, h, (int32_t*)(w + oe), (int64_t*)(w + op), err, st, &nl);
+  g_launches = nl;
+  return e == cudaSuccess ? KMX_OK : KMX_ECUDA;
+}
+
+int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits, const int32_t* f, const int32_t* g,
+                     int64_t* h) {
+  BivarPlan p;
+  int rc = bks_plan(p, variant, batch, lx, ly, coeff_bits);
+  if (rc) return rc;
+  size_t oe, op, tot;
+  bks_layout(p, &oe, &op, &tot);
+  const size_t fb = (size_t)batch * lx * ly * 4;
+  const size_t hb = (size_t)batch * (2 * lx - 1) * (2 * ly - 1) * 8;
+  if (batch == 0) return KMX_OK;
+  void *df = nullptr, *dh = nullptr, *dw = nullptr;
+  cudaStream_t st = nullptr;
+  rc = KMX_ECUDA;
+  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMalloc(&df, 2 * fb + 256) != cudaSuccess || cudaMalloc(&dh, hb) != cudaSuccess ||
+      cudaMalloc(&dw, tot) != cudaSuccess) {
+    rc = KMX_ENOMEM;
+    goto done;
+  }
+  {
+    int32_t* dF = (int32_t*)df;
+    int32_t* dG = (int32_t*)((char*)df + ((fb + 255) & ~(size_t)255));
+    if (cudaMemcpyAsync(dF, f, fb, cudaMemcpyHostToDevice, st) != cudaSuccess) goto done;
+    if (cudaMemcpyAsync(dG, g, fb, cudaMemcpyHostToDevice, st) != cudaSuccess) goto done;
+    rc = kmx_bks_mul(variant, batch, lx, ly, coeff_bits, dF, dG, (int64_t*)dh, dw, tot, st);
+    if (rc) goto done;
+    if (cudaMemcpyAsync(h, dh, hb, cudaMemcpyDeviceToHost, st) != cudaSuccess) { rc = KMX_ECUDA; goto done; }
+    rc = kmx_ws_status(dw, st);
+  }
+done:
+  cudaStreamSynchronize(st);
+  if (df) cudaFree(df);
+  if (dh) cudaFree(dh);
+  if (dw) cudaFree(dw);
+  cudaStreamDestroy(st);
+  return rc;
+}
+
+}  // extern "C"

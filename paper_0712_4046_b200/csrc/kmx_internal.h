@@ -1,0 +1,120 @@
+// Internal launch interface between the C-ABI layer (kmx_api.cu) and the
+// kernels (kmx_ks.cu, kmx_bivar.cu).  Host-visible structs only.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace kmx {
+
+// ------------------------------------------------------------------ pack
+// One packed operand family: the value of a coefficient vector at +-2^N or
+// +-2^-N (pack.py:79-110).  kind: 0 = pack, 1 = pack_negated,
+// 2 = pack_reversed, 3 = pack_negated_reversed.
+struct PackOp {
+  const uint32_t* coeffs;     // pair 0's coefficients; pair p at + p*coeff_pair_stride
+  long long coeff_pair_stride;
+  int len;
+  int kind;
+  uint32_t* out;              // pair 0's operand; pair p at + p*out_pair_stride
+  long long out_pair_stride;
+  uint32_t* meta;             // pair 0's [sign, bitlen]; pair p at + p*meta_pair_stride
+  long long meta_pair_stride;
+  int m;                      // limbs of this operand
+  int validate;               // check 0 <= c < 2^b on this operand's coefficients
+};
+struct PackArgs {
+  PackOp op[8];
+  int nops;
+  int N;                      // evaluation width (bits)
+  int b;                      // coefficient bound (bits)
+  int in_words;
+  int bias;                   // signed inputs: add 2^(b-1) (bias lift)
+  uint32_t* err;
+};
+
+// -------------------------------------------------------------- multiply
+struct MulArgs {
+  const uint32_t* A; long long a_stride; int ma;  // product z: A + z*a_stride
+  const uint32_t* B; long long b_stride; int mb;
+  uint32_t* P; long long p_stride;                // digits, p_stride >= nbands*C
+  unsigned long long* spill;                      // [z][nbands][2]
+  int nprod, nbands, G, TI;
+};
+constexpr int MUL_THREADS = 128;
+constexpr int MUL_R = 8;
+
+// ---------------------------------------------------------------- finish
+// One output digit stream of one pair: digits of (P + qsign*sgn(Q)*|Q|) >> off
+// at width W (the half-sum / half-difference and the exact shifts of
+// ksint.py:270-273 and :320-335, and the unpacks of _unpack_ints).
+struct Stream {
+  int zP, zQ;                 // product slots inside a pair
+  int qsign;                  // 0: P alone; +1 / -1: P + / - signed Q
+  int qmeta;                  // operand-meta slot index (f side) of Q's first operand
+  long long off;              // first bit of digit 0
+  int W;                      // digit width in bits
+  int cnt;                    // number of digits (all higher bits must be zero)
+  int mode;                   // 0: coefficient output, 1: digit buffer
+  int pos0, pstride;          // mode 0: h[pair][pos0 + j*pstride]
+  int dslot;                  // mode 1: digit-buffer slot inside the pair
+  int reversed;               // mode 1: store digit j at index cnt-1-j
+};
+struct FinishArgs {
+  Stream s[4];
+  int ns;
+  const uint32_t* P; long long p_stride; int mp; int nprod_pair;
+  const unsigned long long* spill; int nbands; int band_cols;
+  const uint32_t* meta; int meta_per_pair;        // 2 words per operand
+  int mf_slot_stride;                             // operand meta: f ops at [sub], g ops at [P+sub]
+  uint32_t* h; int out_words; long long h_pair_stride;
+  uint32_t* dbuf; int dwords; long long dslot_stride; int dslots_pair;
+  uint32_t* err;
+};
+constexpr int FIN_THREADS = 256;
+constexpr int FIN_HALO = 32;
+
+// --------------------------------------------------------- reconstruction
+struct ReconStream { int fslot, rslot, count, pos0, pstride; };
+struct ReconArgs {
+  ReconStream s[2];
+  int ns;
+  int batch;
+  int W;
+  const uint32_t* dbuf; int dwords; long long dslot_stride; int dslots_pair;
+  uint32_t* h; int out_words; long long h_pair_stride;
+  uint8_t* carries;           // optional [batch*ns][2*count+1]: fwd carries, rev carries
+  uint32_t* err;
+};
+
+// ---------------------------------------------------------- signed (bias)
+struct BiasArgs {
+  const uint32_t* f; const uint32_t* g; int lf, lg, b;
+  uint32_t* h; int out_words;
+  unsigned long long* scratch;  // [batch][lf+lg+2]
+  int batch;
+};
+
+// kernels launched by the last C-ABI call on this thread (bench gpu_launches)
+extern thread_local int g_launches;
+
+// launchers (return cudaError_t of the launch)
+cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st);
+cudaError_t launch_mul(const MulArgs& a, cudaStream_t st);
+cudaError_t launch_finish(const FinishArgs& a, int batch, cudaStream_t st);
+cudaError_t launch_recon(const ReconArgs& a, cudaStream_t st);
+cudaError_t launch_bias(const BiasArgs& a, cudaStream_t st);
+double measure_imad_peak(int iters);
+
+// ---------------------------------------------------------------- bivariate
+struct BivarPlan {
+  int variant, lx, ly, batch;
+  int P;          // univariate products per pair
+  int Lu;         // univariate operand length
+  int spacing;    // chunk spacing in the evaluation
+  int n4;         // four-point half length
+};
+cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h,
+                         int32_t* evals, int64_t* prods, uint32_t* err, cudaStream_t st,
+                         int* nlaunch);
+
+}  // namespace kmx

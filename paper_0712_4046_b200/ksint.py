@@ -1,0 +1,109 @@
+"""Drop-in integer Kronecker substitution entry points, computed on the GPU.
+
+Mirrors pkg/src/kronmul/ksint.py: same names, signatures, return types and
+exceptions; every product runs through libkmx.so (pack -> multiply ->
+finish -> reconstruct kernels on sm_100a).  There is no CPU fallback.
+
+  derive_params          ksint.py:82-98 (host scalars, via kmx_ks_params)
+  ks1_mul .. ks4_mul     ksint.py:219-348   (kmx_ks_mul_host)
+  reconstruct_overlapped ksint.py:182-195   (kmx_reconstruct_host)
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from ._lib import ReconstructionError, check, lib
+from .kstypes import CoeffVec, KsParams, MulConfig, MulStats, OverlapDigits
+from .words import ints_to_words, words_to_ints
+
+__all__ = ["KsParams", "OverlapDigits", "ReconstructionError", "derive_params", "ks1_mul",
+           "ks2_mul", "ks3_mul", "ks4_mul", "reconstruct_overlapped"]
+
+
+def derive_params(len_f: int, len_g: int, coeff_bits: int) -> KsParams:
+    """Chunk widths for inputs of the given lengths and bit bound
+    (ksint.py:82-98)."""
+    if len_f < 1 or len_g < 1:
+        raise ValueError("polynomial lengths must be >= 1")
+    if coeff_bits < 1:
+        raise ValueError("coefficient bit bound must be >= 1")
+    out = (ctypes.c_int64 * 8)()
+    check(lib().kmx_ks_params(1, len_f, len_g, coeff_bits, 0, out), "derive_params")
+    e, n1, n2, n4 = int(out[0]), int(out[1]), int(out[2]), int(out[3])
+    return KsParams(len_f, len_g, coeff_bits, e, n1, n2, n4)
+
+
+def _ks(variant: int, f: CoeffVec, g: CoeffVec, stats: MulStats | None) -> CoeffVec:
+    b = max(f.width_bound_bits, g.width_bound_bits)
+    words = (b + 31) // 32
+    lf, lg = len(f.coeffs), len(g.coeffs)
+    fw = ints_to_words(f.coeffs, words)
+    gw = ints_to_words(g.coeffs, words)
+    ow = lib().kmx_ks_out_words(lf, lg, b, 0)
+    if ow < 0:
+        check(ow, f"ks{variant}_mul")
+    h = np.zeros((lf + lg - 1, ow), dtype=np.uint32)
+    lp = ctypes.c_uint64(0)
+    rc = lib().kmx_ks_mul_host(variant, 1, lf, lg, b, _lib.ptr(fw), _lib.ptr(gw), words,
+                               _lib.ptr(h), ow, 0, ctypes.byref(lp) if stats is not None else None)
+    check(rc, f"ks{variant}_mul")
+    if stats is not None:
+        stats.limb_products += int(lp.value)
+    return CoeffVec(tuple(words_to_ints(h)), 2 * b + _e(lf, lg))
+
+
+def _e(lf: int, lg: int) -> int:
+    return (min(lf, lg) - 1).bit_length()
+
+
+def ks1_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
+            config: MulConfig | None = None) -> CoeffVec:
+    """Standard substitution: one full-width product (ksint.py:219-226)."""
+    return _ks(1, f, g, stats)
+
+
+def ks2_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
+            config: MulConfig | None = None, parallel: bool = False) -> CoeffVec:
+    """Reciprocal variant: forward and reversed half-width products, carry
+    reconstruction (ksint.py:229-247).  ``parallel`` is accepted for
+    signature compatibility: the sub-products always run concurrently on the
+    GPU, with bit-identical results."""
+    return _ks(2, f, g, stats)
+
+
+def ks3_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
+            config: MulConfig | None = None, parallel: bool = False) -> CoeffVec:
+    """Negated variant: products at +-2^N, half-sum / half-difference
+    (ksint.py:257-279)."""
+    return _ks(3, f, g, stats)
+
+
+def ks4_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
+            config: MulConfig | None = None, parallel: bool = False) -> CoeffVec:
+    """Four-point variant: quarter-width products at +-2^N and +-2^-N, even/odd
+    split, two overlap reconstructions; KS1 fallback when the bound is not
+    certified (ksint.py:289-348)."""
+    return _ks(4, f, g, stats)
+
+
+def reconstruct_overlapped(d: OverlapDigits, *, with_carries: bool = False):
+    """Recover the coefficients behind two overlapped packings
+    (ksint.py:182-195), on the GPU."""
+    w = d.width_bits
+    count = d.coeff_count
+    dw = (w + 31) // 32
+    fw = ints_to_words(d.forward_digits, dw)
+    rw = ints_to_words(d.reversed_digits, dw)
+    hw = (2 * w + 31) // 32
+    h = np.zeros((count, hw), dtype=np.uint32)
+    car = np.zeros(2 * count + 1, dtype=np.uint8) if with_carries else None
+    rc = lib().kmx_reconstruct_host(1, count, w, _lib.ptr(fw), _lib.ptr(rw), dw, _lib.ptr(h), hw,
+                                    _lib.ptr(car) if car is not None else None)
+    check(rc, "reconstruct_overlapped")
+    out = CoeffVec(tuple(words_to_ints(h)), 2 * w)
+    if with_carries:
+        return out, [int(x) for x in car[:count + 1]], [int(x) for x in car[count + 1:]]
+    return out
