@@ -137,6 +137,14 @@ const char* kmx_error_string(int code);
  * this thread (for the bench's gpu_launches count). */
 int kmx_last_launch_count(void);
 
+/* Per-kernel CUDA-event timing of kmx_ks_mul on the calling thread (events
+ * recorded on the caller's stream around each launch).  kmx_prof_read
+ * synchronises on the last call's events and writes the durations in ms to
+ * ms[0..4] = pack, multiply, finish, reconstruct, bias (0 if not launched);
+ * returns the number of kernels timed. */
+void kmx_prof_enable(int on);
+int kmx_prof_read(float* ms, int nslots);
+
 #ifdef __cplusplus
 }
 #endif

@@ -62,6 +62,8 @@ _SIGS = {
     "kmx_imad_peak": (ctypes.c_double, [_i]),
     "kmx_error_string": (ctypes.c_char_p, [_i]),
     "kmx_last_launch_count": (_i, []),
+    "kmx_prof_enable": (None, [_i]),
+    "kmx_prof_read": (_i, [ctypes.POINTER(ctypes.c_float), _i]),
 }
 
 EXPORTED_SYMBOLS = tuple(_SIGS)

@@ -78,6 +78,30 @@ struct KsPlan {
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// optional per-kernel CUDA-event timing of run_plan (kmx_prof_*):
+// slots 0 pack, 1 mul, 2 finish, 3 recon, 4 bias
+struct Prof {
+  bool on = false;
+  bool created = false;
+  cudaEvent_t ev[6][2];
+  bool used[6];
+};
+thread_local Prof g_prof;
+
+void prof_begin(int slot, cudaStream_t st) {
+  if (!g_prof.on) return;
+  if (!g_prof.created) {
+    for (int i = 0; i < 6; i++)
+      for (int j = 0; j < 2; j++) cudaEventCreate(&g_prof.ev[i][j]);
+    g_prof.created = true;
+  }
+  cudaEventRecord(g_prof.ev[slot][0], st);
+  g_prof.used[slot] = true;
+}
+void prof_end(int slot, cudaStream_t st) {
+  if (g_prof.on) cudaEventRecord(g_prof.ev[slot][1], st);
+}
+
 int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_words, unsigned flags) {
   memset(&p, 0, sizeof p);
   if (variant < 1 || variant > 4 || batch < 0 || lf < 1 || lg < 1 || b < 1) return KMX_EINVAL;
@@ -200,6 +224,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   if (out_words < p.out_words_min) return KMX_EINVAL;
   if (ws_bytes < p.total || (!ws && p.total)) return KMX_EINVAL;
   if (p.batch == 0) return KMX_OK;
+  for (int i = 0; i < 6; i++) g_prof.used[i] = false;
   char* w = (char*)ws;
   uint32_t* err = (uint32_t*)(w + p.off_err);
   uint32_t* meta = (uint32_t*)(w + p.off_meta);
@@ -227,7 +252,9 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     Gq.out = opg + (long long)s * p.mgs; Gq.out_pair_stride = (long long)p.P * p.mgs;
     Gq.meta = meta + 2 * (p.P + s); Gq.meta_pair_stride = 4LL * p.P; Gq.m = p.mg; Gq.validate = validate && s == 0;
   }
+  prof_begin(0, st);
   if ((e = launch_pack(pa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+  prof_end(0, st);
   g_launches++;
 
   MulArgs ma;
@@ -235,7 +262,9 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.B = opg; ma.b_stride = p.mgs; ma.mb = p.mg;
   ma.P = prod; ma.p_stride = p.ps; ma.spill = spill;
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
+  prof_begin(1, st);
   if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  prof_end(1, st);
   g_launches++;
 
   FinishArgs fa;
@@ -248,7 +277,9 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.h = h; fa.out_words = out_words; fa.h_pair_stride = (long long)p.out_len * out_words;
   fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = (long long)p.cnt_max * p.dwords;
   fa.dslots_pair = p.dslots; fa.err = err;
+  prof_begin(2, st);
   if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+  prof_end(2, st);
   g_launches++;
 
   if (p.nrs) {
@@ -260,14 +291,18 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     ra.dslots_pair = p.dslots;
     ra.h = h; ra.out_words = out_words; ra.h_pair_stride = (long long)p.out_len * out_words;
     ra.err = err;
+    prof_begin(3, st);
     if ((e = launch_recon(ra, st)) != cudaSuccess) return KMX_ECUDA;
+    prof_end(3, st);
     g_launches++;
   }
   if (p.sign) {
     BiasArgs ba;
     ba.f = f; ba.g = g; ba.lf = p.lf; ba.lg = p.lg; ba.b = p.b;
     ba.h = h; ba.out_words = out_words; ba.scratch = scr; ba.batch = p.batch;
+    prof_begin(4, st);
     if ((e = launch_bias(ba, st)) != cudaSuccess) return KMX_ECUDA;
+    prof_end(4, st);
     g_launches++;
   }
   return KMX_OK;
@@ -485,5 +520,19 @@ const char* kmx_error_string(int code) {
 }
 
 int kmx_last_launch_count(void) { return g_launches; }
+
+void kmx_prof_enable(int on) { g_prof.on = on != 0; }
+
+int kmx_prof_read(float* ms, int nslots) {
+  int n = 0;
+  for (int i = 0; i < nslots && i < 6; i++) {
+    ms[i] = 0.f;
+    if (!g_prof.on || !g_prof.created || !g_prof.used[i]) continue;
+    if (cudaEventSynchronize(g_prof.ev[i][1]) != cudaSuccess) return KMX_ECUDA;
+    if (cudaEventElapsedTime(&ms[i], g_prof.ev[i][0], g_prof.ev[i][1]) != cudaSuccess) return KMX_ECUDA;
+    n++;
+  }
+  return n;
+}
 
 }  // extern "C"
