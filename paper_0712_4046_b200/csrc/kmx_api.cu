@@ -155,17 +155,9 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
   p.mfs = (p.mf + 3) & ~3;
   p.mgs = (p.mg + 3) & ~3;
   p.mp = p.mf + p.mg;
-  // multiply geometry
-  {
-    int need = (p.mp + MUL_R - 1) / MUL_R, G = 1;
-    while (G < need && G < MUL_THREADS) G <<= 1;
-    p.G = G;
-    p.C = G * MUL_R;
-    p.nbands = (p.mp + p.C - 1) / p.C;
-    int ti = (p.mf + 7) & ~7;
-    p.TI = std::min(128, std::max(8, ti));
-    p.ps = (long long)p.nbands * p.C;
-  }
+  // multiply geometry (kmx_mul.cu): G = row split, C = band columns
+  mul_geometry(p.mf, p.mg, &p.G, &p.C, &p.nbands, &p.TI);
+  p.ps = (long long)p.nbands * p.C;
   // output streams (finish) and reconstructions
   const int k = p.out_len, n_even = (k + 1) / 2, n_odd = k / 2;
   auto S = [&](int i) -> Stream& { return p.st[i]; };

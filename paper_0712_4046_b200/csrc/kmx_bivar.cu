@@ -55,91 +55,6 @@ __global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, co
   }
 }
 
-// ---------------------------------------------------------------- k_conv
-// Same band geometry as k_mul: G threads x 8 consecutive columns; the
-// column sums stay in int64 registers (bounds checked on the host).
-struct ConvArgs {
-  const int32_t* A; long long a_stride;
-  const int32_t* B; long long b_stride;
-  int L;                  // operand length (both)
-  int64_t* P; long long p_stride;
-  int nprod, nbands, G, TI;
-};
-
-__global__ void __launch_bounds__(MUL_THREADS) k_conv(ConvArgs a) {
-  extern __shared__ __align__(16) int32_t cs[];
-  const int G = a.G, TI = a.TI;
-  const int C = G * MUL_R;
-  const int slots = MUL_THREADS / G;
-  const int tid = threadIdx.x;
-  const int slot = tid / G, tb = tid - slot * G;
-  const int slot_words = C + 2 * TI;
-  int32_t* as_ = cs + slot * slot_words;
-  int32_t* bs_ = as_ + TI;
-  const long long band = (long long)blockIdx.x * slots + slot;
-  const bool live = band < (long long)a.nprod * a.nbands;
-  const int z = live ? (int)(band / a.nbands) : 0;
-  const int bi = live ? (int)(band - (long long)z * a.nbands) : 0;
-  const int k0 = bi * C;
-  const int32_t* A = a.A + (long long)z * a.a_stride;
-  const int32_t* B = a.B + (long long)z * a.b_stride;
-  const int L = a.L;
-  const int ilo = max(0, k0 - (L - 1));
-  const int ihi = min(L - 1, k0 + C - 1);
-  long long acc[MUL_R];
-#pragma unroll
-  for (int r = 0; r < MUL_R; r++) acc[r] = 0;
-  for (int i0 = ilo; i0 <= ihi; i0 += TI) {
-    for (int x = tb; x < TI; x += G) {
-      const int i = i0 + x;
-      as_[x] = (live && i <= ihi) ? A[i] : 0;
-    }
-    const int bbase = k0 - i0 - TI + 1;
-    for (int x = tb; x < C + TI; x += G) {
-      const int j = bbase + x;
-      bs_[x] = (live && j >= 0 && j < L) ? B[j] : 0;
-    }
-    __syncthreads();
-    const int base0 = tb * MUL_R + TI - 8;
-    int32_t w[16];
-    {
-      const int4* p = reinterpret_cast<const int4*>(bs_ + base0);
-      int4 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-      w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-      w[12] = q3.x; w[13] = q3.y; w[14] = q3.z; w[15] = q3.w;
-    }
-    const int nu = TI >> 3;
-    for (int u = 0; u < nu; u++) {
-      const int4* ap = reinterpret_cast<const int4*>(as_ + 8 * u);
-      const int4 a0 = ap[0], a1 = ap[1];
-      const int32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-      for (int v = 0; v < 8; v++) {
-#pragma unroll
-        for (int r = 0; r < MUL_R; r++) acc[r] += (long long)av[v] * w[7 + r - v];
-      }
-      if (u + 1 < nu) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) w[8 + j] = w[j];
-        const int4* p = reinterpret_cast<const int4*>(bs_ + base0 - 8 * (u + 1));
-        const int4 b0 = p[0], b1 = p[1];
-        w[0] = b0.x; w[1] = b0.y; w[2] = b0.z; w[3] = b0.w;
-        w[4] = b1.x; w[5] = b1.y; w[6] = b1.z; w[7] = b1.w;
-      }
-    }
-    __syncthreads();
-  }
-  if (live) {
-    int64_t* dst = a.P + (long long)z * a.p_stride + k0 + tb * MUL_R;
-    const int kmax = 2 * L - 1;
-#pragma unroll
-    for (int r = 0; r < MUL_R; r++)
-      if (k0 + tb * MUL_R + r < kmax) dst[r] = acc[r];
-  }
-}
-
 // ------------------------------------------------------------ k_brecover
 // One CTA per pair.  prods: [pair][P][p_stride] int64 (2Lu-1 valid).
 // h: [pair][2lx-1][2ly-1] int64.
@@ -233,32 +148,18 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   (*nlaunch)++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  // convolution geometry
-  const int mp = 2 * p.Lu - 1;
-  int need = (mp + MUL_R - 1) / MUL_R, G = 1;
-  while (G < need && G < MUL_THREADS) G <<= 1;
-  const int C = G * MUL_R;
-  const int nbands = (mp + C - 1) / C;
-  int TI = (p.Lu + 7) & ~7;
-  TI = TI < 8 ? 8 : (TI > 128 ? 128 : TI);
-  const long long ps = (long long)nbands * C;
+  // univariate products (kmx_mul.cu)
+  int split, cw, nbands, tr;
+  mul_geometry(p.Lu, p.Lu, &split, &cw, &nbands, &tr);
+  const long long ps = (long long)nbands * cw;
   ConvArgs ca;
   ca.A = evals; ca.a_stride = 2LL * p.Lu;
   ca.B = evals + p.Lu; ca.b_stride = 2LL * p.Lu;
   ca.L = p.Lu;
   ca.P = prods; ca.p_stride = ps;
-  ca.nprod = p.batch * p.P; ca.nbands = nbands; ca.G = G; ca.TI = TI;
-  const int slots = MUL_THREADS / G;
-  const long long nbt = (long long)ca.nprod * nbands;
-  const int cgrid = (int)((nbt + slots - 1) / slots);
-  const size_t smem = (size_t)slots * (C + 2 * TI) * 4;
-  if (smem > 48 * 1024) {
-    e = cudaFuncSetAttribute(k_conv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_conv<<<cgrid, MUL_THREADS, smem, st>>>(ca);
+  ca.nprod = p.batch * p.P; ca.nbands = nbands; ca.G = split; ca.TI = tr;
+  if ((e = launch_conv(ca, st)) != cudaSuccess) return e;
   (*nlaunch)++;
-  if ((e = cudaGetLastError()) != cudaSuccess) return e;
   k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err);
   (*nlaunch)++;
   return cudaGetLastError();
@@ -293,11 +194,9 @@ int bks_plan(BivarPlan& p, int variant, int batch, int lx, int ly, int coeff_bit
 size_t align256b(size_t x) { return (x + 255) & ~(size_t)255; }
 
 void bks_layout(const BivarPlan& p, size_t* off_ev, size_t* off_pr, size_t* total) {
-  const int mp = 2 * p.Lu - 1;
-  int need = (mp + MUL_R - 1) / MUL_R, G = 1;
-  while (G < need && G < MUL_THREADS) G <<= 1;
-  const int C = G * MUL_R;
-  const long long ps = (long long)((mp + C - 1) / C) * C;
+  int split, cw, nbands, tr;
+  mul_geometry(p.Lu, p.Lu, &split, &cw, &nbands, &tr);
+  const long long ps = (long long)nbands * cw;
   size_t o = 256;
   *off_ev = o;
   o = align256b(o + (size_t)p.batch * p.P * 2 * p.Lu * 4);

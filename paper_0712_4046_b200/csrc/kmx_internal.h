@@ -33,15 +33,24 @@ struct PackArgs {
 };
 
 // -------------------------------------------------------------- multiply
+// G carries the row-split factor SPLIT (1, 2, 4): bands are CW = 256/SPLIT
+// columns wide, 8 bands per CTA; TI is the number of operand rows staged
+// per shared-memory chunk (TR).
 struct MulArgs {
   const uint32_t* A; long long a_stride; int ma;  // product z: A + z*a_stride
   const uint32_t* B; long long b_stride; int mb;
-  uint32_t* P; long long p_stride;                // digits, p_stride >= nbands*C
+  uint32_t* P; long long p_stride;                // digits, p_stride >= nbands*CW
   unsigned long long* spill;                      // [z][nbands][2]
   int nprod, nbands, G, TI;
 };
-constexpr int MUL_THREADS = 128;
-constexpr int MUL_R = 8;
+struct ConvArgs {
+  const int32_t* A; long long a_stride;
+  const int32_t* B; long long b_stride;
+  int L;                                          // operand length (both)
+  int64_t* P; long long p_stride;                 // 2L-1 int64 column sums
+  int nprod, nbands, G, TI;
+};
+void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr);
 
 // ---------------------------------------------------------------- finish
 // One output digit stream of one pair: digits of (P + qsign*sgn(Q)*|Q|) >> off
@@ -84,6 +93,7 @@ struct ReconArgs {
   uint32_t* h; int out_words; long long h_pair_stride;
   uint8_t* carries;           // optional [batch*ns][2*count+1]: fwd carries, rev carries
   uint32_t* err;
+  int rch;                    // steps per staged chunk (set by launch_recon)
 };
 
 // ---------------------------------------------------------- signed (bias)
@@ -100,6 +110,7 @@ extern thread_local int g_launches;
 // launchers (return cudaError_t of the launch)
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_mul(const MulArgs& a, cudaStream_t st);
+cudaError_t launch_conv(const ConvArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_recon(const ReconArgs& a, cudaStream_t st);
 cudaError_t launch_bias(const BiasArgs& a, cudaStream_t st);

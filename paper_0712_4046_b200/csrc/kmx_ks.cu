@@ -2,7 +2,7 @@
 //
 //   k_pack    evaluation of coefficient vectors at +-2^N, +-2^-N
 //             (pack.py:62-110 / bignat._pack_ints bignat.py:411-428)
-//   k_mul     independent multiprecision products (bignat.py:323-380)
+//   (k_mul / k_conv: kmx_mul.cu)
 //   k_finish  half-sum / half-difference, exact halving and shifts, digit
 //             extraction (ksint.py:219-279, :305-345; bignat.py:265-274,
 //             :310-317, :431-450)
@@ -155,154 +155,6 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs A) {
 
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   k_pack<<<batch * a.nops, 256, 0, st>>>(a);
-  return cudaGetLastError();
-}
-
-// ========================================================================
-// K2: batched schoolbook multiply, column bands.
-//
-// A band is C = G*8 consecutive product columns of one product; G threads
-// own 8 consecutive columns each and accumulate every a[i]*b[k-i] of those
-// columns in 96-bit registers (IMAD.WIDE.U32 + carry, see mac96).  Operand
-// tiles are staged in shared memory; the inner loop is register-blocked
-// 8 (rows) x 8 (columns): per 64 limb products it issues 2 broadcast
-// LDS.128 for a and 2 LDS.128 for the sliding b window.  Small products pack
-// several bands (one band = a whole product) into one CTA.  The epilogue
-// normalizes the band to 32-bit digits with a segmented carry-map scan and
-// writes the two-digit overflow past the band top as a "spill" that the
-// finish kernel folds in.
-// ========================================================================
-__global__ void __launch_bounds__(MUL_THREADS) k_mul(MulArgs a) {
-  extern __shared__ __align__(16) u32 smem[];
-  __shared__ u32 xs[3][MUL_THREADS];
-  __shared__ i64 sm_hi[MUL_THREADS];
-  __shared__ u32 sm_scan[MUL_THREADS / 32];
-  const int G = a.G, TI = a.TI;
-  const int C = G * MUL_R;
-  const int slots = MUL_THREADS / G;
-  const int tid = threadIdx.x;
-  const int slot = tid / G, tb = tid - slot * G;
-  const int slot_words = C + 2 * TI;
-  u32* as_ = smem + slot * slot_words;
-  u32* bs_ = as_ + TI;
-  const long long band = (long long)blockIdx.x * slots + slot;
-  const bool live = band < (long long)a.nprod * a.nbands;
-  const int z = live ? (int)(band / a.nbands) : 0;
-  const int bi = live ? (int)(band - (long long)z * a.nbands) : 0;
-  const int k0 = bi * C;
-  const u32* A = a.A + (long long)z * a.a_stride;
-  const u32* B = a.B + (long long)z * a.b_stride;
-  // i range (uniform across the CTA: slots > 1 only when nbands == 1)
-  const int ilo = max(0, k0 - (a.mb - 1));
-  const int ihi = min(a.ma - 1, k0 + C - 1);
-
-  u32 c0[MUL_R], c1[MUL_R], c2[MUL_R];
-#pragma unroll
-  for (int r = 0; r < MUL_R; r++) c0[r] = c1[r] = c2[r] = 0u;
-
-  for (int i0 = ilo; i0 <= ihi; i0 += TI) {
-    for (int x = tb; x < TI; x += G) {
-      const int i = i0 + x;
-      as_[x] = (live && i <= ihi) ? A[i] : 0u;
-    }
-    const int bbase = k0 - i0 - TI + 1;
-    for (int x = tb; x < C + TI; x += G) {
-      const int j = bbase + x;
-      bs_[x] = (live && j >= 0 && j < a.mb) ? B[j] : 0u;
-    }
-    __syncthreads();
-    const int base0 = tb * MUL_R + TI - 8;
-    u32 w[16];
-    {
-      const uint4* p = reinterpret_cast<const uint4*>(bs_ + base0);
-      uint4 q0 = p[0], q1 = p[1], q2 = p[2], q3 = p[3];
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-      w[8] = q2.x; w[9] = q2.y; w[10] = q2.z; w[11] = q2.w;
-      w[12] = q3.x; w[13] = q3.y; w[14] = q3.z; w[15] = q3.w;
-    }
-    const int nu = TI >> 3;
-    for (int u = 0; u < nu; u++) {
-      const uint4* ap = reinterpret_cast<const uint4*>(as_ + 8 * u);
-      const uint4 a0 = ap[0], a1 = ap[1];
-      const u32 av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-#pragma unroll
-      for (int v = 0; v < 8; v++) {
-#pragma unroll
-        for (int r = 0; r < MUL_R; r++) mac96(c0[r], c1[r], c2[r], av[v], w[7 + r - v]);
-      }
-      if (u + 1 < nu) {
-#pragma unroll
-        for (int j = 0; j < 8; j++) w[8 + j] = w[j];
-        const uint4* p = reinterpret_cast<const uint4*>(bs_ + base0 - 8 * (u + 1));
-        const uint4 b0 = p[0], b1 = p[1];
-        w[0] = b0.x; w[1] = b0.y; w[2] = b0.z; w[3] = b0.w;
-        w[4] = b1.x; w[5] = b1.y; w[6] = b1.z; w[7] = b1.w;
-      }
-    }
-    __syncthreads();
-  }
-
-  // ---- epilogue: digit y_r = c0_r + c1_{r-1} + c2_{r-2}  (< 3*2^32)
-  xs[0][tid] = c1[MUL_R - 1];
-  xs[1][tid] = c2[MUL_R - 1];
-  xs[2][tid] = c2[MUL_R - 2];
-  __syncthreads();
-  const u32 p_c1 = tb ? xs[0][tid - 1] : 0u;
-  const u32 p_c2 = tb ? xs[1][tid - 1] : 0u;
-  const u32 p_c2b = tb ? xs[2][tid - 1] : 0u;
-  u32 lo[MUL_R];
-  u32 hi[MUL_R];
-#pragma unroll
-  for (int r = 0; r < MUL_R; r++) {
-    const u64 y = (u64)c0[r] + (r >= 1 ? c1[r - 1] : p_c1) + (r >= 2 ? c2[r - 2] : (r == 1 ? p_c2 : p_c2b));
-    lo[r] = (u32)y;
-    hi[r] = (u32)(y >> 32);
-  }
-  sm_hi[tid] = hi[MUL_R - 1];
-  __syncthreads();
-  const u32 hprev = tb ? (u32)sm_hi[tid - 1] : 0u;
-  i64 zz[MUL_R];
-  u32 M = CM_IDENT;
-  u32 mr[MUL_R];
-#pragma unroll
-  for (int r = 0; r < MUL_R; r++) {
-    zz[r] = (i64)lo[r] + (r ? hi[r - 1] : hprev);
-    mr[r] = cm_make(zz[r]);
-    M = cm_compose(M, mr[r]);
-  }
-  u32 tot;
-  const u32 exc = cm_seg_scan(M, G, sm_scan, &tot);
-  int c = cm_apply(exc, 0);
-  u32 d[MUL_R];
-#pragma unroll
-  for (int r = 0; r < MUL_R; r++) {
-    d[r] = (u32)(zz[r] + c);
-    c = cm_apply(mr[r], c);
-  }
-  if (live) {
-    uint4* dst = reinterpret_cast<uint4*>(a.P + (long long)z * a.p_stride + k0 + tb * MUL_R);
-    dst[0] = make_uint4(d[0], d[1], d[2], d[3]);
-    dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
-    if (tb == G - 1) {
-      const i64 s0 = (i64)c + hi[MUL_R - 1] + c1[MUL_R - 1] + c2[MUL_R - 2];
-      unsigned long long* sp = a.spill + ((long long)z * a.nbands + bi) * 2;
-      sp[0] = (unsigned long long)s0;
-      sp[1] = (unsigned long long)c2[MUL_R - 1];
-    }
-  }
-}
-
-cudaError_t launch_mul(const MulArgs& a, cudaStream_t st) {
-  const int slots = MUL_THREADS / a.G;
-  const long long nbt = (long long)a.nprod * a.nbands;
-  const int grid = (int)((nbt + slots - 1) / slots);
-  const size_t smem = (size_t)slots * (a.G * MUL_R + 2 * a.TI) * sizeof(u32);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_mul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_mul<<<grid, MUL_THREADS, smem, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -461,93 +313,282 @@ __device__ __forceinline__ void mw_mask(MW<NW>& x, u32 topmask) { x.w[NW - 1] &=
 
 template <int NW>
 __device__ __forceinline__ void write_coeff(u32* dst, int ow, const MW<NW>& lo, const MW<NW>& hi, int W) {
-  // value = lo + hi * 2^W  (lo < 2^W)
-  for (int w = 0; w < ow; w++) {
-    u32 x = w < NW ? lo.w[w] : 0u;
-    const long long sh = 32LL * w - W;  // bit of hi at word w's start
+  // value = lo + hi * 2^W (lo < 2^W); all register indices are static
+  const int ws = W >> 5, bs = W & 31;
 #pragma unroll
-    for (int k = 0; k < NW; k++) {
-      // hi.w[k] occupies bits [W + 32k, W + 32k + 32) of the value
-      const long long d = 32LL * k - sh;  // position of hi.w[k] relative to word start
-      if (d > -32 && d < 32) x |= d >= 0 ? (hi.w[k] << d) : (hi.w[k] >> (-d));
+  for (int w = 0; w < 2 * NW + 1; w++) {
+    if (w < ow) {
+      u32 x = w < NW ? lo.w[w] : 0u;
+#pragma unroll
+      for (int k = 0; k < NW; k++) {
+        if (w == ws + k) x |= hi.w[k] << bs;
+        if (bs && w == ws + k + 1) x |= hi.w[k] >> (32 - bs);
+      }
+      dst[w] = x;
     }
-    dst[w] = x;
   }
+  for (int w = 2 * NW + 1; w < ow; w++) dst[w] = 0u;
 }
 
 template <int NW>
-__global__ void __launch_bounds__(128) k_recon(ReconArgs a) {
+__device__ __forceinline__ void mw_inc(MW<NW>& r, const MW<NW>& x) {
+  u32 c = 1u;
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const u64 t = (u64)x.w[i] + c;
+    r.w[i] = (u32)t;
+    c = (u32)(t >> 32);
+  }
+}
+template <int NW>
+__device__ __forceinline__ bool mw_is_zero(const MW<NW>& x) {
+  u32 o = 0u;
+#pragma unroll
+  for (int i = 0; i < NW; i++) o |= x.w[i];
+  return o == 0u;
+}
+template <int NW>
+__device__ __forceinline__ void mw_sel(MW<NW>& r, bool c, const MW<NW>& x, const MW<NW>& y) {
+#pragma unroll
+  for (int i = 0; i < NW; i++) r.w[i] = c ? x.w[i] : y.w[i];
+}
+
+// Carry-select form of the recurrence.  With t_j = rev[j] - lo[j-1] and
+// d_j = fwd[j+1] - t_j (both known one step early), the step is
+//   eps   = lo[j] > rev[j+1]                 (the only dependent compare)
+//   s     = fc_j - eps  in {-1, 0, 1}
+//   lo[j+1] = d_j - s                         (select among d+1, d, d-1)
+//   fc_{j+1} = [t_j + s > fwd[j+1]]           (select among 3 precomputed)
+//   hi[j] = t_j - eps
+// which equals ksint.py:153-169 whenever hi[j] is in range (an out-of-range
+// hi[j] == 2^W - 1 is reported as ReconstructionError, as the reference does).
+template <int NW>
+__device__ __forceinline__ void mw_lds(MW<NW>& x, const u32* p) {
+#pragma unroll
+  for (int i = 0; i < NW; i++) x.w[i] = p[i];
+}
+__device__ __forceinline__ void cp_async4(u32* sdst, const u32* gsrc) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N)); }
+
+constexpr int RECON_WARPS = 2;
+
+// One thread per digit-stream pair; the 32 streams of a warp are fed by a
+// warp-cooperative, double-buffered cp.async pipeline: while the lanes run
+// chunk c of their recurrences out of shared memory, chunk c+1 (the next CH
+// digits of all 32 streams, coalesced rows) is in flight.
+//
+// Carry-select form of the recurrence (ksint.py:153-169).  With
+// t_j = rev[j] - lo[j-1] and d_j = fwd[j+1] - t_j (both off the critical
+// path), one step is
+//   eps      = lo[j] > rev[j+1]           (the only dependent compare)
+//   s        = fc_j - eps in {-1, 0, 1}
+//   lo[j+1]  = d_j - s                    (select among d+1, d, d-1)
+//   fc_{j+1} = [t_j + s > fwd[j+1]]       (select among 3 precomputed)
+//   hi[j]    = t_j - eps
+// identical to the reference whenever hi[j] is in range; hi[j] == 2^W - 1 is
+// reported as ReconstructionError (ksint.py:157-158).
+template <int NW>
+__global__ void __launch_bounds__(32 * RECON_WARPS) k_recon(ReconArgs a) {
+  extern __shared__ u32 rsm[];
+  __shared__ const u32* tabF[RECON_WARPS][32];
+  __shared__ const u32* tabR[RECON_WARPS][32];
+  __shared__ int tabC[RECON_WARPS][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int gid = blockIdx.x * blockDim.x + threadIdx.x;
-  if (gid >= a.batch * a.ns) return;
-  const int pair = gid / a.ns, si = gid - pair * a.ns;
-  const ReconStream S = a.s[si];
+  const int total = a.batch * a.ns;
+  const bool live = gid < total;
+  const int g = live ? gid : total - 1;
+  const int pair = g / a.ns, si = g - pair * a.ns;
+  const ReconStream S = si == 0 ? a.s[0] : a.s[1];
   const u32* F = a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride;
   const u32* R = a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride;
   u32* H = a.h + (long long)pair * a.h_pair_stride;
-  const int W = a.W, dw = a.dwords, ow = a.out_words, count = S.count;
-  const int topbits = W - 32 * (NW - 1);
-  const u32 topmask = topbits >= 32 ? 0xffffffffu : ((1u << topbits) - 1u);
-  MW<NW> mask;
+  const int W = a.W, dw = a.dwords, ow = a.out_words;
+  const int count = live ? S.count : 0;
+  tabF[warp][lane] = F;
+  tabR[warp][lane] = R;
+  tabC[warp][lane] = count;
+  const int CH = a.rch;                 // steps per chunk
+  const int CHW = CH * dw;              // words per stream per array per chunk
+  const int SS = 2 * CHW + 1;           // odd stride: conflict-free lane reads
+  u32* buf0 = rsm + warp * 2 * 32 * SS;
+  u32* buf1 = buf0 + 32 * SS;
+  int maxc = count;
 #pragma unroll
-  for (int i = 0; i < NW; i++) mask.w[i] = 0xffffffffu;
-  mw_mask(mask, topmask);
-  MW<NW> zero;
-#pragma unroll
-  for (int i = 0; i < NW; i++) zero.w[i] = 0u;
+  for (int o = 16; o; o >>= 1) maxc = max(maxc, __shfl_xor_sync(0xffffffffu, maxc, o));
+  const int nsteps = maxc - 1;
+  const int nchunks = nsteps > 0 ? (nsteps + CH - 1) / CH : 0;
+  __syncwarp();
 
-  uint8_t* car = a.carries ? a.carries + (long long)gid * (2 * count + 1) : nullptr;
+  auto issue = [&](int c, u32* bufp) {
+    const int w0 = (c * CH + 1) * dw;
+    for (int s = 0; s < 32; s++) {
+      const int lim = (tabC[warp][s] + 1) * dw - w0;  // words that exist from w0
+      const u32* Fs = tabF[warp][s] + w0;
+      const u32* Rs = tabR[warp][s] + w0;
+      u32* dstp = bufp + s * SS;
+      for (int w = lane; w < CHW && w < lim; w += 32) {
+        cp_async4(dstp + w, Fs + w);
+        cp_async4(dstp + CHW + w, Rs + w);
+      }
+    }
+    cp_async_commit();
+  };
+
+  uint8_t* car = (live && a.carries) ? a.carries + (long long)gid * (2 * count + 1) : nullptr;
   if (car) { car[0] = 0; car[count] = 0; car[2 * count] = 0; }
-  MW<NW> lo_prev = zero, lo_cur, h;
-  mw_load(lo_cur, F);  // lo[0] = fwd[0]
-  u32 fc = 0;
   bool bad = false;
-  MW<NW> rj, rj1, fj1;
-  mw_load(rj, R);
-  for (int j = 0; j < count - 1; j++) {
-    mw_load(rj1, R + (long long)(j + 1) * dw);
-    mw_load(fj1, F + (long long)(j + 1) * dw);
-    const u32 eps = mw_gt(lo_cur, rj1) ? 1u : 0u;  // ksint.py:154 (strict)
-    mw_sub(h, rj, lo_prev, eps);
+  u32 fc = 0;
+  if (nchunks > 0) issue(0, buf0);
+
+  if constexpr (NW <= 2) {
+    // ---------------- digits of at most 64 bits: native u64 arithmetic
+    const u64 mask = W >= 64 ? ~0ull : ((1ull << W) - 1ull);
+    auto ld = [&](const u32* p) -> u64 { return NW == 1 ? (u64)p[0] : ((u64)p[0] | ((u64)p[1] << 32)); };
+    u64 lo_prev = 0, lo_cur = 0, rj = 0;
+    if (live) { lo_cur = ld(F); rj = ld(R); }
+    for (int c = 0; c < nchunks; c++) {
+      u32* cur = (c & 1) ? buf1 : buf0;
+      if (c + 1 < nchunks) { issue(c + 1, (c & 1) ? buf0 : buf1); cp_async_wait<1>(); }
+      else cp_async_wait<0>();
+      __syncwarp();
+      const u32* fsm = cur + lane * SS;
+      const u32* rsmp = fsm + CHW;
+      const int jend = min((c + 1) * CH, count - 1);
+      for (int j = c * CH; j < jend; j++) {
+        const int jj = (j - c * CH) * dw;
+        const u64 rj1 = ld(rsmp + jj), fj1 = ld(fsm + jj);
+        const u64 t = (rj - lo_prev) & mask;
+        const u64 tm1 = (t - 1) & mask;
+        const u64 d = (fj1 - t) & mask;
+        const u64 dp1 = (d + 1) & mask, dm1 = (d - 1) & mask;
+        const u32 b0 = t > fj1, bp1 = t >= fj1, bm1 = tm1 > fj1;
+        const u32 eps = lo_cur > rj1;                 // ksint.py:154 (strict)
+        const u64 h = eps ? tm1 : t;
+        bad |= h == mask;
+        // coefficient j = lo[j] + hi[j] * 2^W
+        u64 v0, v1;
+        if (W >= 64) { v0 = lo_cur; v1 = h; }
+        else { v0 = lo_cur | (h << W); v1 = h >> (64 - W); }
+        u32* dst = H + (long long)(S.pos0 + (long long)j * S.pstride) * ow;
+        dst[0] = (u32)v0;
+        if (ow > 1) dst[1] = (u32)(v0 >> 32);
+        if (ow > 2) dst[2] = (u32)v1;
+        if (ow > 3) dst[3] = (u32)(v1 >> 32);
+        for (int w = 4; w < ow; w++) dst[w] = 0u;
+        const int sdir = (int)fc - (int)eps;
+        const u64 nxt = sdir == 0 ? d : (sdir > 0 ? dm1 : dp1);
+        const u32 fcn = sdir == 0 ? b0 : (sdir > 0 ? bp1 : bm1);
+        if (car) { car[j + 1] = (uint8_t)fcn; car[count + 1 + j] = (uint8_t)eps; }
+        fc = fcn;
+        lo_prev = lo_cur;
+        lo_cur = nxt;
+        rj = rj1;
+      }
+      __syncwarp();
+    }
+    if (!live) return;
+    const u64 h = (rj - (count >= 2 ? lo_prev : 0ull)) & mask;   // ksint.py:170-177
+    bad |= h == mask;
+    const u64 rlast = ld(R + (long long)count * dw), flast = ld(F + (long long)count * dw);
+    bad |= lo_cur != rlast;
+    bad |= (h + fc) != flast;
+    u64 v0, v1;
+    if (W >= 64) { v0 = lo_cur; v1 = h; }
+    else { v0 = lo_cur | (h << W); v1 = h >> (64 - W); }
+    u32* dst = H + (long long)(S.pos0 + (long long)(count - 1) * S.pstride) * ow;
+    dst[0] = (u32)v0;
+    if (ow > 1) dst[1] = (u32)(v0 >> 32);
+    if (ow > 2) dst[2] = (u32)v1;
+    if (ow > 3) dst[3] = (u32)(v1 >> 32);
+    for (int w = 4; w < ow; w++) dst[w] = 0u;
+  } else {
+    // ---------------- multiword digits
+    const int topbits = W - 32 * (NW - 1);
+    const u32 topmask = topbits >= 32 ? 0xffffffffu : ((1u << topbits) - 1u);
+    MW<NW> mask, zero;
+#pragma unroll
+    for (int i = 0; i < NW; i++) { mask.w[i] = 0xffffffffu; zero.w[i] = 0u; }
+    mw_mask(mask, topmask);
+    MW<NW> lo_prev = zero, lo_cur = zero, rj = zero;
+    if (live) { mw_load(lo_cur, F); mw_load(rj, R); }
+    for (int c = 0; c < nchunks; c++) {
+      u32* cur = (c & 1) ? buf1 : buf0;
+      if (c + 1 < nchunks) { issue(c + 1, (c & 1) ? buf0 : buf1); cp_async_wait<1>(); }
+      else cp_async_wait<0>();
+      __syncwarp();
+      const u32* fsm = cur + lane * SS;
+      const u32* rsmp = fsm + CHW;
+      const int jend = min((c + 1) * CH, count - 1);
+      for (int j = c * CH; j < jend; j++) {
+        const int jj = (j - c * CH) * dw;
+        MW<NW> rj1, fj1, t, tm1, d, dp1, dm1, h, nxt;
+        mw_lds(rj1, rsmp + jj);
+        mw_lds(fj1, fsm + jj);
+        mw_sub(t, rj, lo_prev, 0u);
+        mw_mask(t, topmask);
+        mw_sub(tm1, t, zero, 1u);
+        mw_mask(tm1, topmask);
+        const u32 b0 = mw_sub(d, fj1, t, 0u);
+        const u32 bm1 = mw_sub(dp1, fj1, tm1, 0u);
+        mw_mask(d, topmask);
+        mw_mask(dp1, topmask);
+        mw_sub(dm1, d, zero, 1u);
+        mw_mask(dm1, topmask);
+        const u32 bp1 = b0 | (mw_is_zero(d) ? 1u : 0u);
+        const u32 eps = mw_gt(lo_cur, rj1) ? 1u : 0u;  // ksint.py:154 (strict)
+        mw_sel(h, eps != 0u, tm1, t);
+        bad |= mw_eq(h, mask);
+        write_coeff(H + (long long)(S.pos0 + (long long)j * S.pstride) * ow, ow, lo_cur, h, W);
+        const int sdir = (int)fc - (int)eps;
+        mw_sel(nxt, sdir > 0, dm1, dp1);
+        mw_sel(nxt, sdir == 0, d, nxt);
+        const u32 fcn = sdir == 0 ? b0 : (sdir > 0 ? bp1 : bm1);
+        if (car) { car[j + 1] = (uint8_t)fcn; car[count + 1 + j] = (uint8_t)eps; }
+        fc = fcn;
+        lo_prev = lo_cur;
+        lo_cur = nxt;
+        rj = rj1;
+      }
+      __syncwarp();
+    }
+    if (!live) return;
+    MW<NW> h;
+    mw_sub(h, rj, count >= 2 ? lo_prev : zero, 0u);  // ksint.py:170-177
     mw_mask(h, topmask);
-    bad |= mw_eq(h, mask);                          // ksint.py:157-158
-    MW<NW> nxt;
-    const u32 br = mw_sub(nxt, fj1, h, fc);         // borrow <=> h + fc > fwd[j+1]
-    mw_mask(nxt, topmask);
-    write_coeff(H + (long long)(S.pos0 + (long long)j * S.pstride) * ow, ow, lo_cur, h, W);
-    fc = br;                                        // ksint.py:163-169
-    if (car) { car[j + 1] = (uint8_t)br; car[count + 1 + j] = (uint8_t)eps; }
-    lo_prev = lo_cur;
-    lo_cur = nxt;
-    rj = rj1;
+    bad |= mw_eq(h, mask);
+    MW<NW> rlast, flast, hs;
+    mw_load(rlast, R + (long long)count * dw);
+    mw_load(flast, F + (long long)count * dw);
+    bad |= !mw_eq(lo_cur, rlast);
+    const u32 br = mw_sub(hs, flast, h, fc);  // h + fc == fwd[count]
+    bad |= (br != 0u) || !mw_is_zero(hs);
+    write_coeff(H + (long long)(S.pos0 + (long long)(count - 1) * S.pstride) * ow, ow, lo_cur, h, W);
   }
-  // final coefficient and consistency checks (ksint.py:170-177)
-  mw_sub(h, rj, count >= 2 ? lo_prev : zero, 0u);
-  mw_mask(h, topmask);
-  bad |= mw_eq(h, mask);
-  MW<NW> rlast, flast;
-  mw_load(rlast, R + (long long)count * dw);
-  mw_load(flast, F + (long long)count * dw);
-  bad |= !mw_eq(lo_cur, rlast);
-  MW<NW> hs;
-  MW<NW> fcw = zero;
-  fcw.w[0] = fc;
-  MW<NW> negf;
-  // h + fc == fwd[count]  <=>  fwd[count] - h - fc == 0 without borrow
-  const u32 br = mw_sub(hs, flast, h, fc);
-  bad |= (br != 0u) || !mw_eq(hs, zero);
-  (void)fcw; (void)negf;
-  write_coeff(H + (long long)(S.pos0 + (long long)(count - 1) * S.pstride) * ow, ow, lo_cur, h, W);
   if (bad) raise_err(a.err, ERR_RECON);
 }
 
 template <int NW>
 static cudaError_t launch_recon_t(const ReconArgs& a, cudaStream_t st) {
   const int n = a.batch * a.ns;
-  k_recon<NW><<<(n + 127) / 128, 128, 0, st>>>(a);
+  const int nth = 32 * RECON_WARPS;
+  const size_t smem = (size_t)RECON_WARPS * 2 * 32 * (2 * a.rch * a.dwords + 1) * sizeof(u32);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_recon<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_recon<NW><<<(n + nth - 1) / nth, nth, smem, st>>>(a);
   return cudaGetLastError();
 }
 
-cudaError_t launch_recon(const ReconArgs& a, cudaStream_t st) {
+cudaError_t launch_recon(const ReconArgs& a0, cudaStream_t st) {
+  ReconArgs a = a0;
+  a.rch = a.dwords >= 32 ? 1 : 32 / a.dwords;  // ~32 words per stream per array per chunk
   switch (a.dwords) {
     case 1: return launch_recon_t<1>(a, st);
     case 2: return launch_recon_t<2>(a, st);
