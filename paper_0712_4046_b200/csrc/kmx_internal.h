@@ -94,6 +94,7 @@ struct ReconArgs {
   uint8_t* carries;           // optional [batch*ns][2*count+1]: fwd carries, rev carries
   uint32_t* err;
   int rch;                    // steps per staged chunk (set by launch_recon)
+  int sequential;             // force the one-thread-per-stream kernel
 };
 
 // ---------------------------------------------------------- signed (bias)

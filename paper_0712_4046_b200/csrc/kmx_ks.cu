@@ -573,6 +573,275 @@ __global__ void __launch_bounds__(32 * RECON_WARPS) k_recon(ReconArgs a) {
   if (bad) raise_err(a.err, ERR_RECON);
 }
 
+// ========================================================================
+// K4b: segmented parallel reconstruction.
+//
+// The recurrence lo[j+1] = lo[j-1] + c_j + e_j (mod 2^W) with
+// c_j = fwd[j+1] - rev[j] (known) and e_j = eps_j - delta_j in {-1,0,1}
+// makes each of the two interleaved chains an exact prefix sum of the c's
+// plus a small integer correction E (the prefix sum of the e's).  One CTA
+// owns one digit-stream pair; thread i owns the steps [iV, (i+1)V).  A block
+// scan of the segments' c-sums gives every segment its exact base values;
+// the corrections E and the carry delta at each segment start are guessed
+// (first guess 0), every thread runs the reference step (ksint.py:153-169)
+// sequentially over its segment from its guessed start state, and a block
+// scan of the segments' e-sums / carry-outs produces the next guesses.  When
+// the guesses reproduce themselves, every step equation of the reference
+// recurrence holds, so by induction on j the result equals the sequential
+// solution; the final walk's outputs are kept.  Without convergence after
+// RECON_MAXIT rounds, thread 0 runs the whole stream sequentially.
+// ========================================================================
+constexpr int RECON_MAXIT = 8;
+
+template <int NW>
+__device__ __forceinline__ void mw_add_small(MW<NW>& r, const MW<NW>& x, int e) {
+  // r = x + e (two's complement sign extension of e)
+  const u32 ext = e < 0 ? 0xffffffffu : 0u;
+  u32 c = 0;
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const u64 t = (u64)x.w[i] + (i == 0 ? (u32)e : ext) + c;
+    r.w[i] = (u32)t;
+    c = (u32)(t >> 32);
+  }
+}
+template <int NW>
+__device__ __forceinline__ void mw_add(MW<NW>& r, const MW<NW>& x, const MW<NW>& y) {
+  u32 c = 0;
+#pragma unroll
+  for (int i = 0; i < NW; i++) {
+    const u64 t = (u64)x.w[i] + y.w[i] + c;
+    r.w[i] = (u32)t;
+    c = (u32)(t >> 32);
+  }
+}
+
+// block-wide exclusive scan (sum mod 2^(32NW), then masked by the caller)
+// of a pair of multiword values; sm needs 2*NW*32 words.
+template <int NW>
+__device__ void block_exscan_mw2(MW<NW>& x0, MW<NW>& x1, u32* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+  MW<NW> i0 = x0, i1 = x1;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    MW<NW> o0, o1;
+#pragma unroll
+    for (int k = 0; k < NW; k++) {
+      o0.w[k] = __shfl_up_sync(0xffffffffu, i0.w[k], off);
+      o1.w[k] = __shfl_up_sync(0xffffffffu, i1.w[k], off);
+    }
+    if (lane >= off) { mw_add(i0, i0, o0); mw_add(i1, i1, o1); }
+  }
+  __syncthreads();
+  if (lane == 31) {
+#pragma unroll
+    for (int k = 0; k < NW; k++) { sm[(warp * 2) * NW + k] = i0.w[k]; sm[(warp * 2 + 1) * NW + k] = i1.w[k]; }
+  }
+  __syncthreads();
+  MW<NW> p0, p1;
+#pragma unroll
+  for (int k = 0; k < NW; k++) { p0.w[k] = 0u; p1.w[k] = 0u; }
+  for (int w = 0; w < warp && w < nw; w++) {
+    MW<NW> t0, t1;
+#pragma unroll
+    for (int k = 0; k < NW; k++) { t0.w[k] = sm[(w * 2) * NW + k]; t1.w[k] = sm[(w * 2 + 1) * NW + k]; }
+    mw_add(p0, p0, t0);
+    mw_add(p1, p1, t1);
+  }
+  // exclusive = prefix of earlier warps + (inclusive - own)
+  MW<NW> e0, e1;
+#pragma unroll
+  for (int k = 0; k < NW; k++) {
+    e0.w[k] = __shfl_up_sync(0xffffffffu, i0.w[k], 1);
+    e1.w[k] = __shfl_up_sync(0xffffffffu, i1.w[k], 1);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NW; k++) { e0.w[k] = 0u; e1.w[k] = 0u; }
+  }
+  mw_add(x0, p0, e0);
+  mw_add(x1, p1, e1);
+  __syncthreads();
+}
+
+// block-wide exclusive scan of two ints; returns the block totals in *t0, *t1
+__device__ void block_exscan_i2(int& x0, int& x1, int* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  int i0 = x0, i1 = x1;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o0 = __shfl_up_sync(0xffffffffu, i0, off), o1 = __shfl_up_sync(0xffffffffu, i1, off);
+    if (lane >= off) { i0 += o0; i1 += o1; }
+  }
+  __syncthreads();
+  if (lane == 31) { sm[2 * warp] = i0; sm[2 * warp + 1] = i1; }
+  __syncthreads();
+  int p0 = 0, p1 = 0;
+  for (int w = 0; w < warp; w++) { p0 += sm[2 * w]; p1 += sm[2 * w + 1]; }
+  x0 = p0 + i0 - x0;
+  x1 = p1 + i1 - x1;
+  __syncthreads();
+}
+
+template <int NW>
+struct ReconState {
+  MW<NW> lo_prev, lo_cur, rj;  // lo[j-1], lo[j], rev[j]
+  u32 fc;                      // delta_j
+};
+
+// Run steps [j0, j1) of the reference recurrence from state st; writes the
+// coefficients; accumulates e_j into esum[(j+1)&1]; latches out-of-range hi.
+template <int NW>
+__device__ __forceinline__ void recon_walk(ReconState<NW>& st, int j0, int j1, const u32* F, const u32* R, int dw,
+                                           u32* H, int pos0, int pstride, int ow, int W, u32 topmask,
+                                           const MW<NW>& mask, int& e0, int& e1, bool& bad) {
+  MW<NW> zero;
+#pragma unroll
+  for (int i = 0; i < NW; i++) zero.w[i] = 0u;
+  for (int j = j0; j < j1; j++) {
+    MW<NW> rj1, fj1, h, nxt;
+    mw_load(rj1, R + (long long)(j + 1) * dw);
+    mw_load(fj1, F + (long long)(j + 1) * dw);
+    const u32 eps = mw_gt(st.lo_cur, rj1) ? 1u : 0u;  // ksint.py:154 (strict)
+    mw_sub(h, st.rj, st.lo_prev, eps);
+    mw_mask(h, topmask);
+    bad |= mw_eq(h, mask);                           // ksint.py:157-158
+    const u32 br = mw_sub(nxt, fj1, h, st.fc);       // borrow <=> h + fc > fwd[j+1]
+    mw_mask(nxt, topmask);
+    write_coeff(H + (long long)(pos0 + (long long)j * pstride) * ow, ow, st.lo_cur, h, W);
+    const int ej = (int)eps - (int)st.fc;
+    if ((j + 1) & 1) e1 += ej; else e0 += ej;
+    st.fc = br;
+    st.lo_prev = st.lo_cur;
+    st.lo_cur = nxt;
+    st.rj = rj1;
+  }
+  (void)zero;
+}
+
+constexpr int RECON_PAR_MAXT = 512;
+
+template <int NW>
+__global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
+  __shared__ u32 smw[2 * 17 * 32];
+  __shared__ int smi[64];
+  __shared__ uint8_t dend[RECON_PAR_MAXT];
+  __shared__ int fallback;
+  const int sid = blockIdx.x;
+  const int pair = sid / a.ns, si = sid - pair * a.ns;
+  const ReconStream S = si == 0 ? a.s[0] : a.s[1];
+  const u32* F = a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride;
+  const u32* R = a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride;
+  u32* H = a.h + (long long)pair * a.h_pair_stride;
+  const int W = a.W, dw = a.dwords, ow = a.out_words, count = S.count;
+  const int nsteps = count - 1;
+  const int T = blockDim.x, tid = threadIdx.x;
+  const int V = nsteps > 0 ? (nsteps + T - 1) / T : 1;
+  const int s0 = min(tid * V, nsteps), s1 = min(s0 + V, nsteps);
+  const int topbits = W - 32 * (NW - 1);
+  const u32 topmask = topbits >= 32 ? 0xffffffffu : ((1u << topbits) - 1u);
+  MW<NW> mask, zero;
+#pragma unroll
+  for (int i = 0; i < NW; i++) { mask.w[i] = 0xffffffffu; zero.w[i] = 0u; }
+  mw_mask(mask, topmask);
+
+  // exact chain bases at the segment start: base_m = init[m&1] + sum c_j,
+  // (j+1) == m (mod 2), j < s0; init = (fwd[0], 0)
+  MW<NW> cs0 = zero, cs1 = zero;
+  for (int j = s0; j < s1; j++) {
+    MW<NW> f1, r0, c;
+    mw_load(f1, F + (long long)(j + 1) * dw);
+    mw_load(r0, R + (long long)j * dw);
+    mw_sub(c, f1, r0, 0u);
+    if ((j + 1) & 1) mw_add(cs1, cs1, c); else mw_add(cs0, cs0, c);
+  }
+  block_exscan_mw2(cs0, cs1, smw);
+  MW<NW> f0;
+  mw_load(f0, F);
+  mw_add(cs0, cs0, f0);  // even chain starts at lo[0] = fwd[0], odd at lo[-1] = 0
+  mw_mask(cs0, topmask);
+  mw_mask(cs1, topmask);
+  // guesses
+  int E0 = 0, E1 = 0;  // corrections at the segment start, by parity
+  u32 dstart = 0;      // delta at the segment start
+  if (tid == 0) fallback = 0;
+  bool bad = false;
+  ReconState<NW> st;
+  bool converged = false;
+  for (int it = 0; it < RECON_MAXIT && !converged; it++) {
+    // start state (lo[s0-1], lo[s0], delta_s0)
+    const int p = s0 & 1;
+    mw_add_small(st.lo_cur, p ? cs1 : cs0, p ? E1 : E0);
+    mw_mask(st.lo_cur, topmask);
+    if (s0 == 0) {
+      st.lo_prev = zero;
+    } else {
+      mw_add_small(st.lo_prev, p ? cs0 : cs1, p ? E0 : E1);
+      mw_mask(st.lo_prev, topmask);
+    }
+    mw_load(st.rj, R + (long long)s0 * dw);
+    st.fc = dstart;
+    int n0 = 0, n1 = 0;
+    bad = false;
+    recon_walk(st, s0, s1, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, bad);
+    // next guesses
+    block_exscan_i2(n0, n1, smi);
+    dend[tid] = (uint8_t)st.fc;
+    __syncthreads();
+    const u32 dnew = tid ? (u32)dend[tid - 1] : 0u;
+    const bool same = (n0 == E0) && (n1 == E1) && (dnew == dstart);
+    converged = __syncthreads_and(same);
+    E0 = n0; E1 = n1; dstart = dnew;
+  }
+  if (!converged) {
+    if (tid == 0) {
+      fallback = 1;
+      st.lo_prev = zero;
+      st.lo_cur = f0;
+      mw_load(st.rj, R);
+      st.fc = 0u;
+      int q0 = 0, q1 = 0;
+      bad = false;
+      recon_walk(st, 0, nsteps, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad);
+    }
+    __syncthreads();
+  }
+  // the thread owning the last step finishes (ksint.py:170-177)
+  const int owner = fallback ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
+  if (tid == owner) {
+    if (nsteps == 0) {
+      st.lo_prev = zero;
+      st.lo_cur = f0;
+      mw_load(st.rj, R);
+      st.fc = 0u;
+    }
+    MW<NW> h;
+    mw_sub(h, st.rj, count >= 2 ? st.lo_prev : zero, 0u);
+    mw_mask(h, topmask);
+    bool b2 = mw_eq(h, mask);
+    MW<NW> rlast, flast, hs;
+    mw_load(rlast, R + (long long)count * dw);
+    mw_load(flast, F + (long long)count * dw);
+    b2 |= !mw_eq(st.lo_cur, rlast);
+    const u32 br = mw_sub(hs, flast, h, st.fc);
+    b2 |= (br != 0u) || !mw_is_zero(hs);
+    write_coeff(H + (long long)(S.pos0 + (long long)(count - 1) * S.pstride) * ow, ow, st.lo_cur, h, W);
+    if (b2) raise_err(a.err, ERR_RECON);
+  }
+  if (bad && (!fallback || tid == 0)) raise_err(a.err, ERR_RECON);
+}
+
+template <int NW>
+static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStream_t st) {
+  const int nsteps = maxcount > 1 ? maxcount - 1 : 1;
+  int T = (nsteps + 7) / 8;             // ~8 steps per thread
+  T = ((T + 31) / 32) * 32;
+  if (T < 32) T = 32;
+  if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;
+  k_recon_par<NW><<<a.batch * a.ns, T, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
 template <int NW>
 static cudaError_t launch_recon_t(const ReconArgs& a, cudaStream_t st) {
   const int n = a.batch * a.ns;
@@ -586,7 +855,33 @@ static cudaError_t launch_recon_t(const ReconArgs& a, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_recon_par(const ReconArgs& a, cudaStream_t st) {
+  int maxcount = a.s[0].count;
+  if (a.ns > 1 && a.s[1].count > maxcount) maxcount = a.s[1].count;
+  switch (a.dwords) {
+    case 1: return launch_recon_par_t<1>(a, maxcount, st);
+    case 2: return launch_recon_par_t<2>(a, maxcount, st);
+    case 3: return launch_recon_par_t<3>(a, maxcount, st);
+    case 4: return launch_recon_par_t<4>(a, maxcount, st);
+    case 5: return launch_recon_par_t<5>(a, maxcount, st);
+    case 6: return launch_recon_par_t<6>(a, maxcount, st);
+    case 7: return launch_recon_par_t<7>(a, maxcount, st);
+    case 8: return launch_recon_par_t<8>(a, maxcount, st);
+    case 9: return launch_recon_par_t<9>(a, maxcount, st);
+    case 10: return launch_recon_par_t<10>(a, maxcount, st);
+    case 11: return launch_recon_par_t<11>(a, maxcount, st);
+    case 12: return launch_recon_par_t<12>(a, maxcount, st);
+    case 13: return launch_recon_par_t<13>(a, maxcount, st);
+    case 14: return launch_recon_par_t<14>(a, maxcount, st);
+    case 15: return launch_recon_par_t<15>(a, maxcount, st);
+    case 16: return launch_recon_par_t<16>(a, maxcount, st);
+    case 17: return launch_recon_par_t<17>(a, maxcount, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_recon(const ReconArgs& a0, cudaStream_t st) {
+  if (!a0.carries && !a0.sequential) return launch_recon_par(a0, st);
   ReconArgs a = a0;
   a.rch = a.dwords >= 32 ? 1 : 32 / a.dwords;  // ~32 words per stream per array per chunk
   switch (a.dwords) {
