@@ -243,6 +243,16 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     Gq.coeffs = g; Gq.coeff_pair_stride = (long long)p.lg * p.in_words; Gq.len = p.lg; Gq.kind = p.kinds[s];
     Gq.out = opg + (long long)s * p.mgs; Gq.out_pair_stride = (long long)p.P * p.mgs;
     Gq.meta = meta + 2 * (p.P + s); Gq.meta_pair_stride = 4LL * p.P; Gq.m = p.mg; Gq.validate = validate && s == 0;
+    if (p.sign && s == 0) {  // prefix sums of the lifted inputs for the fused bias correction
+      F.prefix = scr; F.prefix_pair_stride = p.lf + p.lg + 2;
+      Gq.prefix = scr + p.lf + 1; Gq.prefix_pair_stride = p.lf + p.lg + 2;
+    }
+  }
+  BiasFix bfix;
+  memset(&bfix, 0, sizeof bfix);
+  if (p.sign) {
+    bfix.pf = scr; bfix.pair_stride = p.lf + p.lg + 2;
+    bfix.lf = p.lf; bfix.lg = p.lg; bfix.b = p.b; bfix.enabled = 1;
   }
   prof_begin(0, st);
   if ((e = launch_pack(pa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
@@ -269,6 +279,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.h = h; fa.out_words = out_words; fa.h_pair_stride = (long long)p.out_len * out_words;
   fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = (long long)p.cnt_max * p.dwords;
   fa.dslots_pair = p.dslots; fa.err = err;
+  fa.bias = bfix;
   prof_begin(2, st);
   if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
   prof_end(2, st);
@@ -283,18 +294,10 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     ra.dslots_pair = p.dslots;
     ra.h = h; ra.out_words = out_words; ra.h_pair_stride = (long long)p.out_len * out_words;
     ra.err = err;
+    ra.bias = bfix;
     prof_begin(3, st);
     if ((e = launch_recon(ra, st)) != cudaSuccess) return KMX_ECUDA;
     prof_end(3, st);
-    g_launches++;
-  }
-  if (p.sign) {
-    BiasArgs ba;
-    ba.f = f; ba.g = g; ba.lf = p.lf; ba.lg = p.lg; ba.b = p.b;
-    ba.h = h; ba.out_words = out_words; ba.scratch = scr; ba.batch = p.batch;
-    prof_begin(4, st);
-    if ((e = launch_bias(ba, st)) != cudaSuccess) return KMX_ECUDA;
-    prof_end(4, st);
     g_launches++;
   }
   return KMX_OK;
@@ -308,12 +311,34 @@ int status_from_flag(uint32_t fl) {
 }
 
 // per-device cached buffers for the host entry points
+constexpr int HOST_LANES = 3;     // streams of the pipelined host path
+constexpr int HOST_MAX_CHUNKS = 16;
+
+struct HostLane {
+  cudaStream_t st = nullptr;
+  void* buf[3] = {nullptr, nullptr, nullptr};
+  size_t cap[3] = {0, 0, 0};
+};
+
 struct HostCtx {
   std::mutex mu;
   cudaStream_t st = nullptr;
   void* buf[4] = {nullptr, nullptr, nullptr, nullptr};
   size_t cap[4] = {0, 0, 0, 0};
+  HostLane lane[HOST_LANES];
+  uint32_t* flags = nullptr;        // pinned, one error word per chunk
 };
+
+int ensure_buf(void** buf, size_t* cap, size_t bytes) {
+  if (*cap >= bytes) return KMX_OK;
+  if (*buf) cudaFree(*buf);
+  *buf = nullptr;
+  *cap = 0;
+  size_t want = std::max(bytes, (size_t)4096);
+  if (cudaMalloc(buf, want) != cudaSuccess) return KMX_ENOMEM;
+  *cap = want;
+  return KMX_OK;
+}
 HostCtx g_ctx[16];
 
 int ensure(HostCtx& c, int i, size_t bytes) {
@@ -333,6 +358,58 @@ HostCtx* host_ctx(int* rc) {
   HostCtx& c = g_ctx[dev];
   *rc = KMX_OK;
   return &c;
+}
+
+// Pipelined host path: the batch is cut into chunks that rotate over
+// HOST_LANES streams, so the host->device copy of chunk i+1, the kernels of
+// chunk i and the device->host copy of chunk i-1 overlap (with pinned host
+// buffers; pageable buffers still work, without the overlap).
+int ks_mul_host_pipelined(const KsPlan& pfull, HostCtx* c, const uint32_t* f, const uint32_t* g,
+                                 uint32_t* h, int out_words, int nchunks) {
+  const int batch = pfull.batch;
+  const int cb = (batch + nchunks - 1) / nchunks;
+  nchunks = (batch + cb - 1) / cb;
+  KsPlan pc, pt;
+  int rc = make_plan(pc, pfull.req_variant, cb, pfull.lf, pfull.lg, pfull.b, pfull.in_words, pfull.flags);
+  if (rc) return rc;
+  const int tail = batch - (nchunks - 1) * cb;
+  rc = make_plan(pt, pfull.req_variant, tail, pfull.lf, pfull.lg, pfull.b, pfull.in_words, pfull.flags);
+  if (rc) return rc;
+  const size_t fpp = (size_t)pfull.lf * pfull.in_words, gpp = (size_t)pfull.lg * pfull.in_words;
+  const size_t hpp = (size_t)pfull.out_len * out_words;
+  const size_t fb = (size_t)cb * fpp * 4, gb = (size_t)cb * gpp * 4, hb = (size_t)cb * hpp * 4;
+  if (!c->flags && cudaMallocHost(&c->flags, HOST_MAX_CHUNKS * sizeof(uint32_t)) != cudaSuccess) return KMX_ENOMEM;
+  for (int l = 0; l < HOST_LANES && l < nchunks; l++) {
+    HostLane& L = c->lane[l];
+    if (!L.st && cudaStreamCreateWithFlags(&L.st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+    if ((rc = ensure_buf(&L.buf[0], &L.cap[0], align256(fb) + gb + 256))) return rc;
+    if ((rc = ensure_buf(&L.buf[1], &L.cap[1], hb))) return rc;
+    if ((rc = ensure_buf(&L.buf[2], &L.cap[2], pc.total))) return rc;
+  }
+  int nl = 0;
+  for (int i = 0; i < nchunks; i++) {
+    HostLane& L = c->lane[i % HOST_LANES];
+    const KsPlan& pp = (i == nchunks - 1) ? pt : pc;
+    const int bi = pp.batch;
+    uint32_t* df = (uint32_t*)L.buf[0];
+    uint32_t* dg = (uint32_t*)((char*)L.buf[0] + align256(fb));
+    if (cudaMemcpyAsync(df, f + (size_t)i * cb * fpp, (size_t)bi * fpp * 4, cudaMemcpyHostToDevice, L.st) != cudaSuccess)
+      return KMX_ECUDA;
+    if (cudaMemcpyAsync(dg, g + (size_t)i * cb * gpp, (size_t)bi * gpp * 4, cudaMemcpyHostToDevice, L.st) != cudaSuccess)
+      return KMX_ECUDA;
+    rc = run_plan(pp, df, dg, (uint32_t*)L.buf[1], out_words, L.buf[2], L.cap[2], L.st);
+    if (rc) return rc;
+    nl += g_launches;
+    if (cudaMemcpyAsync(h + (size_t)i * cb * hpp, L.buf[1], (size_t)bi * hpp * 4, cudaMemcpyDeviceToHost, L.st) != cudaSuccess)
+      return KMX_ECUDA;
+    if (cudaMemcpyAsync(c->flags + i, L.buf[2], 4, cudaMemcpyDeviceToHost, L.st) != cudaSuccess) return KMX_ECUDA;
+  }
+  for (int l = 0; l < HOST_LANES && l < nchunks; l++)
+    if (cudaStreamSynchronize(c->lane[l].st) != cudaSuccess) return KMX_ECUDA;
+  g_launches = nl;
+  uint32_t fl = 0;
+  for (int i = 0; i < nchunks; i++) fl |= c->flags[i];
+  return status_from_flag(fl);
 }
 
 }  // namespace
@@ -411,9 +488,16 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
   HostCtx* c = host_ctx(&rc);
   if (!c) return rc;
   std::lock_guard<std::mutex> lk(c->mu);
-  if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
   const size_t fb = (size_t)batch * len_f * p.in_words * 4, gb = (size_t)batch * len_g * p.in_words * 4;
   const size_t hb = (size_t)batch * p.out_len * out_words * 4;
+  if (!limb_products64 && batch >= 2) {
+    // chunks of >= ~2 MB of output, at most HOST_MAX_CHUNKS
+    size_t nch = hb / (2u << 20);
+    if (nch > (size_t)HOST_MAX_CHUNKS) nch = HOST_MAX_CHUNKS;
+    if (nch > (size_t)batch) nch = batch;
+    if (nch >= 2) return ks_mul_host_pipelined(p, c, f, g, h, out_words, (int)nch);
+  }
+  if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
   if ((rc = ensure(*c, 0, fb + gb + 256))) return rc;
   if ((rc = ensure(*c, 1, hb))) return rc;
   if ((rc = ensure(*c, 2, p.total))) return rc;
@@ -430,6 +514,7 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
     rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, coeff_bits, flags, limb_products64, c->st);
   return rc;
 }
+
 
 size_t kmx_reconstruct_workspace_bytes(int batch, int count, int dwords) {
   if (batch < 0 || count < 1 || dwords < 1) return 0;

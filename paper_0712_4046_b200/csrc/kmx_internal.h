@@ -21,6 +21,8 @@ struct PackOp {
   long long meta_pair_stride;
   int m;                      // limbs of this operand
   int validate;               // check 0 <= c < 2^b on this operand's coefficients
+  unsigned long long* prefix; // signed path: prefix sums of the lifted coefficients (or null)
+  long long prefix_pair_stride;
 };
 struct PackArgs {
   PackOp op[8];
@@ -52,6 +54,15 @@ struct ConvArgs {
 };
 void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr);
 
+// Signed inputs (bias lift): the coefficient writers apply
+// h = h' - 2^(b-1) (J*f' + J*g') + 2^(2b-2) (J*J) before storing, from the
+// prefix sums PF, PG of the lifted inputs ([pair][lf+1 | lg+1]).
+struct BiasFix {
+  const unsigned long long* pf;
+  long long pair_stride;
+  int lf, lg, b, enabled;
+};
+
 // ---------------------------------------------------------------- finish
 // One output digit stream of one pair: digits of (P + qsign*sgn(Q)*|Q|) >> off
 // at width W (the half-sum / half-difference and the exact shifts of
@@ -77,6 +88,7 @@ struct FinishArgs {
   int mf_slot_stride;                             // operand meta: f ops at [sub], g ops at [P+sub]
   uint32_t* h; int out_words; long long h_pair_stride;
   uint32_t* dbuf; int dwords; long long dslot_stride; int dslots_pair;
+  BiasFix bias;
   uint32_t* err;
 };
 constexpr int FIN_THREADS = 256;
@@ -92,9 +104,11 @@ struct ReconArgs {
   const uint32_t* dbuf; int dwords; long long dslot_stride; int dslots_pair;
   uint32_t* h; int out_words; long long h_pair_stride;
   uint8_t* carries;           // optional [batch*ns][2*count+1]: fwd carries, rev carries
+  BiasFix bias;
   uint32_t* err;
   int rch;                    // steps per staged chunk (set by launch_recon)
   int sequential;             // force the one-thread-per-stream kernel
+  int stage;                  // k_recon_par: stream digits staged in shared memory
 };
 
 // ---------------------------------------------------------- signed (bias)

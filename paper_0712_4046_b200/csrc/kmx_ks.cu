@@ -39,111 +39,214 @@ __device__ __forceinline__ u32 block_resolve1(i64 y, i64 cin, u32* sm_scan, i64*
   return (u32)(z + c);
 }
 
+// ---- signed-input bias correction applied at store time (see BiasFix)
+__device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int128 hp, long long k, const BiasFix& bf,
+                                               long long pair) {
+  __int128 v = (__int128)hp;
+  if (bf.enabled) {
+    const unsigned long long* PF = bf.pf + pair * bf.pair_stride;
+    const unsigned long long* PG = PF + bf.lf + 1;
+    const long long lf = bf.lf, lg = bf.lg;
+    const long long i0 = k - lg + 1 > 0 ? k - lg + 1 : 0, i1 = k < lf - 1 ? k : lf - 1;
+    const long long j0 = k - lf + 1 > 0 ? k - lf + 1 : 0, j1 = k < lg - 1 ? k : lg - 1;
+    const unsigned long long sf = PF[i1 + 1] - PF[i0], sg = PG[j1 + 1] - PG[j0];
+    v = v - ((__int128)(sf + sg) << (bf.b - 1)) + ((__int128)(i1 - i0 + 1) << (2 * bf.b - 2));
+  }
+  for (int w = 0; w < ow; w++) dst[w] = w < 4 ? (u32)(v >> (32 * w)) : (v < 0 ? 0xffffffffu : 0u);
+}
+
 // ========================================================================
-// K1: pack.  One CTA per (pair, operand).  Digit q of the packed value is
-// the signed sum of the bits of every coefficient overlapping the 32-bit
-// window [32q, 32q+32) (at most two per bit position since 2N >= b,
-// pack.py:55-59), followed by a block carry scan; negated packs that come out
-// negative are two's-complement negated in a second pass (sign-magnitude,
-// as SignedBig, bignat.py:218-277).
+// K1: pack.  One CTA per (pair, operand).  The packed value is
+// V = sum_i s_i d_i 2^(iN) (d_i = c_i, or c_(L-1-i) for the reversed packs;
+// s_i = (-1)^i for the negated packs, times -1 for pack_negated_reversed at
+// even L, pack.py:62-110).  Because 2N >= b (pack.py:55-59) the even- and
+// odd-position coefficients each form a clean bitstream E, O, so digit q of
+// V is e_q + o_q (positive packs, carries in {0,1}) or |e_q - o_q| with the
+// larger stream first (negated packs; the order is decided up front by a
+// top-down warp compare of E and O, so the magnitude is produced in one pass
+// -- sign-magnitude as SignedBig, bignat.py:218-277).  Each thread owns
+// PK_V consecutive digits and walks the coefficient windows incrementally;
+// carries are resolved with one block scan of carry maps per chunk.
 // ========================================================================
-__global__ void __launch_bounds__(256) k_pack(PackArgs A) {
-  __shared__ u32 sm_scan[8];
-  __shared__ i64 sm_hi[256];
-  __shared__ int sm_sign, sm_top;
+__device__ void block_prefix_u64(const u32* x, int n, u32 bias, u32 bmask, unsigned long long* out) {
+  // out[0] = 0, out[i+1] = sum_{k<=i} ((x[k] + bias) & bmask)
+  __shared__ unsigned long long wsum[8];
+  __shared__ unsigned long long run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { run = 0; out[0] = 0; }
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int i = i0 + tid;
+    unsigned long long v = i < n ? (unsigned long long)((x[i] + bias) & bmask) : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += o;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    unsigned long long pre = run;
+    for (int k = 0; k < warp; k++) pre += wsum[k];
+    if (i < n) out[i + 1] = pre + v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) run = pre + v;
+    __syncthreads();
+  }
+}
+
+constexpr int PK_T = 256;
+constexpr int PK_V = 8;
+
+struct PackCtx {
+  const u32* cf;
+  int L, N, b, iw;
+  bool rev, bias;
+  u32 biasw, bmask;
+  __device__ __forceinline__ u32 word(int i, int w) const {  // word w of the coefficient at position i
+    if (w >= iw) return 0u;
+    const int ci = rev ? (L - 1 - i) : i;
+    u32 x = __ldg(cf + (long long)ci * iw + w);
+    if (bias) x = (x + biasw) & bmask;  // signed inputs: lift by 2^(b-1) (iw == 1)
+    return x;
+  }
+  // bits of coefficient i that fall in the 32-bit window starting at bit lo
+  __device__ __forceinline__ u32 window(int i, long long lo) const {
+    const long long s = lo - (long long)i * N;
+    if (s <= 0) return (-s) >= 32 ? 0u : (word(i, 0) << (int)(-s));
+    const int wq = (int)(s >> 5), sb = (int)(s & 31);
+    const u32 x = word(i, wq);
+    return sb ? ((x >> sb) | (word(i, wq + 1) << (32 - sb))) : x;
+  }
+  // e (even positions) and o (odd positions) bits of window q; *icur is a
+  // monotone cursor: the first position whose span may still reach window q
+  __device__ __forceinline__ void digit(int q, int* icur, u32* e, u32* o) const {
+    const long long lo = 32LL * q;
+    int i = *icur;
+    while (i < L && (long long)i * N + b <= lo) i++;
+    *icur = i;
+    u32 ev = 0u, ov = 0u;
+    for (int k = i; k < L && (long long)k * N < lo + 32; k++) {
+      const u32 x = window(k, lo);
+      if (k & 1) ov |= x; else ev |= x;
+    }
+    *e = ev;
+    *o = ov;
+  }
+};
+
+__global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
+  __shared__ u32 sm_scan[PK_T / 32];
+  __shared__ int sm_order, sm_top;
+  const int T = blockDim.x;  // 32..PK_T, sized to the operand
+  __shared__ i64 sm_carry;
   const int tid = threadIdx.x;
   const int nops = A.nops;
   const int pair = blockIdx.x / nops;
   const int o = blockIdx.x - pair * nops;
-  const u32* cf = A.op[o].coeffs + (long long)pair * A.op[o].coeff_pair_stride;
+  PackCtx C;
+  C.cf = A.op[o].coeffs + (long long)pair * A.op[o].coeff_pair_stride;
   u32* out = A.op[o].out + (long long)pair * A.op[o].out_pair_stride;
   u32* meta = A.op[o].meta + (long long)pair * A.op[o].meta_pair_stride;
-  const int L = A.op[o].len, kind = A.op[o].kind, m = A.op[o].m;
-  const int N = A.N, b = A.b, iw = A.in_words;
-  const bool neg = kind & 1, rev = (kind & 2) != 0;
-  const bool flip = (kind == 3) && ((L & 1) == 0);  // pack.py:106-109
-  const u32 bmask = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
-  const u32 biasw = A.bias ? (1u << (b - 1)) : 0u;
+  const int kind = A.op[o].kind, m = A.op[o].m;
+  C.L = A.op[o].len; C.N = A.N; C.b = A.b; C.iw = A.in_words;
+  C.rev = (kind & 2) != 0;
+  C.bias = A.bias != 0;
+  C.bmask = C.b >= 32 ? 0xffffffffu : ((1u << C.b) - 1u);
+  C.biasw = A.bias ? (1u << (C.b - 1)) : 0u;
+  const bool neg = kind & 1;
+  const bool flip = (kind == 3) && ((C.L & 1) == 0);  // pack.py:106-109
 
   if (A.op[o].validate) {  // CoeffVec invariant 0 <= c < 2^b (pack.py:36-46)
-    for (int i = tid; i < L; i += blockDim.x) {
-      const u32* c = cf + (long long)i * iw;
+    for (int i = tid; i < C.L; i += T) {
+      const u32* c = C.cf + (long long)i * C.iw;
       bool bad = false;
       if (A.bias) {
         const int v = (int)c[0];
-        if (b < 32) bad = (v < -(1 << (b - 1))) || (v >= (1 << (b - 1)));
+        if (C.b < 32) bad = (v < -(1 << (C.b - 1))) || (v >= (1 << (C.b - 1)));
       } else {
-        for (int w = 0; w < iw; w++) {
+        for (int w = 0; w < C.iw; w++) {
           const int lo_bit = 32 * w;
-          if (lo_bit >= b) bad |= c[w] != 0u;
-          else if (b - lo_bit < 32) bad |= (c[w] >> (b - lo_bit)) != 0u;
+          if (lo_bit >= C.b) bad |= c[w] != 0u;
+          else if (C.b - lo_bit < 32) bad |= (c[w] >> (C.b - lo_bit)) != 0u;
         }
       }
       if (bad) raise_err(A.err, ERR_INVAL);
     }
   }
-  if (tid == 0) { sm_sign = 0; sm_top = 0; }
-
-  i64 carry = 0;
-  int my_top = 0;
-  for (int q0 = 0; q0 <= m; q0 += blockDim.x) {
-    const int q = q0 + tid;
-    i64 y = 0;
-    if (q < m) {
-      const long long wlo = 32LL * q;
-      const long long t = wlo - b;
-      int ilo = t >= 0 ? (int)(t / N) + 1 : 0;
-      int ihi = (int)((wlo + 31) / N);
-      if (ihi > L - 1) ihi = L - 1;
-      for (int i = ilo; i <= ihi; i++) {
-        const int ci = rev ? (L - 1 - i) : i;
-        const u32* c = cf + (long long)ci * iw;
-        const long long s = wlo - (long long)i * N;  // coefficient bit at window start
-        u32 x;
-        if (s <= 0) {
-          u32 c0 = c[0];
-          if (A.bias) c0 = (c0 + biasw) & bmask;
-          x = c0 << (int)(-s);
-        } else {
-          const int wq = (int)(s >> 5), sb = (int)(s & 31);
-          u32 lo = wq < iw ? c[wq] : 0u;
-          u32 hi = (wq + 1) < iw ? c[wq + 1] : 0u;
-          if (A.bias) { lo = wq == 0 ? ((lo + biasw) & bmask) : lo; }
-          x = sb ? ((lo >> sb) | (hi << (32 - sb))) : lo;
-        }
-        bool minus = neg && (i & 1);
-        if (flip) minus = !minus;
-        y += minus ? -(i64)x : (i64)x;
+  if (A.op[o].prefix) {  // signed path: prefix sums of the lifted coefficients
+    block_prefix_u64(C.cf, C.L, C.biasw, C.bmask, A.op[o].prefix + (long long)pair * A.op[o].prefix_pair_stride);
+    __syncthreads();
+  }
+  if (tid == 0) { sm_top = 0; sm_order = 1; sm_carry = 0; }
+  // negated packs: order of E and O from the most significant differing digit
+  if (neg && tid < 32) {
+    int order = 0;  // +1: E > O, -1: E < O, 0: equal
+    for (int base = m - 1; base >= 0 && order == 0; base -= 32) {
+      const int q = base - tid;
+      u32 e = 0u, ov = 0u;
+      if (q >= 0) {
+        int ic = 0;
+        const long long t = 32LL * q - C.b;
+        if (t >= 0) ic = (int)(t / C.N) + 1;
+        C.digit(q, &ic, &e, &ov);
+      }
+      const unsigned diff = __ballot_sync(0xffffffffu, e != ov);
+      if (diff) {
+        const int l = __ffs(diff) - 1;  // lowest lane = highest digit
+        const int gt = __shfl_sync(0xffffffffu, e > ov ? 1 : 0, l);
+        order = gt ? 1 : -1;
       }
     }
-    i64 cout;
-    const u32 d = block_resolve1(y, carry, sm_scan, sm_hi, &cout);
-    carry = cout;
-    if (q < m) {
-      out[q] = d;
-      if (d) my_top = q + 1;
-    } else if (q == m) {
-      if (d == 0xffffffffu) sm_sign = 1;
-      else if (d != 0u) raise_err(A.err, ERR_INEXACT);  // operand overflow (cannot happen)
-    }
+    if (tid == 0) sm_order = order >= 0 ? 1 : -1;
   }
   __syncthreads();
-  const int negative = sm_sign;
-  if (negative) {  // magnitude = ~D + 1 (mod 2^(32m))
-    my_top = 0;
-    carry = 1;
-    for (int q0 = 0; q0 < m; q0 += blockDim.x) {
-      const int q = q0 + tid;
-      const i64 y = q < m ? (i64)(u32)(~out[q]) : 0;
-      i64 cout;
-      const u32 d = block_resolve1(y, carry, sm_scan, sm_hi, &cout);
-      carry = cout;
-      if (q < m) {
-        out[q] = d;
-        if (d) my_top = q + 1;
-      }
+  const int order = sm_order;  // E - O (order 1) or O - E (order -1)
+  const int negative = neg ? ((order < 0) != flip ? 1 : 0) : 0;
+
+  int my_top = 0;
+  for (int c0 = 0; c0 < m; c0 += T * PK_V) {
+    const int q0 = c0 + tid * PK_V;
+    i64 t[PK_V];
+    int ic = 0;
+    {
+      const long long tt = 32LL * q0 - C.b;
+      if (tt >= 0) ic = (int)(tt / C.N) + 1;
     }
+    u32 M = CM_IDENT, mr[PK_V];
+#pragma unroll
+    for (int v = 0; v < PK_V; v++) {
+      const int q = q0 + v;
+      u32 e = 0u, ov = 0u;
+      if (q < m) C.digit(q, &ic, &e, &ov);
+      t[v] = !neg ? (i64)e + ov : (order > 0 ? (i64)e - ov : (i64)ov - e);
+      mr[v] = cm_make(t[v]);
+      M = cm_compose(M, mr[v]);
+    }
+    u32 tot;
+    const u32 exc = cm_seg_scan(M, T, sm_scan, &tot);
+    const int cin = (int)sm_carry;
+    int c = cm_apply(exc, cin);
+    u32 d[PK_V];
+#pragma unroll
+    for (int v = 0; v < PK_V; v++) {
+      d[v] = (u32)(t[v] + c);
+      c = cm_apply(mr[v], c);
+      if (q0 + v < m && d[v]) my_top = q0 + v + 1;
+    }
+    if (q0 + PK_V <= m) {
+      uint4* dst = reinterpret_cast<uint4*>(out + q0);
+      dst[0] = make_uint4(d[0], d[1], d[2], d[3]);
+      dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++)
+        if (q0 + v < m) out[q0 + v] = d[v];
+    }
+    __syncthreads();
+    if (tid == 0) sm_carry = cm_apply(tot, cin);
+    __syncthreads();
   }
+  if (tid == 0 && sm_carry != 0) raise_err(A.err, ERR_INEXACT);  // operand overflow (cannot happen)
   atomicMax(&sm_top, my_top);
   __syncthreads();
   if (tid == 0) {
@@ -154,7 +257,11 @@ __global__ void __launch_bounds__(256) k_pack(PackArgs A) {
 }
 
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
-  k_pack<<<batch * a.nops, 256, 0, st>>>(a);
+  int mmax = 0;
+  for (int i = 0; i < a.nops; i++) mmax = a.op[i].m > mmax ? a.op[i].m : mmax;
+  int T = 32;
+  while (T < PK_T && T * PK_V < mmax) T <<= 1;
+  k_pack<<<batch * a.nops, T, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -167,25 +274,27 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
 // above off + cnt*W must be zero and the value non-negative; violations
 // latch ERR_INEXACT (the reference raises ValueError there).
 // ========================================================================
-__device__ __forceinline__ i64 prod_digit(const u32* P, const unsigned long long* sp, int q, int mp, int C) {
+constexpr int FN_T = 256;
+constexpr int FN_V = 8;
+constexpr int FN_CH = FN_T * FN_V;  // limbs per chunk
+
+__device__ __forceinline__ i64 prod_digit(const u32* P, const unsigned long long* sp, int q, int mp, int lgC) {
   if (q >= mp) return 0;
   i64 y = P[q];
-  const int bnd = q / C, r = q - bnd * C;
-  if (bnd > 0) {
-    if (r == 0) y += (i64)sp[(bnd - 1) * 2 + 0];
-    else if (r == 1) y += (i64)sp[(bnd - 1) * 2 + 1];
-  }
+  const int bnd = q >> lgC, r = q & ((1 << lgC) - 1);
+  if (bnd > 0 && r < 2) y += (i64)sp[(bnd - 1) * 2 + r];
   return y;
 }
 
-__global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
-  __shared__ u32 buf[FIN_HALO + FIN_THREADS];
-  __shared__ u32 sm_scan[FIN_THREADS / 32];
-  __shared__ i64 sm_hi[FIN_THREADS];
+__global__ void __launch_bounds__(FN_T) k_finish(FinishArgs a) {
+  __shared__ u32 buf[FIN_HALO + FN_CH];
+  __shared__ u32 sm_scan[FN_T / 32];
+  __shared__ i64 sm_hi[FN_T];
+  __shared__ i64 sm_cin;
   const int tid = threadIdx.x;
   const int pair = blockIdx.x / a.ns;
   const int si = blockIdx.x - pair * a.ns;
-  const Stream S = a.s[si];
+  const Stream S = si == 0 ? a.s[0] : (si == 1 ? a.s[1] : (si == 2 ? a.s[2] : a.s[3]));
   const long long zP = (long long)pair * a.nprod_pair + S.zP;
   const u32* Pp = a.P + zP * a.p_stride;
   const unsigned long long* spP = a.spill + zP * a.nbands * 2;
@@ -197,51 +306,90 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
     Qp = a.P + zQ * a.p_stride;
     spQ = a.spill + zQ * a.nbands * 2;
     const u32* mt = a.meta + (long long)pair * a.meta_per_pair;
-    const u32 neg = mt[2 * S.qmeta] ^ mt[2 * (S.qmeta + a.mf_slot_stride)];  // mul_signed: xor
-    sg = neg ? -S.qsign : S.qsign;
+    const u32 ngt = mt[2 * S.qmeta] ^ mt[2 * (S.qmeta + a.mf_slot_stride)];  // mul_signed: xor
+    sg = ngt ? -S.qsign : S.qsign;
   }
   const long long off = S.off;
   const int W = S.W;
   const int Wd = (W + 31) >> 5;
   const long long E = off + (long long)S.cnt * W;
-  const int C = a.band_cols;
+  const int lgC = 31 - __clz(a.band_cols);
   const int mp = a.mp;
   int Qd = mp + 1;
   const long long qe = (E + 31) / 32 + 1;
   if (qe > Qd) Qd = (int)qe;
   if (tid < FIN_HALO) buf[tid] = 0u;
-  i64 carry = 0;
-  for (int q0 = 0; q0 < Qd; q0 += FIN_THREADS) {
-    const int q = q0 + tid;
-    i64 y = prod_digit(Pp, spP, q, mp, C);
-    if (sg) y += sg * prod_digit(Qp, spQ, q, mp, C);
-    i64 cout;
-    const u32 d = block_resolve1(y, carry, sm_scan, sm_hi, &cout);
-    carry = cout;
-    buf[FIN_HALO + tid] = d;
-    const long long bit0 = 32LL * q;
-    if (bit0 < off) {
-      const long long nb = off - bit0;
-      const u32 msk = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
-      if (d & msk) raise_err(a.err, ERR_INEXACT);
+  if (tid == 0) sm_cin = 0;  // carry into the chunk (small, any sign)
+  __syncthreads();
+  for (int q00 = 0; q00 < Qd; q00 += FN_CH) {
+    const int q0 = q00 + tid * FN_V;
+    u32 lo[FN_V];
+    i64 hi[FN_V];
+#pragma unroll
+    for (int v = 0; v < FN_V; v++) {
+      i64 y = prod_digit(Pp, spP, q0 + v, mp, lgC);
+      if (sg) y += sg * prod_digit(Qp, spQ, q0 + v, mp, lgC);
+      lo[v] = (u32)y;
+      hi[v] = y >> 32;
     }
-    if (bit0 + 32 > E) {
-      const long long from = E - bit0;
-      const u32 msk = from <= 0 ? 0xffffffffu : (0xffffffffu << from);
-      if (d & msk) raise_err(a.err, ERR_INEXACT);
+    sm_hi[tid] = hi[FN_V - 1];
+    __syncthreads();
+    const i64 cin_chunk = sm_cin;
+    const i64 hprev = tid ? sm_hi[tid - 1] : cin_chunk;
+    const i64 hlast = sm_hi[FN_T - 1];
+    i64 z[FN_V];
+    u32 mr[FN_V], M = CM_IDENT;
+#pragma unroll
+    for (int v = 0; v < FN_V; v++) {
+      z[v] = (i64)lo[v] + (v ? hi[v - 1] : hprev);
+      mr[v] = cm_make(z[v]);
+      M = cm_compose(M, mr[v]);
+    }
+    u32 tot;
+    const u32 exc = cm_seg_scan(M, FN_T, sm_scan, &tot);
+    int c = cm_apply(exc, 0);
+#pragma unroll
+    for (int v = 0; v < FN_V; v++) {
+      const u32 d = (u32)(z[v] + c);
+      c = cm_apply(mr[v], c);
+      buf[FIN_HALO + tid * FN_V + v] = d;
+      const long long bit0 = 32LL * (q0 + v);
+      if (bit0 < off) {
+        const long long nb = off - bit0;
+        const u32 msk = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
+        if (d & msk) raise_err(a.err, ERR_INEXACT);
+      }
+      if (bit0 + 32 > E && q0 + v < Qd) {
+        const long long from = E - bit0;
+        const u32 msk = from <= 0 ? 0xffffffffu : (0xffffffffu << from);
+        if (d & msk) raise_err(a.err, ERR_INEXACT);
+      }
     }
     __syncthreads();
-    const long long clo = 32LL * q0, chi = 32LL * (q0 + FIN_THREADS);
+    if (tid == 0) sm_cin = (i64)cm_apply(tot, 0) + hlast;
+    const long long clo = 32LL * q00, chi = 32LL * (q00 + FN_CH);
     const long long t = clo - off + 1;
     long long jl = t <= 0 ? 0 : (t + W - 1) / W - 1;
     if (jl < 0) jl = 0;
     const long long u = chi - off;
     long long jh = u <= 0 ? 0 : u / W;
     if (jh > S.cnt) jh = S.cnt;
-    for (long long j = jl + tid; j < jh; j += FIN_THREADS) {
-      const long long lb = off + j * W - 32LL * (q0 - FIN_HALO);
+    for (long long j = jl + tid; j < jh; j += FN_T) {
+      const long long lb = off + j * W - 32LL * (q00 - FIN_HALO);
       u32* dst;
       int ow;
+      if (S.mode == 0 && a.bias.enabled) {
+        unsigned __int128 hp = 0;
+        for (int w = 0; w < Wd && w < 4; w++) {
+          u32 x = bits32(buf, FIN_HALO + FN_CH, lb + 32 * w);
+          const int rem = W - 32 * w;
+          if (rem < 32) x &= (1u << rem) - 1u;
+          hp |= (unsigned __int128)x << (32 * w);
+        }
+        const long long kpos = S.pos0 + j * S.pstride;
+        store_coeff128(a.h + (long long)pair * a.h_pair_stride + kpos * a.out_words, a.out_words, hp, kpos, a.bias, pair);
+        continue;
+      }
       if (S.mode == 0) {
         dst = a.h + (long long)pair * a.h_pair_stride + (long long)(S.pos0 + j * S.pstride) * a.out_words;
         ow = a.out_words;
@@ -253,7 +401,7 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
       for (int w = 0; w < ow; w++) {
         u32 x = 0u;
         if (w < Wd) {
-          x = bits32(buf, FIN_HALO + FIN_THREADS, lb + 32 * w);
+          x = bits32(buf, FIN_HALO + FN_CH, lb + 32 * w);
           const int rem = W - 32 * w;
           if (rem < 32) x &= (1u << rem) - 1u;
         }
@@ -261,14 +409,14 @@ __global__ void __launch_bounds__(FIN_THREADS) k_finish(FinishArgs a) {
       }
     }
     __syncthreads();
-    if (tid < FIN_HALO) buf[tid] = buf[FIN_THREADS + tid];
+    if (tid < FIN_HALO) buf[tid] = buf[FN_CH + tid];
     __syncthreads();
   }
-  if (tid == 0 && carry != 0) raise_err(a.err, ERR_INEXACT);
+  if (tid == 0 && sm_cin != 0) raise_err(a.err, ERR_INEXACT);
 }
 
 cudaError_t launch_finish(const FinishArgs& a, int batch, cudaStream_t st) {
-  k_finish<<<batch * a.ns, FIN_THREADS, 0, st>>>(a);
+  k_finish<<<batch * a.ns, FN_T, 0, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -592,6 +740,7 @@ __global__ void __launch_bounds__(32 * RECON_WARPS) k_recon(ReconArgs a) {
 // RECON_MAXIT rounds, thread 0 runs the whole stream sequentially.
 // ========================================================================
 constexpr int RECON_MAXIT = 8;
+constexpr int RECON_PAR_MAXT = 512;
 
 template <int NW>
 __device__ __forceinline__ void mw_add_small(MW<NW>& r, const MW<NW>& x, int e) {
@@ -684,6 +833,12 @@ __device__ void block_exscan_i2(int& x0, int& x1, int* sm) {
 }
 
 template <int NW>
+__device__ __forceinline__ void mw_ld(MW<NW>& x, const u32* p) {
+#pragma unroll
+  for (int i = 0; i < NW; i++) x.w[i] = p[i];
+}
+
+template <int NW>
 struct ReconState {
   MW<NW> lo_prev, lo_cur, rj;  // lo[j-1], lo[j], rev[j]
   u32 fc;                      // delta_j
@@ -691,47 +846,83 @@ struct ReconState {
 
 // Run steps [j0, j1) of the reference recurrence from state st; writes the
 // coefficients; accumulates e_j into esum[(j+1)&1]; latches out-of-range hi.
-template <int NW>
+template <int NW, bool STORE>
 __device__ __forceinline__ void recon_walk(ReconState<NW>& st, int j0, int j1, const u32* F, const u32* R, int dw,
                                            u32* H, int pos0, int pstride, int ow, int W, u32 topmask,
-                                           const MW<NW>& mask, int& e0, int& e1, bool& bad) {
-  MW<NW> zero;
-#pragma unroll
-  for (int i = 0; i < NW; i++) zero.w[i] = 0u;
-  for (int j = j0; j < j1; j++) {
-    MW<NW> rj1, fj1, h, nxt;
-    mw_load(rj1, R + (long long)(j + 1) * dw);
-    mw_load(fj1, F + (long long)(j + 1) * dw);
-    const u32 eps = mw_gt(st.lo_cur, rj1) ? 1u : 0u;  // ksint.py:154 (strict)
-    mw_sub(h, st.rj, st.lo_prev, eps);
-    mw_mask(h, topmask);
-    bad |= mw_eq(h, mask);                           // ksint.py:157-158
-    const u32 br = mw_sub(nxt, fj1, h, st.fc);       // borrow <=> h + fc > fwd[j+1]
-    mw_mask(nxt, topmask);
-    write_coeff(H + (long long)(pos0 + (long long)j * pstride) * ow, ow, st.lo_cur, h, W);
-    const int ej = (int)eps - (int)st.fc;
-    if ((j + 1) & 1) e1 += ej; else e0 += ej;
-    st.fc = br;
-    st.lo_prev = st.lo_cur;
-    st.lo_cur = nxt;
-    st.rj = rj1;
+                                           const MW<NW>& mask, int& e0, int& e1, bool& bad,
+                                           const BiasFix& bf, long long pair) {
+  if constexpr (NW <= 2) {
+    // native 64-bit digits
+    const u64 m64 = W >= 64 ? ~0ull : ((1ull << W) - 1ull);
+    auto ld = [&](const u32* p) -> u64 { return NW == 1 ? (u64)p[0] : ((u64)p[0] | ((u64)p[1] << 32)); };
+    u64 lo_prev = st.lo_prev.w[0], lo_cur = st.lo_cur.w[0], rj = st.rj.w[0];
+    if (NW == 2) {
+      lo_prev |= (u64)st.lo_prev.w[NW - 1] << 32;
+      lo_cur |= (u64)st.lo_cur.w[NW - 1] << 32;
+      rj |= (u64)st.rj.w[NW - 1] << 32;
+    }
+    u32 fc = st.fc;
+    for (int j = j0; j < j1; j++) {
+      const u64 rj1 = ld(R + (j + 1) * dw), fj1 = ld(F + (j + 1) * dw);
+      const u32 eps = lo_cur > rj1;                     // ksint.py:154 (strict)
+      const u64 h = (rj - lo_prev - eps) & m64;
+      bad |= h == m64;                                  // ksint.py:157-158
+      const u64 nxt = (fj1 - h - fc) & m64;
+      const u32 br = h + fc > fj1;
+      u64 v0, v1;
+      if (W >= 64) { v0 = lo_cur; v1 = h; }
+      else { v0 = lo_cur | (h << W); v1 = h >> (64 - W); }
+      const long long kpos = pos0 + (long long)j * pstride;
+      u32* dst = H + kpos * ow;
+      if (!STORE) {
+      } else if (bf.enabled) {
+        store_coeff128(dst, ow, (unsigned __int128)v0 | ((unsigned __int128)v1 << 64), kpos, bf, pair);
+      } else {
+        dst[0] = (u32)v0;
+        if (ow > 1) dst[1] = (u32)(v0 >> 32);
+        if (ow > 2) dst[2] = (u32)v1;
+        if (ow > 3) dst[3] = (u32)(v1 >> 32);
+        for (int w = 4; w < ow; w++) dst[w] = 0u;
+      }
+      const int ej = (int)eps - (int)fc;
+      if ((j + 1) & 1) e1 += ej; else e0 += ej;
+      fc = br;
+      lo_prev = lo_cur;
+      lo_cur = nxt;
+      rj = rj1;
+    }
+    st.lo_prev.w[0] = (u32)lo_prev; st.lo_cur.w[0] = (u32)lo_cur; st.rj.w[0] = (u32)rj;
+    if (NW == 2) {
+      st.lo_prev.w[NW - 1] = (u32)(lo_prev >> 32);
+      st.lo_cur.w[NW - 1] = (u32)(lo_cur >> 32);
+      st.rj.w[NW - 1] = (u32)(rj >> 32);
+    }
+    st.fc = fc;
+  } else {
+    for (int j = j0; j < j1; j++) {
+      MW<NW> rj1, fj1, h, nxt;
+      mw_ld(rj1, R + (long long)(j + 1) * dw);
+      mw_ld(fj1, F + (long long)(j + 1) * dw);
+      const u32 eps = mw_gt(st.lo_cur, rj1) ? 1u : 0u;  // ksint.py:154 (strict)
+      mw_sub(h, st.rj, st.lo_prev, eps);
+      mw_mask(h, topmask);
+      bad |= mw_eq(h, mask);                           // ksint.py:157-158
+      const u32 br = mw_sub(nxt, fj1, h, st.fc);       // borrow <=> h + fc > fwd[j+1]
+      mw_mask(nxt, topmask);
+      if (STORE) write_coeff(H + (long long)(pos0 + (long long)j * pstride) * ow, ow, st.lo_cur, h, W);
+      const int ej = (int)eps - (int)st.fc;
+      if ((j + 1) & 1) e1 += ej; else e0 += ej;
+      st.fc = br;
+      st.lo_prev = st.lo_cur;
+      st.lo_cur = nxt;
+      st.rj = rj1;
+    }
   }
-  (void)zero;
 }
 
-constexpr int RECON_PAR_MAXT = 512;
-
 template <int NW>
-__global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
-  __shared__ u32 smw[2 * 17 * 32];
-  __shared__ int smi[64];
-  __shared__ uint8_t dend[RECON_PAR_MAXT];
-  __shared__ int fallback;
-  const int sid = blockIdx.x;
-  const int pair = sid / a.ns, si = sid - pair * a.ns;
-  const ReconStream S = si == 0 ? a.s[0] : a.s[1];
-  const u32* F = a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride;
-  const u32* R = a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride;
+__device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconStream& S, int pair, const u32* F,
+                                               const u32* R, u32* smw, int* smi, uint8_t* dend, int* fallback) {
   u32* H = a.h + (long long)pair * a.h_pair_stride;
   const int W = a.W, dw = a.dwords, ow = a.out_words, count = S.count;
   const int nsteps = count - 1;
@@ -750,23 +941,23 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
   MW<NW> cs0 = zero, cs1 = zero;
   for (int j = s0; j < s1; j++) {
     MW<NW> f1, r0, c;
-    mw_load(f1, F + (long long)(j + 1) * dw);
-    mw_load(r0, R + (long long)j * dw);
+    mw_ld(f1, F + (long long)(j + 1) * dw);
+    mw_ld(r0, R + (long long)j * dw);
     mw_sub(c, f1, r0, 0u);
     if ((j + 1) & 1) mw_add(cs1, cs1, c); else mw_add(cs0, cs0, c);
   }
   block_exscan_mw2(cs0, cs1, smw);
   MW<NW> f0;
-  mw_load(f0, F);
+  mw_ld(f0, F);
   mw_add(cs0, cs0, f0);  // even chain starts at lo[0] = fwd[0], odd at lo[-1] = 0
   mw_mask(cs0, topmask);
   mw_mask(cs1, topmask);
   // guesses
   int E0 = 0, E1 = 0;  // corrections at the segment start, by parity
   u32 dstart = 0;      // delta at the segment start
-  if (tid == 0) fallback = 0;
+  if (tid == 0) *fallback = 0;
   bool bad = false;
-  ReconState<NW> st;
+  ReconState<NW> st, st0;
   bool converged = false;
   for (int it = 0; it < RECON_MAXIT && !converged; it++) {
     // start state (lo[s0-1], lo[s0], delta_s0)
@@ -779,11 +970,12 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
       mw_add_small(st.lo_prev, p ? cs0 : cs1, p ? E0 : E1);
       mw_mask(st.lo_prev, topmask);
     }
-    mw_load(st.rj, R + (long long)s0 * dw);
+    mw_ld(st.rj, R + (long long)s0 * dw);
     st.fc = dstart;
     int n0 = 0, n1 = 0;
     bad = false;
-    recon_walk(st, s0, s1, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, bad);
+    st0 = st;
+    recon_walk<NW, false>(st, s0, s1, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, bad, a.bias, pair);
     // next guesses
     block_exscan_i2(n0, n1, smi);
     dend[tid] = (uint8_t)st.fc;
@@ -793,26 +985,32 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
     converged = __syncthreads_and(same);
     E0 = n0; E1 = n1; dstart = dnew;
   }
+  if (converged) {  // output walk from the verified start state
+    ReconState<NW> sw = st0;
+    int q0 = 0, q1 = 0;
+    bool b3 = false;
+    recon_walk<NW, true>(sw, s0, s1, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, b3, a.bias, pair);
+  }
   if (!converged) {
     if (tid == 0) {
-      fallback = 1;
+      *fallback = 1;
       st.lo_prev = zero;
       st.lo_cur = f0;
-      mw_load(st.rj, R);
+      mw_ld(st.rj, R);
       st.fc = 0u;
       int q0 = 0, q1 = 0;
       bad = false;
-      recon_walk(st, 0, nsteps, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad);
+      recon_walk<NW, true>(st, 0, nsteps, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, a.bias, pair);
     }
     __syncthreads();
   }
   // the thread owning the last step finishes (ksint.py:170-177)
-  const int owner = fallback ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
+  const int owner = *fallback ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
   if (tid == owner) {
     if (nsteps == 0) {
       st.lo_prev = zero;
       st.lo_cur = f0;
-      mw_load(st.rj, R);
+      mw_ld(st.rj, R);
       st.fc = 0u;
     }
     MW<NW> h;
@@ -820,15 +1018,60 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
     mw_mask(h, topmask);
     bool b2 = mw_eq(h, mask);
     MW<NW> rlast, flast, hs;
-    mw_load(rlast, R + (long long)count * dw);
-    mw_load(flast, F + (long long)count * dw);
+    mw_ld(rlast, R + (long long)count * dw);
+    mw_ld(flast, F + (long long)count * dw);
     b2 |= !mw_eq(st.lo_cur, rlast);
     const u32 br = mw_sub(hs, flast, h, st.fc);
     b2 |= (br != 0u) || !mw_is_zero(hs);
-    write_coeff(H + (long long)(S.pos0 + (long long)(count - 1) * S.pstride) * ow, ow, st.lo_cur, h, W);
+    {
+      const long long kpos = S.pos0 + (long long)(count - 1) * S.pstride;
+      if (a.bias.enabled && NW <= 2) {
+        unsigned __int128 lo128 = st.lo_cur.w[0], hi128 = h.w[0];
+        if (NW == 2) { lo128 |= (unsigned __int128)st.lo_cur.w[NW - 1] << 32; hi128 |= (unsigned __int128)h.w[NW - 1] << 32; }
+        store_coeff128(H + kpos * ow, ow, lo128 | (hi128 << W), kpos, a.bias, pair);
+      } else {
+        write_coeff(H + kpos * ow, ow, st.lo_cur, h, W);
+      }
+    }
     if (b2) raise_err(a.err, ERR_RECON);
   }
-  if (bad && (!fallback || tid == 0)) raise_err(a.err, ERR_RECON);
+  if (bad && (!*fallback || tid == 0)) raise_err(a.err, ERR_RECON);
+}
+
+template <int NW>
+__global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
+  __shared__ u32 smw[2 * 17 * 32];
+  __shared__ int smi[64];
+  __shared__ uint8_t dend[RECON_PAR_MAXT];
+  __shared__ int fallback;
+  extern __shared__ u32 rst[];
+  const int sid = blockIdx.x;
+  const int pair = sid / a.ns, si = sid - pair * a.ns;
+  const ReconStream S = si == 0 ? a.s[0] : a.s[1];
+  const u32* F = a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride;
+  const u32* R = a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride;
+  if (a.stage) {  // whole stream resident in shared memory for all walks (cp.async, all in flight)
+    const int nw = (S.count + 1) * a.dwords;
+    for (int x = threadIdx.x; x < nw; x += blockDim.x) {
+      cp_async4(rst + x, F + x);
+      cp_async4(rst + nw + x, R + x);
+    }
+    ReconArgs b = a;
+    if (a.bias.enabled) {  // prefix sums of the lifted inputs next to the digits
+      const int np = 2 * (a.bias.lf + a.bias.lg + 2);  // u32 words
+      u32* pdst = rst + 2 * nw + ((2 * nw) & 1);      // 8-byte aligned
+      const u32* psrc = reinterpret_cast<const u32*>(a.bias.pf + (long long)pair * a.bias.pair_stride);
+      for (int x = threadIdx.x; x < np; x += blockDim.x) cp_async4(pdst + x, psrc + x);
+      b.bias.pf = reinterpret_cast<const unsigned long long*>(pdst);
+      b.bias.pair_stride = 0;
+    }
+    cp_async_commit();
+    cp_async_wait<0>();
+    __syncthreads();
+    recon_par_body<NW>(b, S, pair, rst, rst + nw, smw, smi, dend, &fallback);
+  } else {
+    recon_par_body<NW>(a, S, pair, F, R, smw, smi, dend, &fallback);
+  }
 }
 
 template <int NW>
@@ -838,7 +1081,15 @@ static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStre
   T = ((T + 31) / 32) * 32;
   if (T < 32) T = 32;
   if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;
-  k_recon_par<NW><<<a.batch * a.ns, T, 0, st>>>(a);
+  ReconArgs b = a;
+  size_t smem = (size_t)2 * (maxcount + 1) * a.dwords * sizeof(u32) + 8;
+  if (a.bias.enabled) smem += (size_t)(a.bias.lf + a.bias.lg + 2) * 8;
+  b.stage = smem <= 160 * 1024;
+  if (b.stage && smem > 32 * 1024) {  // dynamic + ~5 KB static must fit the opt-in limit
+    cudaError_t e = cudaFuncSetAttribute(k_recon_par<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_recon_par<NW><<<a.batch * a.ns, T, b.stage ? smem : 0, st>>>(b);
   return cudaGetLastError();
 }
 
@@ -912,32 +1163,6 @@ cudaError_t launch_recon(const ReconArgs& a0, cudaStream_t st) {
 // h = h' - 2^(b-1) (J*f' + J*g') + 2^(2b-2) (J*J), J the all-ones vector
 // (sliding window sums via prefix sums).  One CTA per pair.
 // ========================================================================
-__device__ void block_prefix_u64(const u32* x, int n, u32 bias, u32 bmask, unsigned long long* out) {
-  // out[0] = 0, out[i+1] = sum_{k<=i} ((x[k] + bias) & bmask)
-  __shared__ unsigned long long wsum[8];
-  __shared__ unsigned long long run;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) { run = 0; out[0] = 0; }
-  __syncthreads();
-  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int i = i0 + tid;
-    unsigned long long v = i < n ? (unsigned long long)((x[i] + bias) & bmask) : 0ull;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, v, off);
-      if (lane >= off) v += o;
-    }
-    if (lane == 31) wsum[warp] = v;
-    __syncthreads();
-    unsigned long long pre = run;
-    for (int k = 0; k < warp; k++) pre += wsum[k];
-    if (i < n) out[i + 1] = pre + v;
-    __syncthreads();
-    if (tid == blockDim.x - 1) run = pre + v;
-    __syncthreads();
-  }
-}
-
 __global__ void __launch_bounds__(256) k_bias(BiasArgs a) {
   const int pair = blockIdx.x;
   const int lf = a.lf, lg = a.lg, b = a.b;

@@ -263,3 +263,21 @@ def test_full_config2_checksum(kmx, variant):
     ge = _eval_mod(g[:, :, 0].tolist(), x, p)
     he = _eval_mod(hv, x, p)
     assert all((a * c - d) % p == 0 for a, c, d in zip(fe, ge, he))
+
+
+@pytest.mark.parametrize("variant", [1, 4])
+def test_host_pipelined_path(kmx, variant):
+    # the host API splits large batches into chunks over several streams;
+    # an uneven batch exercises the tail chunk
+    rng = np.random.default_rng(77)
+    B, n = 777, 1024
+    f = rng.integers(-2**31, 2**31, size=(B, n, 1), dtype=np.int64).astype(np.int32).view(np.uint32)
+    g = rng.integers(-2**31, 2**31, size=(B, n, 1), dtype=np.int64).astype(np.int32).view(np.uint32)
+    fp = torch.from_numpy(f.view(np.int32)).pin_memory().numpy().view(np.uint32)
+    gp = torch.from_numpy(g.view(np.int32)).pin_memory().numpy().view(np.uint32)
+    h = kmx.ks_mul_host(variant, fp, gp, 32, signed=True)
+    from paper_0712_4046_b200.words import words_to_ints
+    for p in (0, 388, 776):
+        want = O.ks_mul_signed(1, [int(x) for x in f[p, :, 0].view(np.int32)],
+                               [int(x) for x in g[p, :, 0].view(np.int32)], 32, mode="native")
+        assert words_to_ints(h[p], signed=True) == want
