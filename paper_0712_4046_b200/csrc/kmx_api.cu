@@ -226,7 +226,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   unsigned long long* spill = (unsigned long long*)(w + p.off_spill);
   uint32_t* dbuf = (uint32_t*)(w + p.off_dbuf);
   unsigned long long* scr = (unsigned long long*)(w + p.off_scr);
-  cudaError_t e = cudaMemsetAsync(err, 0, 4, st);
+  cudaError_t e = cudaMemsetAsync(err, 0, 8, st);  // error flag + multiply work counter
   if (e != cudaSuccess) return KMX_ECUDA;
 
   PackArgs pa;
@@ -264,6 +264,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.B = opg; ma.b_stride = p.mgs; ma.mb = p.mg;
   ma.P = prod; ma.p_stride = p.ps; ma.spill = spill;
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
+  ma.counter = (int*)(err + 1);
   prof_begin(1, st);
   if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
   prof_end(1, st);

@@ -158,6 +158,7 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   ca.L = p.Lu;
   ca.P = prods; ca.p_stride = ps;
   ca.nprod = p.batch * p.P; ca.nbands = nbands; ca.G = split; ca.TI = tr;
+  ca.counter = (int*)(err + 1);
   if ((e = launch_conv(ca, st)) != cudaSuccess) return e;
   (*nlaunch)++;
   k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err);
@@ -228,7 +229,7 @@ int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits, const in
   cudaStream_t st = (cudaStream_t)stream;
   char* w = (char*)workspace;
   uint32_t* err = (uint32_t*)w;
-  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMemsetAsync(err, 0, 8, st) != cudaSuccess) return KMX_ECUDA;  // error flag + work counter
   int nl = 0;
   cudaError_t e = launch_bivar(p, f, g, h, (int32_t*)(w + oe), (int64_t*)(w + op), err, st, &nl);
   g_launches = nl;

@@ -44,6 +44,7 @@ struct MulArgs {
   uint32_t* P; long long p_stride;                // digits, p_stride >= nbands*CW
   unsigned long long* spill;                      // [z][nbands][2]
   int nprod, nbands, G, TI;
+  int* counter;                                   // work-unit counter, zeroed before launch
 };
 struct ConvArgs {
   const int32_t* A; long long a_stride;
@@ -51,6 +52,7 @@ struct ConvArgs {
   int L;                                          // operand length (both)
   int64_t* P; long long p_stride;                 // 2L-1 int64 column sums
   int nprod, nbands, G, TI;
+  int* counter;                                   // work-unit counter, zeroed before launch
 };
 void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr);
 

@@ -20,6 +20,8 @@
 // register block: per 64 limb products two broadcast LDS.128 for a and two
 // LDS.128 for the sliding b window, whose two 8-word halves swap roles every
 // block (no register moves).
+#include <cstdlib>
+
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
 
@@ -102,208 +104,252 @@ __device__ __forceinline__ void walk(ACC& acc, const u32* ap, const u32* bp, int
   }
 }
 
-struct BandGeom {
-  int K0, Kw, ilo, ihi, gb_lo, gb_hi;  // global 8-row blocks [gb_lo, gb_hi) of this group
-};
+// ------------------------------------------------------------------------
+// Persistent warp workers.  A work unit is one band (CW columns) of one
+// product; every warp repeatedly claims the next unit from a global counter
+// (longest-first: bands from the middle of each product outwards, products
+// interleaved), stages the operand rows / columns its band needs in its own
+// shared-memory slice TR rows at a time (warp-synchronous, no CTA barriers),
+// and walks exactly the rows its columns need.
+// ------------------------------------------------------------------------
+constexpr int MUL_WARPS = 8;
 
-// Main loop shared by both kernels.  Returns with acc holding this lane's
-// partial column sums (before the cross-group reduction).
-template <int SPLIT, class ACC>
-__device__ __forceinline__ void band_engine(ACC& acc, const u32* A, int ma, const u32* B, int mb, int K0, int TR,
-                                            u32* smem, int& Kw_out) {
-  constexpr int LPG = 32 / SPLIT;
-  constexpr int CW = 8 * LPG;
-  constexpr int CC = 8 * CW;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int grp = lane / LPG, p = lane - grp * LPG;
-  const int Kw = K0 + warp * CW;
-  Kw_out = Kw;
-  u32* as_ = smem;
-  u32* bs_ = smem + TR;
-  const int ilo = max(0, K0 - (mb - 1));
-  const int ihi = min(ma - 1, K0 + CC - 1);
-  // this warp's rows (8-row blocks relative to ilo) and this group's slice
-  const int wlo = max(0, Kw - (mb - 1)), whi = min(ma - 1, Kw + CW - 1);
-  int wb_lo = (wlo - ilo) >> 3, wb_hi = (whi - ilo + 8) >> 3;
-  if (whi < wlo) wb_hi = wb_lo;
-  const int qb = (wb_hi - wb_lo + SPLIT - 1) / SPLIT;
-  const int gb_lo = min(wb_hi, wb_lo + grp * qb), gb_hi = min(wb_hi, gb_lo + qb);
-  acc.zero();
-  const int TRB = TR >> 3;
-  for (int i0 = ilo; i0 <= ihi; i0 += TR) {
-    for (int x = tid; x < TR; x += blockDim.x) {
-      const int i = i0 + x;
-      as_[x] = i < ma ? A[i] : 0u;
-    }
-    const int bbase = K0 - i0 - TR + 1;
-    for (int x = tid; x < CC + TR; x += blockDim.x) {
-      const int j = bbase + x;
-      bs_[x] = (j >= 0 && j < mb) ? B[j] : 0u;
-    }
-    __syncthreads();
-    const int cb0 = (i0 - ilo) >> 3;
-    const int s = max(gb_lo, cb0), e = min(gb_hi, cb0 + TRB);
-    if (s < e) {
-      const int xb = (Kw - K0) + 8 * p - 8 * (s - cb0) + TR - 8;
-      walk(acc, as_ + 8 * (s - cb0), bs_ + xb, e - s);
-    }
-    __syncthreads();
+__device__ __forceinline__ int middle_out(int r, int nb) {
+  const int mid = (nb - 1) >> 1;
+  const int L = mid, R = nb - 1 - mid;
+  if (r == 0) return mid;
+  const int m0 = L < R ? L : R;
+  if (r <= 2 * m0) {
+    const int t = (r + 1) >> 1;
+    return (r & 1) ? mid + t : mid - t;
   }
-  // cross-group reduction: group 0 ends with the band's column sums
-#pragma unroll
-  for (int st = SPLIT / 2; st >= 1; st >>= 1) acc.add_from_lane(st * LPG);
+  const int k = r - 2 * m0;
+  return L > R ? mid - m0 - k : mid + m0 + k;
+}
+
+__device__ __forceinline__ void cpa4_zfill(u32* sdst, const u32* gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  const int n = valid ? 4 : 0;  // src-size 0: zero-fill
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(sa), "l"(gsrc), "r"(n));
+}
+
+// Skewed band schedule.  Lane p owns columns k = Kw + 8p + r (r < 8) and at
+// step t multiplies rows i = t + 8p + v (v < 8): then every lane needs
+// b[Kw + r - t - v] -- the same 16-word window for the whole warp (broadcast
+// LDS.128), a sliding by 8 per step -- and its own a[t + 8p .. t + 8p + 7],
+// and every lane's valid steps are the same interval
+//   t in [max(Kw - mb + 1, -8*31), min(Kw + 7, ma - 1)],
+// so the warp does no zero-padding work away from the product's ends.
+// Steps are staged TR at a time: a[t0 .. t0+TR+256) and b[Kw-t0-TR+1 ..
+// Kw-t0+8], double-buffered with cp.async (zero-filled out of range).
+constexpr int SK_CW = 256;  // columns per warp band
+template <int CW>
+__device__ __forceinline__ void stage_skew(u32* buf, const u32* A, int ma, const u32* B, int mb, int Kw, int t0,
+                                           int TR, int lane) {
+  for (int x = lane; x < TR + CW; x += 32) {
+    const int i = t0 + x;
+    const bool ok = i >= 0 && i < ma;
+    cpa4_zfill(buf + x, ok ? A + i : A, ok);
+  }
+  const int bbase = Kw - t0 - TR + 1;
+  for (int x = lane; x < TR + 8; x += 32) {
+    const int j = bbase + x;
+    const bool ok = j >= 0 && j < mb;
+    cpa4_zfill(buf + TR + CW + x, ok ? B + j : B, ok);
+  }
+  asm volatile("cp.async.commit_group;");
+}
+
+template <class ACC>
+__device__ __forceinline__ void warp_band(ACC& acc, const u32* A, int ma, const u32* B, int mb, int Kw, int TR,
+                                          u32* wsm) {
+  constexpr int CW = SK_CW;
+  const int p = threadIdx.x & 31;
+  const int bufw = 2 * TR + CW + 8;
+  acc.zero();
+  int tlo = Kw - (mb - 1);
+  if (tlo < -8 * 31) tlo = -8 * 31;
+  const int thi = min(Kw + 7, ma - 1);
+  if (thi < tlo) return;
+  const int nblk = (thi - tlo + 8) >> 3;
+  const int TRB = TR >> 3;
+  const int nch = (nblk + TRB - 1) / TRB;
+  stage_skew<CW>(wsm, A, ma, B, mb, Kw, tlo, TR, p);
+  for (int c = 0; c < nch; c++) {
+    u32* cur = wsm + (c & 1) * bufw;
+    if (c + 1 < nch) {
+      stage_skew<CW>(wsm + ((c + 1) & 1) * bufw, A, ma, B, mb, Kw, tlo + (c + 1) * TR, TR, p);
+      asm volatile("cp.async.wait_group 1;");
+    } else {
+      asm volatile("cp.async.wait_group 0;");
+    }
+    __syncwarp();
+    const int n = min(TRB, nblk - c * TRB);
+    // a: per lane at cur[8s + 8p]; b window (broadcast) at cur[TR + CW + TR - 8 - 8s]
+    walk(acc, cur + 8 * p, cur + TR + CW + TR - 8, n);
+    __syncwarp();
+  }
 }
 
 // ======================================================= bigint products
-template <int SPLIT>
-__global__ void __launch_bounds__(256) k_mul(MulArgs a) {
+__global__ void __launch_bounds__(32 * MUL_WARPS) k_mul(MulArgs a) {
   extern __shared__ __align__(16) u32 smem[];
-  constexpr int LPG = 32 / SPLIT;
-  constexpr int CW = 8 * LPG;
-  constexpr int CC = 8 * CW;
-  const int nbpp = a.nbands / 8;  // CTAs per product
-  const int z = blockIdx.x / nbpp;
-  const int K0 = (blockIdx.x - z * nbpp) * CC;
-  const u32* A = a.A + (long long)z * a.a_stride;
-  const u32* B = a.B + (long long)z * a.b_stride;
-  AccBig acc;
-  int Kw;
-  band_engine<SPLIT>(acc, A, a.ma, B, a.mb, K0, a.TI, smem, Kw);
-
-  // ---- band normalization (group-0 lanes; others compute and discard)
-  const int lane = threadIdx.x & 31;
-  const int grp = lane / LPG, p = lane - grp * LPG;
-  // digit y_r = c0_r + c1_{r-1} + c2_{r-2} (< 3 * 2^32)
-  u32 p_c1 = __shfl_up_sync(0xffffffffu, acc.c1[7], 1, LPG);
-  u32 p_c2 = __shfl_up_sync(0xffffffffu, acc.c2[7], 1, LPG);
-  u32 p_c2b = __shfl_up_sync(0xffffffffu, acc.c2[6], 1, LPG);
-  if (p == 0) p_c1 = p_c2 = p_c2b = 0u;
-  u32 lo[8], hi[8];
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    const u64 y = (u64)acc.c0[r] + (r >= 1 ? acc.c1[r - 1] : p_c1) +
-                  (r >= 2 ? acc.c2[r - 2] : (r == 1 ? p_c2 : p_c2b));
-    lo[r] = (u32)y;
-    hi[r] = (u32)(y >> 32);
-  }
-  u32 hprev = __shfl_up_sync(0xffffffffu, hi[7], 1, LPG);
-  if (p == 0) hprev = 0u;
-  i64 zz[8];
-  u32 mr[8], M = CM_IDENT;
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    zz[r] = (i64)lo[r] + (r ? hi[r - 1] : hprev);
-    mr[r] = cm_make(zz[r]);
-    M = cm_compose(M, mr[r]);
-  }
-  u32 tot;
-  const u32 exc = cm_seg_scan(M, LPG, nullptr, &tot);
-  int c = cm_apply(exc, 0);
-  u32 d[8];
-#pragma unroll
-  for (int r = 0; r < 8; r++) {
-    d[r] = (u32)(zz[r] + c);
-    c = cm_apply(mr[r], c);
-  }
+  constexpr int LPG = 32;
+  constexpr int CW = SK_CW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = 0, p = lane;
+  u32* wsm = smem + warp * 2 * (2 * a.TI + CW + 8);
   const int mp = a.ma + a.mb;
-  if (grp == 0 && Kw < mp) {
-    uint4* dst = reinterpret_cast<uint4*>(a.P + (long long)z * a.p_stride + Kw + 8 * p);
-    dst[0] = make_uint4(d[0], d[1], d[2], d[3]);
-    dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
-    if (p == LPG - 1) {
-      const int band = Kw / CW;
-      const i64 s0 = (i64)c + hi[7] + acc.c1[7] + acc.c2[6];
-      unsigned long long* sp = a.spill + ((long long)z * a.nbands + band) * 2;
-      sp[0] = (unsigned long long)s0;
-      sp[1] = (unsigned long long)acc.c2[7];
+  const int nunits = a.nprod * a.nbands;
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(a.counter, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nunits) break;
+    const int z = u % a.nprod;
+    const int bi = middle_out(u / a.nprod, a.nbands);
+    const int Kw = bi * CW;
+    AccBig acc;
+    warp_band(acc, a.A + (long long)z * a.a_stride, a.ma, a.B + (long long)z * a.b_stride, a.mb, Kw, a.TI, wsm);
+    // ---- band normalization (group-0 lanes; others compute and discard)
+    // digit y_r = c0_r + c1_{r-1} + c2_{r-2} (< 3 * 2^32)
+    u32 p_c1 = __shfl_up_sync(0xffffffffu, acc.c1[7], 1, LPG);
+    u32 p_c2 = __shfl_up_sync(0xffffffffu, acc.c2[7], 1, LPG);
+    u32 p_c2b = __shfl_up_sync(0xffffffffu, acc.c2[6], 1, LPG);
+    if (p == 0) p_c1 = p_c2 = p_c2b = 0u;
+    u32 lo[8], hi[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      const u64 y = (u64)acc.c0[r] + (r >= 1 ? acc.c1[r - 1] : p_c1) +
+                    (r >= 2 ? acc.c2[r - 2] : (r == 1 ? p_c2 : p_c2b));
+      lo[r] = (u32)y;
+      hi[r] = (u32)(y >> 32);
+    }
+    u32 hprev = __shfl_up_sync(0xffffffffu, hi[7], 1, LPG);
+    if (p == 0) hprev = 0u;
+    i64 zz[8];
+    u32 mr[8], M = CM_IDENT;
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      zz[r] = (i64)lo[r] + (r ? hi[r - 1] : hprev);
+      mr[r] = cm_make(zz[r]);
+      M = cm_compose(M, mr[r]);
+    }
+    u32 tot;
+    const u32 exc = cm_seg_scan(M, LPG, nullptr, &tot);
+    int c = cm_apply(exc, 0);
+    u32 d[8];
+#pragma unroll
+    for (int r = 0; r < 8; r++) {
+      d[r] = (u32)(zz[r] + c);
+      c = cm_apply(mr[r], c);
+    }
+    if (grp == 0 && Kw < mp) {
+      uint4* dst = reinterpret_cast<uint4*>(a.P + (long long)z * a.p_stride + Kw + 8 * p);
+      dst[0] = make_uint4(d[0], d[1], d[2], d[3]);
+      dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
+      if (p == LPG - 1) {
+        const i64 s0 = (i64)c + hi[7] + acc.c1[7] + acc.c2[6];
+        unsigned long long* sp = a.spill + ((long long)z * a.nbands + bi) * 2;
+        sp[0] = (unsigned long long)s0;
+        sp[1] = (unsigned long long)acc.c2[7];
+      }
     }
   }
 }
 
-template <int SPLIT>
-static cudaError_t launch_mul_t(const MulArgs& a, cudaStream_t st) {
-  const int grid = a.nprod * (a.nbands / 8);
-  constexpr int CW = 8 * (32 / SPLIT);
-  const size_t smem = (size_t)(2 * a.TI + 8 * CW) * sizeof(u32);
+static int g_num_sms = 0;
+static int num_sms() {
+  if (!g_num_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    if (g_num_sms <= 0) g_num_sms = 148;
+  }
+  return g_num_sms;
+}
+
+template <class KERN>
+static cudaError_t launch_persistent(KERN k, size_t smem, long long units, cudaStream_t st, void* args) {
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_mul<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
-  k_mul<SPLIT><<<grid, 256, smem, st>>>(a);
-  return cudaGetLastError();
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, 32 * MUL_WARPS, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  long long grid = (long long)num_sms() * per_sm;
+  const long long need = (units + MUL_WARPS - 1) / MUL_WARPS;
+  if (grid > need) grid = need;
+  if (grid < 1) grid = 1;
+  void* kargs[] = {args};
+  return cudaLaunchKernel((const void*)k, dim3((unsigned)grid), dim3(32 * MUL_WARPS), kargs, smem, st);
 }
 
 cudaError_t launch_mul(const MulArgs& a, cudaStream_t st) {
-  switch (a.G) {  // G carries SPLIT
-    case 1: return launch_mul_t<1>(a, st);
-    case 2: return launch_mul_t<2>(a, st);
-    case 4: return launch_mul_t<4>(a, st);
-    default: return cudaErrorInvalidValue;
-  }
+  const size_t smem = (size_t)MUL_WARPS * 2 * (2 * a.TI + SK_CW + 8) * sizeof(u32);
+  MulArgs b = a;
+  return launch_persistent(k_mul, smem, (long long)a.nprod * a.nbands, st, &b);
+}
+
+// tuning overrides (KMX_SPLIT=1|2|4, KMX_TR=rows) for sweeps; defaults below
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  return v && *v ? atoi(v) : dflt;
 }
 
 void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr) {
   const int m = ma < mb ? ma : mb;
-  int s = m < 1024 ? 4 : (m < 4096 ? 2 : 1);
-  const int CW = 8 * (32 / s);
-  const int CC = 8 * CW;
+  const int s = 1;
+  const int CW = SK_CW;
   const int mp = ma + mb;
-  const int nbpp = (mp + CC - 1) / CC;
-  int T = (ma + 7) & ~7;
-  if (T > 1024) T = 1024;
-  if (T < 8) T = 8;
   *split = s;
   *cw = CW;
-  *nbands = nbpp * 8;
+  *nbands = (mp + CW - 1) / CW;
+  // rows per staged chunk (double-buffered per warp): the whole row span of a
+  // band when it is short
+  int T = ((m + CW + 7) & ~7);
+  int cap = 512;
+  const int te = env_int("KMX_TR", 0);
+  if (te >= 8) cap = te & ~7;
+  if (T > cap) T = cap;
   *tr = T;
 }
 
 // ================================================= univariate Z[x] products
-template <int SPLIT>
-__global__ void __launch_bounds__(256) k_conv(ConvArgs a) {
+__global__ void __launch_bounds__(32 * MUL_WARPS) k_conv(ConvArgs a) {
   extern __shared__ __align__(16) u32 smem[];
-  constexpr int LPG = 32 / SPLIT;
-  constexpr int CW = 8 * LPG;
-  constexpr int CC = 8 * CW;
-  const int nbpp = a.nbands / 8;
-  const int z = blockIdx.x / nbpp;
-  const int K0 = (blockIdx.x - z * nbpp) * CC;
-  const u32* A = reinterpret_cast<const u32*>(a.A + (long long)z * a.a_stride);
-  const u32* B = reinterpret_cast<const u32*>(a.B + (long long)z * a.b_stride);
-  AccI64 acc;
-  int Kw;
-  band_engine<SPLIT>(acc, A, a.L, B, a.L, K0, a.TI, smem, Kw);
-  const int lane = threadIdx.x & 31;
-  const int grp = lane / LPG, p = lane - grp * LPG;
+  constexpr int CW = SK_CW;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int grp = 0, p = lane;
+  u32* wsm = smem + warp * 2 * (2 * a.TI + CW + 8);
+  const int nunits = a.nprod * a.nbands;
   const int kmax = 2 * a.L - 1;
-  if (grp == 0) {
-    int64_t* dst = a.P + (long long)z * a.p_stride + Kw + 8 * p;
+  for (;;) {
+    int u = 0;
+    if (lane == 0) u = atomicAdd(a.counter, 1);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if (u >= nunits) break;
+    const int z = u % a.nprod;
+    const int bi = middle_out(u / a.nprod, a.nbands);
+    const int Kw = bi * CW;
+    AccI64 acc;
+    warp_band(acc, reinterpret_cast<const u32*>(a.A + (long long)z * a.a_stride), a.L,
+              reinterpret_cast<const u32*>(a.B + (long long)z * a.b_stride), a.L, Kw, a.TI, wsm);
+    if (grp == 0) {
+      int64_t* dst = a.P + (long long)z * a.p_stride + Kw + 8 * p;
 #pragma unroll
-    for (int r = 0; r < 8; r++)
-      if (Kw + 8 * p + r < kmax) dst[r] = acc.s[r];
+      for (int r = 0; r < 8; r++)
+        if (Kw + 8 * p + r < kmax) dst[r] = acc.s[r];
+    }
   }
-}
-
-template <int SPLIT>
-static cudaError_t launch_conv_t(const ConvArgs& a, cudaStream_t st) {
-  const int grid = a.nprod * (a.nbands / 8);
-  constexpr int CW = 8 * (32 / SPLIT);
-  const size_t smem = (size_t)(2 * a.TI + 8 * CW) * sizeof(u32);
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(k_conv<SPLIT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_conv<SPLIT><<<grid, 256, smem, st>>>(a);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t st) {
-  switch (a.G) {
-    case 1: return launch_conv_t<1>(a, st);
-    case 2: return launch_conv_t<2>(a, st);
-    case 4: return launch_conv_t<4>(a, st);
-    default: return cudaErrorInvalidValue;
-  }
+  const size_t smem = (size_t)MUL_WARPS * 2 * (2 * a.TI + SK_CW + 8) * sizeof(u32);
+  ConvArgs b = a;
+  return launch_persistent(k_conv, smem, (long long)a.nprod * a.nbands, st, &b);
 }
 
 }  // namespace kmx
