@@ -226,7 +226,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   unsigned long long* spill = (unsigned long long*)(w + p.off_spill);
   uint32_t* dbuf = (uint32_t*)(w + p.off_dbuf);
   unsigned long long* scr = (unsigned long long*)(w + p.off_scr);
-  cudaError_t e = cudaMemsetAsync(err, 0, 8, st);  // error flag + multiply work counter
+  cudaError_t e = cudaMemsetAsync(err, 0, 12, st);  // error flag, multiply work counter, recon fallbacks
   if (e != cudaSuccess) return KMX_ECUDA;
 
   PackArgs pa;
@@ -252,7 +252,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   memset(&bfix, 0, sizeof bfix);
   if (p.sign) {
     bfix.pf = scr; bfix.pair_stride = p.lf + p.lg + 2;
-    bfix.lf = p.lf; bfix.lg = p.lg; bfix.b = p.b; bfix.enabled = 1;
+    bfix.lf = p.lf; bfix.lg = p.lg; bfix.b = p.b; bfix.enabled = 1; bfix.lgpad = -1;
   }
   prof_begin(0, st);
   if ((e = launch_pack(pa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
@@ -296,6 +296,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     ra.h = h; ra.out_words = out_words; ra.h_pair_stride = (long long)p.out_len * out_words;
     ra.err = err;
     ra.bias = bfix;
+    ra.diag = err + 2;
     prof_begin(3, st);
     if ((e = launch_recon(ra, st)) != cudaSuccess) return KMX_ECUDA;
     prof_end(3, st);

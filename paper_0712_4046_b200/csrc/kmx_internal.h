@@ -63,6 +63,7 @@ struct BiasFix {
   const unsigned long long* pf;
   long long pair_stride;
   int lf, lg, b, enabled;
+  int lgpad;                  // staged (padded) copy: entry i at i + (i >> lgpad); -1: unpadded
 };
 
 // ---------------------------------------------------------------- finish
@@ -111,6 +112,8 @@ struct ReconArgs {
   int rch;                    // steps per staged chunk (set by launch_recon)
   int sequential;             // force the one-thread-per-stream kernel
   int stage;                  // k_recon_par: stream digits staged in shared memory
+  uint32_t* diag;             // optional counter of sequential fallbacks
+  int rw_slice;               // k_recon_warp: shared-memory words per warp
 };
 
 // ---------------------------------------------------------- signed (bias)

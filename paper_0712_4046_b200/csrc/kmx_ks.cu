@@ -42,17 +42,31 @@ __device__ __forceinline__ u32 block_resolve1(i64 y, i64 cin, u32* sm_scan, i64*
 // ---- signed-input bias correction applied at store time (see BiasFix)
 __device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int128 hp, long long k, const BiasFix& bf,
                                                long long pair) {
-  __int128 v = (__int128)hp;
+  u64 lo = (u64)hp, hi = (u64)(hp >> 64);
   if (bf.enabled) {
     const unsigned long long* PF = bf.pf + pair * bf.pair_stride;
-    const unsigned long long* PG = PF + bf.lf + 1;
     const long long lf = bf.lf, lg = bf.lg;
     const long long i0 = k - lg + 1 > 0 ? k - lg + 1 : 0, i1 = k < lf - 1 ? k : lf - 1;
     const long long j0 = k - lf + 1 > 0 ? k - lf + 1 : 0, j1 = k < lg - 1 ? k : lg - 1;
-    const unsigned long long sf = PF[i1 + 1] - PF[i0], sg = PG[j1 + 1] - PG[j0];
-    v = v - ((__int128)(sf + sg) << (bf.b - 1)) + ((__int128)(i1 - i0 + 1) << (2 * bf.b - 2));
+    // staged copies are padded: entry i at i + (i >> lgpad) (PG follows PF)
+    auto pe = [&](long long i) -> u64 { return PF[bf.lgpad >= 0 ? i + (i >> bf.lgpad) : i]; };
+    const long long g0 = lf + 1;
+    const u64 S = (pe(i1 + 1) - pe(i0)) + (pe(g0 + j1 + 1) - pe(g0 + j0));
+    const u64 cnt = (u64)(i1 - i0 + 1);
+    const int sh1 = bf.b - 1, sh2 = 2 * bf.b - 2;       // 0..31, 0..62
+    const u64 a_lo = S << sh1, a_hi = sh1 ? (S >> (64 - sh1)) : 0ull;
+    const u64 c_lo = cnt << sh2, c_hi = sh2 ? (cnt >> (64 - sh2)) : 0ull;
+    const u64 l1 = lo - a_lo;                          // v - S 2^(b-1)
+    const u64 h1 = hi - a_hi - (l1 > lo ? 1ull : 0ull);
+    lo = l1 + c_lo;                                    // + cnt 2^(2b-2)
+    hi = h1 + c_hi + (lo < l1 ? 1ull : 0ull);
   }
-  for (int w = 0; w < ow; w++) dst[w] = w < 4 ? (u32)(v >> (32 * w)) : (v < 0 ? 0xffffffffu : 0u);
+  const u32 ext = (hi >> 63) ? 0xffffffffu : 0u;
+  dst[0] = (u32)lo;
+  if (ow > 1) dst[1] = (u32)(lo >> 32);
+  if (ow > 2) dst[2] = (u32)hi;
+  if (ow > 3) dst[3] = (u32)(hi >> 32);
+  for (int w = 4; w < ow; w++) dst[w] = ext;
 }
 
 // ========================================================================
@@ -740,6 +754,12 @@ __global__ void __launch_bounds__(32 * RECON_WARPS) k_recon(ReconArgs a) {
 // RECON_MAXIT rounds, thread 0 runs the whole stream sequentially.
 // ========================================================================
 constexpr int RECON_MAXIT = 8;
+#ifdef KMX_TRACE
+__device__ unsigned long long g_trace[64 * 8];
+#define TRACE(slot) do { if (threadIdx.x == 0 && blockIdx.x < 64) g_trace[blockIdx.x * 8 + (slot)] = clock64(); } while (0)
+#else
+#define TRACE(slot) do { } while (0)
+#endif
 constexpr int RECON_PAR_MAXT = 512;
 
 template <int NW>
@@ -846,9 +866,14 @@ struct ReconState {
 
 // Run steps [j0, j1) of the reference recurrence from state st; writes the
 // coefficients; accumulates e_j into esum[(j+1)&1]; latches out-of-range hi.
+// Digit d of a staged stream sits at word d*dw + (d >> lgV) (one pad word per
+// V = 2^lgV digits, so the lanes' segments start on different banks); lgV < 0:
+// unpadded.
+__device__ __forceinline__ int dpos(int d, int dw, int lgV) { return d * dw + (lgV >= 0 ? (d >> lgV) : 0); }
+
 template <int NW, bool STORE>
 __device__ __forceinline__ void recon_walk(ReconState<NW>& st, int j0, int j1, const u32* F, const u32* R, int dw,
-                                           u32* H, int pos0, int pstride, int ow, int W, u32 topmask,
+                                           int lgV, u32* H, int pos0, int pstride, int ow, int W, u32 topmask,
                                            const MW<NW>& mask, int& e0, int& e1, bool& bad,
                                            const BiasFix& bf, long long pair) {
   if constexpr (NW <= 2) {
@@ -863,7 +888,8 @@ __device__ __forceinline__ void recon_walk(ReconState<NW>& st, int j0, int j1, c
     }
     u32 fc = st.fc;
     for (int j = j0; j < j1; j++) {
-      const u64 rj1 = ld(R + (j + 1) * dw), fj1 = ld(F + (j + 1) * dw);
+      const int pj = dpos(j + 1, dw, lgV);
+      const u64 rj1 = ld(R + pj), fj1 = ld(F + pj);
       const u32 eps = lo_cur > rj1;                     // ksint.py:154 (strict)
       const u64 h = (rj - lo_prev - eps) & m64;
       bad |= h == m64;                                  // ksint.py:157-158
@@ -901,8 +927,9 @@ __device__ __forceinline__ void recon_walk(ReconState<NW>& st, int j0, int j1, c
   } else {
     for (int j = j0; j < j1; j++) {
       MW<NW> rj1, fj1, h, nxt;
-      mw_ld(rj1, R + (long long)(j + 1) * dw);
-      mw_ld(fj1, F + (long long)(j + 1) * dw);
+      const int pj = dpos(j + 1, dw, lgV);
+      mw_ld(rj1, R + pj);
+      mw_ld(fj1, F + pj);
       const u32 eps = mw_gt(st.lo_cur, rj1) ? 1u : 0u;  // ksint.py:154 (strict)
       mw_sub(h, st.rj, st.lo_prev, eps);
       mw_mask(h, topmask);
@@ -920,14 +947,83 @@ __device__ __forceinline__ void recon_walk(ReconState<NW>& st, int j0, int j1, c
   }
 }
 
+// Stage fwd and rev digit streams (count+1 digits of dw words) into smem with
+// one pad word per 2^lgV digits; returns the per-stream slot size in words.
+__device__ __forceinline__ int stage_stream(u32* dst, const u32* F, const u32* R, int count, int dw, int lgV,
+                                            int t, int nt) {
+  const int slot = dpos(count + 1, dw, lgV) + 1;
+  for (int d = t; d <= count; d += nt) {
+    const int pd = dpos(d, dw, lgV);
+    for (int w = 0; w < dw; w++) {
+      cp_async4(dst + pd + w, F + d * dw + w);
+      cp_async4(dst + slot + pd + w, R + d * dw + w);
+    }
+  }
+  return slot;
+}
+
+// Stage the pair's prefix sums (PF then PG, u64) padded by one entry per
+// 2^lgpad, lgpad chosen from the lanes' output stride; updates bfx to point at it.
+__device__ __forceinline__ void stage_prefix(u32* dst, BiasFix& bfx, int pair, int lgV, int pstride, int t, int nt) {
+  dst = reinterpret_cast<u32*>((reinterpret_cast<uintptr_t>(dst) + 7) & ~(uintptr_t)7);
+  int lgp = lgV + (pstride > 1 ? 1 : 0);
+  const int ne = bfx.lf + bfx.lg + 2;
+  const u32* src = reinterpret_cast<const u32*>(bfx.pf + (long long)pair * bfx.pair_stride);
+  for (int i = t; i < ne; i += nt) {
+    const int pi = i + (i >> lgp);
+    cp_async4(dst + 2 * pi, src + 2 * i);
+    cp_async4(dst + 2 * pi + 1, src + 2 * i + 1);
+  }
+  bfx.pf = reinterpret_cast<const unsigned long long*>(dst);
+  bfx.pair_stride = 0;
+  bfx.lgpad = lgp;
+}
+
+// last coefficient and the consistency checks (ksint.py:170-177)
+template <int NW>
+__device__ __forceinline__ void recon_final(const ReconArgs& a, const ReconStream& S, int pair, ReconState<NW> st,
+                                            bool from_start, const u32* F, const u32* R, int dw, int lgV, u32* H,
+                                            int W, int ow, u32 topmask, const MW<NW>& mask, const BiasFix& bfx) {
+  const int count = S.count;
+  MW<NW> zero;
+#pragma unroll
+  for (int i = 0; i < NW; i++) zero.w[i] = 0u;
+  if (from_start) {
+    st.lo_prev = zero;
+    mw_ld(st.lo_cur, F);
+    mw_ld(st.rj, R);
+    st.fc = 0u;
+  }
+  MW<NW> h;
+  mw_sub(h, st.rj, count >= 2 ? st.lo_prev : zero, 0u);
+  mw_mask(h, topmask);
+  bool b2 = mw_eq(h, mask);
+  MW<NW> rlast, flast, hs;
+  mw_ld(rlast, R + dpos(count, dw, lgV));
+  mw_ld(flast, F + dpos(count, dw, lgV));
+  b2 |= !mw_eq(st.lo_cur, rlast);
+  const u32 br = mw_sub(hs, flast, h, st.fc);  // h + fc == fwd[count]
+  b2 |= (br != 0u) || !mw_is_zero(hs);
+  const long long kpos = S.pos0 + (long long)(count - 1) * S.pstride;
+  if (bfx.enabled && NW <= 2) {
+    unsigned __int128 lo128 = st.lo_cur.w[0], hi128 = h.w[0];
+    if (NW == 2) { lo128 |= (unsigned __int128)st.lo_cur.w[NW - 1] << 32; hi128 |= (unsigned __int128)h.w[NW - 1] << 32; }
+    store_coeff128(H + kpos * ow, ow, lo128 | (hi128 << W), kpos, bfx, pair);
+  } else {
+    write_coeff(H + kpos * ow, ow, st.lo_cur, h, W);
+  }
+  if (b2) raise_err(a.err, ERR_RECON);
+}
+
 template <int NW>
 __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconStream& S, int pair, const u32* F,
-                                               const u32* R, u32* smw, int* smi, uint8_t* dend, int* fallback) {
+                                               const u32* R, int lgV, int V, const BiasFix& bfx, u32* smw, int* smi,
+                                               uint8_t* dend, int* fallback) {
   u32* H = a.h + (long long)pair * a.h_pair_stride;
   const int W = a.W, dw = a.dwords, ow = a.out_words, count = S.count;
   const int nsteps = count - 1;
-  const int T = blockDim.x, tid = threadIdx.x;
-  const int V = nsteps > 0 ? (nsteps + T - 1) / T : 1;
+  const int tid = threadIdx.x;
+  TRACE(1);
   const int s0 = min(tid * V, nsteps), s1 = min(s0 + V, nsteps);
   const int topbits = W - 32 * (NW - 1);
   const u32 topmask = topbits >= 32 ? 0xffffffffu : ((1u << topbits) - 1u);
@@ -935,24 +1031,24 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
 #pragma unroll
   for (int i = 0; i < NW; i++) { mask.w[i] = 0xffffffffu; zero.w[i] = 0u; }
   mw_mask(mask, topmask);
-
   // exact chain bases at the segment start: base_m = init[m&1] + sum c_j,
   // (j+1) == m (mod 2), j < s0; init = (fwd[0], 0)
   MW<NW> cs0 = zero, cs1 = zero;
   for (int j = s0; j < s1; j++) {
     MW<NW> f1, r0, c;
-    mw_ld(f1, F + (long long)(j + 1) * dw);
-    mw_ld(r0, R + (long long)j * dw);
+    mw_ld(f1, F + dpos(j + 1, dw, lgV));
+    mw_ld(r0, R + dpos(j, dw, lgV));
     mw_sub(c, f1, r0, 0u);
     if ((j + 1) & 1) mw_add(cs1, cs1, c); else mw_add(cs0, cs0, c);
   }
+  TRACE(2);
   block_exscan_mw2(cs0, cs1, smw);
+  TRACE(3);
   MW<NW> f0;
   mw_ld(f0, F);
   mw_add(cs0, cs0, f0);  // even chain starts at lo[0] = fwd[0], odd at lo[-1] = 0
   mw_mask(cs0, topmask);
   mw_mask(cs1, topmask);
-  // guesses
   int E0 = 0, E1 = 0;  // corrections at the segment start, by parity
   u32 dstart = 0;      // delta at the segment start
   if (tid == 0) *fallback = 0;
@@ -960,7 +1056,6 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
   ReconState<NW> st, st0;
   bool converged = false;
   for (int it = 0; it < RECON_MAXIT && !converged; it++) {
-    // start state (lo[s0-1], lo[s0], delta_s0)
     const int p = s0 & 1;
     mw_add_small(st.lo_cur, p ? cs1 : cs0, p ? E1 : E0);
     mw_mask(st.lo_cur, topmask);
@@ -970,13 +1065,12 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
       mw_add_small(st.lo_prev, p ? cs0 : cs1, p ? E0 : E1);
       mw_mask(st.lo_prev, topmask);
     }
-    mw_ld(st.rj, R + (long long)s0 * dw);
+    mw_ld(st.rj, R + dpos(s0, dw, lgV));
     st.fc = dstart;
-    int n0 = 0, n1 = 0;
-    bad = false;
     st0 = st;
-    recon_walk<NW, false>(st, s0, s1, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, bad, a.bias, pair);
-    // next guesses
+    int n0 = 0, n1 = 0;
+    bool b1 = false;
+    recon_walk<NW, false>(st, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, b1, bfx, pair);
     block_exscan_i2(n0, n1, smi);
     dend[tid] = (uint8_t)st.fc;
     __syncthreads();
@@ -985,56 +1079,28 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
     converged = __syncthreads_and(same);
     E0 = n0; E1 = n1; dstart = dnew;
   }
+  TRACE(4);
   if (converged) {  // output walk from the verified start state
     ReconState<NW> sw = st0;
     int q0 = 0, q1 = 0;
-    bool b3 = false;
-    recon_walk<NW, true>(sw, s0, s1, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, b3, a.bias, pair);
-  }
-  if (!converged) {
+    recon_walk<NW, true>(sw, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bfx, pair);
+  } else {
     if (tid == 0) {
       *fallback = 1;
+      if (a.diag) atomicAdd(a.diag, 1u);
       st.lo_prev = zero;
       st.lo_cur = f0;
       mw_ld(st.rj, R);
       st.fc = 0u;
       int q0 = 0, q1 = 0;
-      bad = false;
-      recon_walk<NW, true>(st, 0, nsteps, F, R, dw, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, a.bias, pair);
+      recon_walk<NW, true>(st, 0, nsteps, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bfx, pair);
     }
     __syncthreads();
   }
-  // the thread owning the last step finishes (ksint.py:170-177)
+  TRACE(5);
   const int owner = *fallback ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
-  if (tid == owner) {
-    if (nsteps == 0) {
-      st.lo_prev = zero;
-      st.lo_cur = f0;
-      mw_ld(st.rj, R);
-      st.fc = 0u;
-    }
-    MW<NW> h;
-    mw_sub(h, st.rj, count >= 2 ? st.lo_prev : zero, 0u);
-    mw_mask(h, topmask);
-    bool b2 = mw_eq(h, mask);
-    MW<NW> rlast, flast, hs;
-    mw_ld(rlast, R + (long long)count * dw);
-    mw_ld(flast, F + (long long)count * dw);
-    b2 |= !mw_eq(st.lo_cur, rlast);
-    const u32 br = mw_sub(hs, flast, h, st.fc);
-    b2 |= (br != 0u) || !mw_is_zero(hs);
-    {
-      const long long kpos = S.pos0 + (long long)(count - 1) * S.pstride;
-      if (a.bias.enabled && NW <= 2) {
-        unsigned __int128 lo128 = st.lo_cur.w[0], hi128 = h.w[0];
-        if (NW == 2) { lo128 |= (unsigned __int128)st.lo_cur.w[NW - 1] << 32; hi128 |= (unsigned __int128)h.w[NW - 1] << 32; }
-        store_coeff128(H + kpos * ow, ow, lo128 | (hi128 << W), kpos, a.bias, pair);
-      } else {
-        write_coeff(H + kpos * ow, ow, st.lo_cur, h, W);
-      }
-    }
-    if (b2) raise_err(a.err, ERR_RECON);
-  }
+  if (tid == owner)
+    recon_final(a, S, pair, st, nsteps == 0, F, R, dw, lgV, H, W, ow, topmask, mask, bfx);
   if (bad && (!*fallback || tid == 0)) raise_err(a.err, ERR_RECON);
 }
 
@@ -1045,45 +1111,200 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
   __shared__ uint8_t dend[RECON_PAR_MAXT];
   __shared__ int fallback;
   extern __shared__ u32 rst[];
+  TRACE(0);
   const int sid = blockIdx.x;
   const int pair = sid / a.ns, si = sid - pair * a.ns;
   const ReconStream S = si == 0 ? a.s[0] : a.s[1];
   const u32* F = a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride;
   const u32* R = a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride;
-  if (a.stage) {  // whole stream resident in shared memory for all walks (cp.async, all in flight)
-    const int nw = (S.count + 1) * a.dwords;
-    for (int x = threadIdx.x; x < nw; x += blockDim.x) {
-      cp_async4(rst + x, F + x);
-      cp_async4(rst + nw + x, R + x);
-    }
-    ReconArgs b = a;
-    if (a.bias.enabled) {  // prefix sums of the lifted inputs next to the digits
-      const int np = 2 * (a.bias.lf + a.bias.lg + 2);  // u32 words
-      u32* pdst = rst + 2 * nw + ((2 * nw) & 1);      // 8-byte aligned
-      const u32* psrc = reinterpret_cast<const u32*>(a.bias.pf + (long long)pair * a.bias.pair_stride);
-      for (int x = threadIdx.x; x < np; x += blockDim.x) cp_async4(pdst + x, psrc + x);
-      b.bias.pf = reinterpret_cast<const unsigned long long*>(pdst);
-      b.bias.pair_stride = 0;
-    }
+  const int nsteps = S.count - 1;
+  int lgV = 0;
+  while ((blockDim.x << lgV) < nsteps) lgV++;  // V = 2^lgV >= nsteps / T
+  const int V = 1 << lgV;
+  if (a.stage) {  // whole stream resident in shared memory (padded), cp.async all in flight
+    const int slot = stage_stream(rst, F, R, S.count, a.dwords, lgV, threadIdx.x, blockDim.x);
+    BiasFix bfx = a.bias;
+    if (a.bias.enabled) stage_prefix(rst + 2 * slot, bfx, pair, lgV, S.pstride, threadIdx.x, blockDim.x);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    recon_par_body<NW>(b, S, pair, rst, rst + nw, smw, smi, dend, &fallback);
+    recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback);
+    TRACE(6);
   } else {
-    recon_par_body<NW>(a, S, pair, F, R, smw, smi, dend, &fallback);
+    recon_par_body<NW>(a, S, pair, F, R, -1, V, a.bias, smw, smi, dend, &fallback);
   }
+}
+
+// ------------------------------------------------------------------------
+// Warp-per-stream variant of K4b for short streams (count <= RW_MAXC): the
+// same speculate / scan / verify rounds, with every scan a warp shuffle and
+// no CTA barriers; each warp stages its own stream (digits + prefix sums of
+// the signed path) in its own shared-memory slice.
+// ------------------------------------------------------------------------
+constexpr int RW_WARPS = 4;
+constexpr int RW_MAXC = 2048;
+
+template <int NW>
+__device__ __forceinline__ void warp_exscan_mw2(MW<NW>& x0, MW<NW>& x1) {
+  const int lane = threadIdx.x & 31;
+  MW<NW> i0 = x0, i1 = x1;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    MW<NW> o0, o1;
+#pragma unroll
+    for (int k = 0; k < NW; k++) {
+      o0.w[k] = __shfl_up_sync(0xffffffffu, i0.w[k], off);
+      o1.w[k] = __shfl_up_sync(0xffffffffu, i1.w[k], off);
+    }
+    if (lane >= off) { mw_add(i0, i0, o0); mw_add(i1, i1, o1); }
+  }
+#pragma unroll
+  for (int k = 0; k < NW; k++) {
+    x0.w[k] = __shfl_up_sync(0xffffffffu, i0.w[k], 1);
+    x1.w[k] = __shfl_up_sync(0xffffffffu, i1.w[k], 1);
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NW; k++) { x0.w[k] = 0u; x1.w[k] = 0u; }
+  }
+}
+
+__device__ __forceinline__ void warp_exscan_i2(int& x0, int& x1) {
+  const int lane = threadIdx.x & 31;
+  int i0 = x0, i1 = x1;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o0 = __shfl_up_sync(0xffffffffu, i0, off), o1 = __shfl_up_sync(0xffffffffu, i1, off);
+    if (lane >= off) { i0 += o0; i1 += o1; }
+  }
+  x0 = i0 - x0;
+  x1 = i1 - x1;
+}
+
+template <int NW>
+__global__ void __launch_bounds__(32 * RW_WARPS) k_recon_warp(ReconArgs a) {
+  extern __shared__ u32 rws[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int sid = blockIdx.x * RW_WARPS + warp;
+  if (sid >= a.batch * a.ns) return;
+  const int pair = sid / a.ns, si = sid - pair * a.ns;
+  const ReconStream S = si == 0 ? a.s[0] : a.s[1];
+  const int dw = a.dwords, W = a.W, ow = a.out_words, count = S.count;
+  const int nsteps = count - 1;
+  int lgV = 0;
+  while ((32 << lgV) < nsteps) lgV++;
+  const int V = 1 << lgV;
+  u32* Fs = rws + warp * a.rw_slice;
+  const int slot = stage_stream(Fs, a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride,
+                                a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride, count, dw, lgV,
+                                lane, 32);
+  BiasFix bf = a.bias;
+  if (bf.enabled) stage_prefix(Fs + 2 * slot, bf, pair, lgV, S.pstride, lane, 32);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  const u32* F = Fs;
+  const u32* R = Fs + slot;
+  u32* H = a.h + (long long)pair * a.h_pair_stride;
+  const int s0 = min(lane * V, nsteps), s1 = min(s0 + V, nsteps);
+  const int topbits = W - 32 * (NW - 1);
+  const u32 topmask = topbits >= 32 ? 0xffffffffu : ((1u << topbits) - 1u);
+  MW<NW> mask, zero;
+#pragma unroll
+  for (int i = 0; i < NW; i++) { mask.w[i] = 0xffffffffu; zero.w[i] = 0u; }
+  mw_mask(mask, topmask);
+  MW<NW> cs0 = zero, cs1 = zero;
+  for (int j = s0; j < s1; j++) {
+    MW<NW> f1, r0, c;
+    mw_ld(f1, F + dpos(j + 1, dw, lgV));
+    mw_ld(r0, R + dpos(j, dw, lgV));
+    mw_sub(c, f1, r0, 0u);
+    if ((j + 1) & 1) mw_add(cs1, cs1, c); else mw_add(cs0, cs0, c);
+  }
+  warp_exscan_mw2(cs0, cs1);
+  MW<NW> f0;
+  mw_ld(f0, F);
+  mw_add(cs0, cs0, f0);
+  mw_mask(cs0, topmask);
+  mw_mask(cs1, topmask);
+  int E0 = 0, E1 = 0;
+  u32 dstart = 0;
+  bool bad = false;
+  ReconState<NW> st, st0;
+  bool converged = false;
+  for (int it = 0; it < RECON_MAXIT && !converged; it++) {
+    const int p = s0 & 1;
+    mw_add_small(st.lo_cur, p ? cs1 : cs0, p ? E1 : E0);
+    mw_mask(st.lo_cur, topmask);
+    if (s0 == 0) {
+      st.lo_prev = zero;
+    } else {
+      mw_add_small(st.lo_prev, p ? cs0 : cs1, p ? E0 : E1);
+      mw_mask(st.lo_prev, topmask);
+    }
+    mw_ld(st.rj, R + dpos(s0, dw, lgV));
+    st.fc = dstart;
+    st0 = st;
+    int n0 = 0, n1 = 0;
+    bool b1 = false;
+    recon_walk<NW, false>(st, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, b1, bf, pair);
+    warp_exscan_i2(n0, n1);
+    u32 dnew = __shfl_up_sync(0xffffffffu, st.fc, 1);
+    if (lane == 0) dnew = 0u;
+    const bool same = (n0 == E0) && (n1 == E1) && (dnew == dstart);
+    converged = __all_sync(0xffffffffu, same);
+    E0 = n0; E1 = n1; dstart = dnew;
+  }
+  bool fb = false;
+  if (converged) {
+    ReconState<NW> sw = st0;
+    int q0 = 0, q1 = 0;
+    recon_walk<NW, true>(sw, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bf, pair);
+  } else {
+    fb = true;
+    if (lane == 0) {
+      if (a.diag) atomicAdd(a.diag, 1u);
+      st.lo_prev = zero;
+      st.lo_cur = f0;
+      mw_ld(st.rj, R);
+      st.fc = 0u;
+      int q0 = 0, q1 = 0;
+      recon_walk<NW, true>(st, 0, nsteps, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bf, pair);
+    }
+  }
+  const int owner = fb ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
+  if (lane == owner) recon_final(a, S, pair, st, nsteps == 0, F, R, dw, lgV, H, W, ow, topmask, mask, bf);
+  if (bad && (!fb || lane == 0)) raise_err(a.err, ERR_RECON);
 }
 
 template <int NW>
 static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStream_t st) {
+  if (maxcount <= RW_MAXC) {
+    ReconArgs b = a;
+    // padded digit slots (+1 word per digit at most) + padded prefix sums
+    int slice = 2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4;
+    if (a.bias.enabled) slice += 4 * (a.bias.lf + a.bias.lg + 2) + 4;
+    slice = (slice + 3) & ~3;
+    const size_t smem = (size_t)RW_WARPS * slice * sizeof(u32);
+    if (smem <= 200 * 1024) {
+      b.rw_slice = slice;
+      if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k_recon_warp<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      const int n = a.batch * a.ns;
+      k_recon_warp<NW><<<(n + RW_WARPS - 1) / RW_WARPS, 32 * RW_WARPS, smem, st>>>(b);
+      return cudaGetLastError();
+    }
+  }
   const int nsteps = maxcount > 1 ? maxcount - 1 : 1;
   int T = (nsteps + 7) / 8;             // ~8 steps per thread
   T = ((T + 31) / 32) * 32;
   if (T < 32) T = 32;
   if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;
   ReconArgs b = a;
-  size_t smem = (size_t)2 * (maxcount + 1) * a.dwords * sizeof(u32) + 8;
-  if (a.bias.enabled) smem += (size_t)(a.bias.lf + a.bias.lg + 2) * 8;
+  size_t smem = (size_t)(2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4) * sizeof(u32);
+  if (a.bias.enabled) smem += (size_t)(4 * (a.bias.lf + a.bias.lg + 2) + 4) * sizeof(u32);
   b.stage = smem <= 160 * 1024;
   if (b.stage && smem > 32 * 1024) {  // dynamic + ~5 KB static must fit the opt-in limit
     cudaError_t e = cudaFuncSetAttribute(k_recon_par<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1218,6 +1439,12 @@ __global__ void __launch_bounds__(512) k_imad_peak(const u32* in, u32* out, int 
   for (int r = 0; r < 8; r++) s ^= c0[r] ^ c1[r] ^ c2[r];
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
+
+#ifdef KMX_TRACE
+extern "C" int kmx_debug_trace(unsigned long long* out, int n) {
+  return cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * (n < 512 ? n : 512)) == cudaSuccess ? 0 : -4;
+}
+#endif
 
 double measure_imad_peak(int iters) {
   int dev = 0, sms = 0;
