@@ -117,34 +117,42 @@ struct PackCtx {
   bool rev, bias;
   u32 biasw, bmask;
   __device__ __forceinline__ u32 word(int i, int w) const {  // word w of the coefficient at position i
-    if (w >= iw) return 0u;
+    if (i >= L || w >= iw) return 0u;
     const int ci = rev ? (L - 1 - i) : i;
     u32 x = __ldg(cf + (long long)ci * iw + w);
     if (bias) x = (x + biasw) & bmask;  // signed inputs: lift by 2^(b-1) (iw == 1)
     return x;
   }
-  // bits of coefficient i that fall in the 32-bit window starting at bit lo
-  __device__ __forceinline__ u32 window(int i, long long lo) const {
-    const long long s = lo - (long long)i * N;
-    if (s <= 0) return (-s) >= 32 ? 0u : (word(i, 0) << (int)(-s));
-    const int wq = (int)(s >> 5), sb = (int)(s & 31);
-    const u32 x = word(i, wq);
-    return sb ? ((x >> sb) | (word(i, wq + 1) << (32 - sb))) : x;
+};
+
+// Cursor over one parity stream: coefficients at positions i = 2m + par start
+// at bit off + m*S (S = 2N >= b, so they never overlap inside a stream).
+// Invariant for the current digit q: m = the last coefficient starting at or
+// below bit 32q (m may be -1), t = 32q - start(m).
+struct StreamCur {
+  int m, t;
+  __device__ __forceinline__ void init(int q, int off, int S) {
+    const int x = 32 * q - off;
+    m = x >= 0 ? x / S : -((-x + S - 1) / S);
+    t = x - m * S;
   }
-  // e (even positions) and o (odd positions) bits of window q; *icur is a
-  // monotone cursor: the first position whose span may still reach window q
-  __device__ __forceinline__ void digit(int q, int* icur, u32* e, u32* o) const {
-    const long long lo = 32LL * q;
-    int i = *icur;
-    while (i < L && (long long)i * N + b <= lo) i++;
-    *icur = i;
-    u32 ev = 0u, ov = 0u;
-    for (int k = i; k < L && (long long)k * N < lo + 32; k++) {
-      const u32 x = window(k, lo);
-      if (k & 1) ov |= x; else ev |= x;
+  __device__ __forceinline__ void next(int S) {
+    t += 32;
+    while (t >= S) { t -= S; m++; }
+  }
+  // the 32 bits of this stream in the current digit window
+  __device__ __forceinline__ u32 bits(const PackCtx& C, int par, int S) const {
+    u32 v = 0u;
+    if (m >= 0 && t < C.b) {
+      const int wq = t >> 5, sb = t & 31;
+      const int i = 2 * m + par;
+      const u32 lo = C.word(i, wq);
+      v = sb ? ((lo >> sb) | (C.word(i, wq + 1) << (32 - sb))) : lo;
     }
-    *e = ev;
-    *o = ov;
+    for (int k = 1, sh = S - t; sh < 32; k++, sh += S) {  // coefficients starting inside the window
+      if (m + k >= 0) v |= C.word(2 * (m + k) + par, 0) << sh;
+    }
+    return v;
   }
 };
 
@@ -192,6 +200,7 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
     __syncthreads();
   }
   if (tid == 0) { sm_top = 0; sm_order = 1; sm_carry = 0; }
+  const int S = 2 * C.N;
   // negated packs: order of E and O from the most significant differing digit
   if (neg && tid < 32) {
     int order = 0;  // +1: E > O, -1: E < O, 0: equal
@@ -199,10 +208,11 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
       const int q = base - tid;
       u32 e = 0u, ov = 0u;
       if (q >= 0) {
-        int ic = 0;
-        const long long t = 32LL * q - C.b;
-        if (t >= 0) ic = (int)(t / C.N) + 1;
-        C.digit(q, &ic, &e, &ov);
+        StreamCur ce, co;
+        ce.init(q, 0, S);
+        co.init(q, C.N, S);
+        e = ce.bits(C, 0, S);
+        ov = co.bits(C, 1, S);
       }
       const unsigned diff = __ballot_sync(0xffffffffu, e != ov);
       if (diff) {
@@ -221,17 +231,20 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
   for (int c0 = 0; c0 < m; c0 += T * PK_V) {
     const int q0 = c0 + tid * PK_V;
     i64 t[PK_V];
-    int ic = 0;
-    {
-      const long long tt = 32LL * q0 - C.b;
-      if (tt >= 0) ic = (int)(tt / C.N) + 1;
-    }
+    StreamCur ce, co;
+    ce.init(q0, 0, S);
+    co.init(q0, C.N, S);
     u32 M = CM_IDENT, mr[PK_V];
 #pragma unroll
     for (int v = 0; v < PK_V; v++) {
       const int q = q0 + v;
       u32 e = 0u, ov = 0u;
-      if (q < m) C.digit(q, &ic, &e, &ov);
+      if (q < m) {
+        e = ce.bits(C, 0, S);
+        ov = co.bits(C, 1, S);
+      }
+      ce.next(S);
+      co.next(S);
       t[v] = !neg ? (i64)e + ov : (order > 0 ? (i64)e - ov : (i64)ov - e);
       mr[v] = cm_make(t[v]);
       M = cm_compose(M, mr[v]);
@@ -273,8 +286,9 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   int mmax = 0;
   for (int i = 0; i < a.nops; i++) mmax = a.op[i].m > mmax ? a.op[i].m : mmax;
-  int T = 32;
-  while (T < PK_T && T * PK_V < mmax) T <<= 1;
+  int T = ((mmax + PK_V - 1) / PK_V + 31) & ~31;  // sized to the operand
+  if (T < 32) T = 32;
+  if (T > PK_T) T = PK_T;
   k_pack<<<batch * a.nops, T, 0, st>>>(a);
   return cudaGetLastError();
 }
