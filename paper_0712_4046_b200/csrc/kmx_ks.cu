@@ -10,6 +10,8 @@
 //   k_bias    signed-input bias correction
 //
 // All arithmetic is exact integer arithmetic on 32-bit limbs.
+#include <cstdlib>
+
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
 
@@ -993,6 +995,23 @@ __device__ __forceinline__ void stage_prefix(u32* dst, BiasFix& bfx, int pair, i
   bfx.lgpad = lgp;
 }
 
+// In-place signed correction of one stream's coefficients h[pos0 + j*pstride]
+// (j < count) by nl cooperating lanes: independent loads, no dependency
+// chain, so the L2 latency of h' and of the prefix sums overlaps.
+__device__ __forceinline__ void bias_pass(const BiasFix& bf, int pair, u32* H, int ow, int pos0, int pstride, int count,
+                                          int t, int nt) {
+#pragma unroll 4
+  for (int j = t; j < count; j += nt) {
+    const long long k = pos0 + (long long)j * pstride;
+    u32* hk = H + k * ow;
+    unsigned __int128 hp = hk[0];
+    if (ow > 1) hp |= (unsigned __int128)hk[1] << 32;
+    if (ow > 2) hp |= (unsigned __int128)hk[2] << 64;
+    if (ow > 3) hp |= (unsigned __int128)hk[3] << 96;
+    store_coeff128(hk, ow, hp, k, bf, pair);
+  }
+}
+
 // last coefficient and the consistency checks (ksint.py:170-177)
 template <int NW>
 __device__ __forceinline__ void recon_final(const ReconArgs& a, const ReconStream& S, int pair, ReconState<NW> st,
@@ -1137,7 +1156,7 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
   const int V = 1 << lgV;
   if (a.stage) {  // whole stream resident in shared memory (padded), cp.async all in flight
     const int slot = stage_stream(rst, F, R, S.count, a.dwords, lgV, threadIdx.x, blockDim.x);
-    BiasFix bfx = a.bias;
+    BiasFix bfx = a.bias;  // signed inputs: prefix sums staged next to the digits, fused into the output walk
     if (a.bias.enabled) stage_prefix(rst + 2 * slot, bfx, pair, lgV, S.pstride, threadIdx.x, blockDim.x);
     cp_async_commit();
     cp_async_wait<0>();
@@ -1145,7 +1164,12 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
     recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback);
     TRACE(6);
   } else {
-    recon_par_body<NW>(a, S, pair, F, R, -1, V, a.bias, smw, smi, dend, &fallback);
+    recon_par_body<NW>(a, S, pair, F, R, -1, V, BiasFix{}, smw, smi, dend, &fallback);
+    if (a.bias.enabled) {  // signed inputs: correct this stream's coefficients in place
+      __syncthreads();
+      bias_pass(a.bias, pair, a.h + (long long)pair * a.h_pair_stride, a.out_words, S.pos0, S.pstride, S.count,
+                threadIdx.x, blockDim.x);
+    }
   }
 }
 
@@ -1212,8 +1236,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_recon_warp(ReconArgs a) {
   const int slot = stage_stream(Fs, a.dbuf + ((long long)pair * a.dslots_pair + S.fslot) * a.dslot_stride,
                                 a.dbuf + ((long long)pair * a.dslots_pair + S.rslot) * a.dslot_stride, count, dw, lgV,
                                 lane, 32);
-  BiasFix bf = a.bias;
-  if (bf.enabled) stage_prefix(Fs + 2 * slot, bf, pair, lgV, S.pstride, lane, 32);
+  const BiasFix bf{};  // raw h' from the walks; signed correction in bias_pass below
   cp_async_commit();
   cp_async_wait<0>();
   __syncwarp();
@@ -1289,15 +1312,19 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_recon_warp(ReconArgs a) {
   const int owner = fb ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
   if (lane == owner) recon_final(a, S, pair, st, nsteps == 0, F, R, dw, lgV, H, W, ow, topmask, mask, bf);
   if (bad && (!fb || lane == 0)) raise_err(a.err, ERR_RECON);
+  if (a.bias.enabled) {
+    __syncwarp();
+    bias_pass(a.bias, pair, H, ow, S.pos0, S.pstride, count, lane, 32);
+  }
 }
 
 template <int NW>
 static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStream_t st) {
-  if (maxcount <= RW_MAXC) {
+  static const int use_warp = getenv("KMX_RECON_WARP") ? atoi(getenv("KMX_RECON_WARP")) : 0;
+  if (use_warp && maxcount <= RW_MAXC) {
     ReconArgs b = a;
     // padded digit slots (+1 word per digit at most) + padded prefix sums
     int slice = 2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4;
-    if (a.bias.enabled) slice += 4 * (a.bias.lf + a.bias.lg + 2) + 4;
     slice = (slice + 3) & ~3;
     const size_t smem = (size_t)RW_WARPS * slice * sizeof(u32);
     if (smem <= 200 * 1024) {
