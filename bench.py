@@ -124,6 +124,27 @@ def pack_unpack_bytes(cfg, variant):
     return {"pack_bytes": pack, "finish_bytes": fin}
 
 
+# -------------------------------------------------------------- multi-rank
+def rank_env():
+    return (int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1")),
+            int(os.environ.get("LOCAL_RANK", "0")))
+
+
+def max_over_ranks(x, dist=None, device=None):
+    """Max of a host float over all ranks (timings are max over ranks)."""
+    if dist is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_products(batch_per_rank, world):
+    """Weak scaling: every rank multiplies its own batch of independent pairs."""
+    return batch_per_rank * world
+
+
 # ------------------------------------------------------------------ clocks
 class ClockMonitor:
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -190,12 +211,8 @@ def run_ours(args, cfg, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize()
 
-    def max_over_ranks(x):
-        if dist is None:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+    def mor(x):
+        return max_over_ranks(x, dist, dev)
 
     fh, gh = make_inputs(cfg, rank)
     signed = cfg.get("signed", False)
@@ -253,9 +270,9 @@ def run_ours(args, cfg, rank, world, local_rank):
         if mon is not None:
             clocks = mon.stop()
         op.status()
-        total_ms = max_over_ranks(total_ms)
+        total_ms = mor(total_ms)
         ms = total_ms / args.steps
-        rec = {"products_per_s": world * B / (ms * 1e-3), "ms_per_step": ms, "launches_per_step": launches / args.steps}
+        rec = {"products_per_s": job_products(B, world) / (ms * 1e-3), "ms_per_step": ms, "launches_per_step": launches / args.steps}
         if cfg["kind"] == "ks":
             names = ["pack", "mul", "finish", "recon", "bias"]
             rec["kernel_ms"] = {nm: kern[i] / args.steps for i, nm in enumerate(names) if kern[i] > 0}
@@ -297,8 +314,8 @@ def run_ours(args, cfg, rank, world, local_rank):
         call()
         tot += time.perf_counter() - t0
     barrier()
-    tot = max_over_ranks(tot)
-    e2e = {"value": world * B / (tot / args.steps), "unit": "poly products/s",
+    tot = mor(tot)
+    e2e = {"value": job_products(B, world) / (tot / args.steps), "unit": "poly products/s",
            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
            "ms_per_step": 1e3 * tot / args.steps, "api": "paper_0712_4046_b200.ks_mul_host -> kmx_ks_mul_host"
            if cfg["kind"] == "ks" else "paper_0712_4046_b200.bks_mul_host -> kmx_bks_mul_host"}
@@ -330,8 +347,8 @@ def run_ours(args, cfg, rank, world, local_rank):
 def _cpu_task(args):
     kind, v, f, g, b, signed = args
     from oracle import ks_oracle as O
-    if kind == "bks":
-        return len(O.bks(v, f, g))
+    if kind == "bks":  # the reference's default UniMul (uni_schoolbook, oracle.py:58-69)
+        return len(O.bks(v, f, g, umul=O.uni_schoolbook))
     if signed:
         return len(O.ks_mul_signed(v, f, g, b, mode="karatsuba"))
     return len(O.ks_mul(v, f, g, b, mode="karatsuba"))
@@ -365,7 +382,8 @@ def cpu_baseline(cfg, variant, budget_s=12.0):
     _cpu_task(cpu_tasks(cfg, variant, 1)[0])
     t_pair = max(1e-4, time.perf_counter() - t0)
     n = int(max(cores, min(cfg["batch"] * 4, budget_s * cores / t_pair)))
-    n = max(cores, min(n, 8 * cores if cfg["kind"] == "bks" else n))
+    if cfg["kind"] == "bks":
+        n = cores  # one pair per core (seconds each through the pure-Python UniMul)
     tasks = cpu_tasks(cfg, variant, n)
     while len(tasks) < n:
         tasks += tasks[:n - len(tasks)]
@@ -396,7 +414,7 @@ def run_reference(args, cfg):
     import multiprocessing as mp
     cores = host_cores()
     v = args.variant
-    per_step = cores * (1 if cfg["kind"] == "bks" else 2)
+    per_step = cores * (1 if cfg["kind"] == "bks" else 2)  # bks: one pair per core per step
     tasks = cpu_tasks(cfg, v, per_step)
     while len(tasks) < per_step:
         tasks += tasks[:per_step - len(tasks)]
@@ -459,9 +477,7 @@ def main():
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local_rank = rank_env()
 
     if args.impl == "reference":
         if rank == 0:

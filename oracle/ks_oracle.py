@@ -445,6 +445,19 @@ def schoolbook(f, g) -> list[int]:
     return out
 
 
+def uni_schoolbook(a, b) -> list[int]:
+    """oracle.py:58-69 with ring_z(): the reference's default univariate
+    multiplier for the bivariate reductions (bipoly.py:121-125), a plain
+    double loop through the ring callbacks -- kept with that cost structure
+    for the CPU baseline of config 3."""
+    add, mul = operator.add, operator.mul
+    out = [0] * (len(a) + len(b) - 1)
+    for i, x in enumerate(a):
+        for j, y in enumerate(b):
+            out[i + j] = add(out[i + j], mul(x, y))
+    return out
+
+
 def convolve_exact(a, b) -> list[int]:
     """Exact integer convolution for the univariate products of the
     bivariate reductions (the role of ``uni_schoolbook`` over Z,

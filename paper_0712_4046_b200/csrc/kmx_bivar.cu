@@ -9,6 +9,7 @@
 //   k_brecover half-sums, exact halving and the chunk overlap recovery
 //              (_overlap_recover bipoly.py:151-174; _split_chunks :146-148)
 #include <cstring>
+#include <mutex>
 
 #include "../../include/kmx.h"
 #include "kmx_common.cuh"
@@ -238,6 +239,14 @@ int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits, const in
 
 int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits, const int32_t* f, const int32_t* g,
                      int64_t* h) {
+  // cached per-device buffers and stream (as kmx_ks_mul_host)
+  struct Ctx {
+    std::mutex mu;
+    cudaStream_t st = nullptr;
+    void* buf[3] = {nullptr, nullptr, nullptr};
+    size_t cap[3] = {0, 0, 0};
+  };
+  static Ctx ctx[16];
   BivarPlan p;
   int rc = bks_plan(p, variant, batch, lx, ly, coeff_bits);
   if (rc) return rc;
@@ -246,32 +255,29 @@ int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits, con
   const size_t fb = (size_t)batch * lx * ly * 4;
   const size_t hb = (size_t)batch * (2 * lx - 1) * (2 * ly - 1) * 8;
   if (batch == 0) return KMX_OK;
-  void *df = nullptr, *dh = nullptr, *dw = nullptr;
-  cudaStream_t st = nullptr;
-  rc = KMX_ECUDA;
-  if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
-  if (cudaMalloc(&df, 2 * fb + 256) != cudaSuccess || cudaMalloc(&dh, hb) != cudaSuccess ||
-      cudaMalloc(&dw, tot) != cudaSuccess) {
-    rc = KMX_ENOMEM;
-    goto done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) return KMX_ECUDA;
+  Ctx& c = ctx[dev];
+  std::lock_guard<std::mutex> lk(c.mu);
+  if (!c.st && cudaStreamCreateWithFlags(&c.st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+  const size_t need[3] = {2 * align256b(fb), hb, tot};
+  for (int i = 0; i < 3; i++) {
+    if (c.cap[i] < need[i]) {
+      if (c.buf[i]) cudaFree(c.buf[i]);
+      c.buf[i] = nullptr;
+      c.cap[i] = 0;
+      if (cudaMalloc(&c.buf[i], need[i] > 4096 ? need[i] : 4096) != cudaSuccess) return KMX_ENOMEM;
+      c.cap[i] = need[i] > 4096 ? need[i] : 4096;
+    }
   }
-  {
-    int32_t* dF = (int32_t*)df;
-    int32_t* dG = (int32_t*)((char*)df + ((fb + 255) & ~(size_t)255));
-    if (cudaMemcpyAsync(dF, f, fb, cudaMemcpyHostToDevice, st) != cudaSuccess) goto done;
-    if (cudaMemcpyAsync(dG, g, fb, cudaMemcpyHostToDevice, st) != cudaSuccess) goto done;
-    rc = kmx_bks_mul(variant, batch, lx, ly, coeff_bits, dF, dG, (int64_t*)dh, dw, tot, st);
-    if (rc) goto done;
-    if (cudaMemcpyAsync(h, dh, hb, cudaMemcpyDeviceToHost, st) != cudaSuccess) { rc = KMX_ECUDA; goto done; }
-    rc = kmx_ws_status(dw, st);
-  }
-done:
-  cudaStreamSynchronize(st);
-  if (df) cudaFree(df);
-  if (dh) cudaFree(dh);
-  if (dw) cudaFree(dw);
-  cudaStreamDestroy(st);
-  return rc;
+  int32_t* dF = (int32_t*)c.buf[0];
+  int32_t* dG = (int32_t*)((char*)c.buf[0] + align256b(fb));
+  if (cudaMemcpyAsync(dF, f, fb, cudaMemcpyHostToDevice, c.st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMemcpyAsync(dG, g, fb, cudaMemcpyHostToDevice, c.st) != cudaSuccess) return KMX_ECUDA;
+  rc = kmx_bks_mul(variant, batch, lx, ly, coeff_bits, dF, dG, (int64_t*)c.buf[1], c.buf[2], c.cap[2], c.st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(h, c.buf[1], hb, cudaMemcpyDeviceToHost, c.st) != cudaSuccess) return KMX_ECUDA;
+  return kmx_ws_status(c.buf[2], c.st);
 }
 
 }  // extern "C"

@@ -32,6 +32,7 @@ struct PackArgs {
   int in_words;
   int bias;                   // signed inputs: add 2^(b-1) (bias lift)
   uint32_t* err;
+  int stage;                  // set by launch_pack: coefficients staged in shared memory
 };
 
 // -------------------------------------------------------------- multiply

@@ -115,10 +115,12 @@ constexpr int PK_V = 8;
 
 struct PackCtx {
   const u32* cf;
+  const u32* sc;   // staged coefficients in position order (reversal and bias applied), or null
   int L, N, b, iw;
   bool rev, bias;
   u32 biasw, bmask;
   __device__ __forceinline__ u32 word(int i, int w) const {  // word w of the coefficient at position i
+    if (sc) return w < iw ? sc[i * iw + w] : 0u;  // zero-padded past L
     if (i >= L || w >= iw) return 0u;
     const int ci = rev ? (L - 1 - i) : i;
     u32 x = __ldg(cf + (long long)ci * iw + w);
@@ -126,6 +128,8 @@ struct PackCtx {
     return x;
   }
 };
+constexpr int PK_STAGE_WORDS = 12288;  // stage coefficient vectors up to 48 KB
+constexpr int PK_PAD = 64;             // zero positions past L (window reads beyond the top)
 
 // Cursor over one parity stream: coefficients at positions i = 2m + par start
 // at bit off + m*S (S = 2N >= b, so they never overlap inside a stream).
@@ -159,6 +163,7 @@ struct StreamCur {
 };
 
 __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
+  extern __shared__ u32 pk_sc[];
   __shared__ u32 sm_scan[PK_T / 32];
   __shared__ int sm_order, sm_top;
   const int T = blockDim.x;  // 32..PK_T, sized to the operand
@@ -179,6 +184,16 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
   C.biasw = A.bias ? (1u << (C.b - 1)) : 0u;
   const bool neg = kind & 1;
   const bool flip = (kind == 3) && ((C.L & 1) == 0);  // pack.py:106-109
+  C.sc = nullptr;
+  if (A.stage) {  // stage the vector in position order with zero padding
+    const int nw = (C.L + PK_PAD) * C.iw;
+    for (int x = tid; x < nw; x += T) {
+      const int i = x / C.iw, w = x - i * C.iw;
+      pk_sc[x] = C.word(i, w);
+    }
+    __syncthreads();
+    C.sc = pk_sc;
+  }
 
   if (A.op[o].validate) {  // CoeffVec invariant 0 <= c < 2^b (pack.py:36-46)
     for (int i = tid; i < C.L; i += T) {
@@ -291,7 +306,17 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   int T = ((mmax + PK_V - 1) / PK_V + 31) & ~31;  // sized to the operand
   if (T < 32) T = 32;
   if (T > PK_T) T = PK_T;
-  k_pack<<<batch * a.nops, T, 0, st>>>(a);
+  int lmax = 0;
+  for (int i = 0; i < a.nops; i++) lmax = a.op[i].len > lmax ? a.op[i].len : lmax;
+  PackArgs b = a;
+  const int nw = (lmax + PK_PAD) * a.in_words;
+  b.stage = nw <= PK_STAGE_WORDS;
+  const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_pack<<<batch * a.nops, T, smem, st>>>(b);
   return cudaGetLastError();
 }
 
@@ -355,12 +380,42 @@ __global__ void __launch_bounds__(FN_T) k_finish(FinishArgs a) {
     const int q0 = q00 + tid * FN_V;
     u32 lo[FN_V];
     i64 hi[FN_V];
+    {
+      // limbs q0..q0+7 of P (and Q): two 16-byte loads when in range; the
+      // band spills only land on the first two limbs of a band (q0 % C == 0)
+      u32 pv[FN_V], qv[FN_V];
+      i64 s0 = 0, s1 = 0;
+      const bool full = q0 + FN_V <= mp;
+      const bool bstart = q0 > 0 && q0 < mp && (q0 & ((1 << lgC) - 1)) == 0;
+      const int bidx = (q0 >> lgC) - 1;
+      if (full) {
+        const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(Pp + q0));
+        const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(Pp + q0) + 1);
+        pv[0] = x0.x; pv[1] = x0.y; pv[2] = x0.z; pv[3] = x0.w; pv[4] = x1.x; pv[5] = x1.y; pv[6] = x1.z; pv[7] = x1.w;
+      } else {
 #pragma unroll
-    for (int v = 0; v < FN_V; v++) {
-      i64 y = prod_digit(Pp, spP, q0 + v, mp, lgC);
-      if (sg) y += sg * prod_digit(Qp, spQ, q0 + v, mp, lgC);
-      lo[v] = (u32)y;
-      hi[v] = y >> 32;
+        for (int v = 0; v < FN_V; v++) pv[v] = q0 + v < mp ? Pp[q0 + v] : 0u;
+      }
+      if (bstart) { s0 = (i64)spP[bidx * 2]; s1 = (i64)spP[bidx * 2 + 1]; }
+      if (sg) {
+        if (full) {
+          const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(Qp + q0));
+          const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(Qp + q0) + 1);
+          qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w; qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
+        } else {
+#pragma unroll
+          for (int v = 0; v < FN_V; v++) qv[v] = q0 + v < mp ? Qp[q0 + v] : 0u;
+        }
+        if (bstart) { s0 += sg * (i64)spQ[bidx * 2]; s1 += sg * (i64)spQ[bidx * 2 + 1]; }
+      }
+#pragma unroll
+      for (int v = 0; v < FN_V; v++) {
+        i64 y = (i64)pv[v] + (sg ? sg * (i64)qv[v] : 0);
+        if (v == 0) y += s0;
+        if (v == 1) y += s1;
+        lo[v] = (u32)y;
+        hi[v] = y >> 32;
+      }
     }
     sm_hi[tid] = hi[FN_V - 1];
     __syncthreads();

@@ -131,3 +131,14 @@ def test_words_roundtrip():
     w = O.ints_to_words(sv, 3, signed=True)
     back = [v - (1 << 96) if v >> 95 else v for v in O.words_to_ints(w)]
     assert back == sv
+
+
+def test_oracle_uni_schoolbook_matches_convolution():
+    # the restated reference UniMul (oracle.py:58-69) used by the CPU baseline
+    rng = random.Random(9)
+    for _ in range(20):
+        a = [rng.randrange(-99, 100) for _ in range(rng.randrange(1, 30))]
+        b = [rng.randrange(-99, 100) for _ in range(rng.randrange(1, 30))]
+        assert O.uni_schoolbook(a, b) == O.convolve_exact(a, b) == O.schoolbook(a, b)
+    tag, f, g, h = G.bivar_cases()[3]
+    assert O.bks(4, f, g, umul=O.uni_schoolbook) == h
