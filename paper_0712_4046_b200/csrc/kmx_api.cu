@@ -12,6 +12,7 @@
 //                          at 2*N4; KS1 fallback if not four_point_safe and
 //                          the out_len == 1 single product (:299-303).
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -493,8 +494,9 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
   const size_t fb = (size_t)batch * len_f * p.in_words * 4, gb = (size_t)batch * len_g * p.in_words * 4;
   const size_t hb = (size_t)batch * p.out_len * out_words * 4;
   if (!limb_products64 && batch >= 2) {
-    // chunks of >= ~2 MB of output, at most HOST_MAX_CHUNKS
-    size_t nch = hb / (2u << 20);
+    // chunks of >= ~chunk_mb MB of output (KMX_HOST_CHUNK_MB, default 4), at most HOST_MAX_CHUNKS
+    static const int chunk_mb = getenv("KMX_HOST_CHUNK_MB") ? atoi(getenv("KMX_HOST_CHUNK_MB")) : 4;
+    size_t nch = hb / ((size_t)(chunk_mb > 0 ? chunk_mb : 2) << 20);
     if (nch > (size_t)HOST_MAX_CHUNKS) nch = HOST_MAX_CHUNKS;
     if (nch > (size_t)batch) nch = batch;
     if (nch >= 2) return ks_mul_host_pipelined(p, c, f, g, h, out_words, (int)nch);

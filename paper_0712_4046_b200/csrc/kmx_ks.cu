@@ -120,7 +120,10 @@ struct PackCtx {
   bool rev, bias;
   u32 biasw, bmask;
   __device__ __forceinline__ u32 word(int i, int w) const {  // word w of the coefficient at position i
-    if (sc) return w < iw ? sc[i * iw + w] : 0u;  // zero-padded past L
+    if (sc) return w < iw ? sc[i * iw + w] : 0u;  // zero-padded past L (staged)
+    return gword(i, w);
+  }
+  __device__ __forceinline__ u32 gword(int i, int w) const {  // unstaged (very long vectors)
     if (i >= L || w >= iw) return 0u;
     const int ci = rev ? (L - 1 - i) : i;
     u32 x = __ldg(cf + (long long)ci * iw + w);
@@ -245,12 +248,29 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
   const int negative = neg ? ((order < 0) != flip ? 1 : 0) : 0;
 
   int my_top = 0;
+  if (!neg && C.N >= C.b) {
+    // disjoint bit fields (pack.py:66-67): V = E | O, no carries at all --
+    // a pure gather, every thread independent
+    for (int q0 = tid * PK_V; q0 < m; q0 += T * PK_V) {
+      StreamCur ce, co;
+      ce.init(q0, 0, S);
+      co.init(q0, C.N, S);
+#pragma unroll 1
+      for (int v = 0; v < PK_V && q0 + v < m; v++) {
+        const u32 d = ce.bits(C, 0, S) | co.bits(C, 1, S);
+        ce.next(S);
+        co.next(S);
+        out[q0 + v] = d;
+        if (d) my_top = q0 + v + 1;
+      }
+    }
+  } else
   for (int c0 = 0; c0 < m; c0 += T * PK_V) {
     const int q0 = c0 + tid * PK_V;
-    i64 t[PK_V];
     StreamCur ce, co;
     ce.init(q0, 0, S);
     co.init(q0, C.N, S);
+    i64 t[PK_V];
     u32 M = CM_IDENT, mr[PK_V];
 #pragma unroll
     for (int v = 0; v < PK_V; v++) {
@@ -312,7 +332,7 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   const int nw = (lmax + PK_PAD) * a.in_words;
   b.stage = nw <= PK_STAGE_WORDS;
   const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;
-  if (smem > 48 * 1024) {
+  if (smem > 44 * 1024) {  // + static shared memory must fit the opt-in limit
     cudaError_t e = cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
   }
@@ -1103,6 +1123,25 @@ __device__ __forceinline__ void recon_final(const ReconArgs& a, const ReconStrea
   if (b2) raise_err(a.err, ERR_RECON);
 }
 
+// sequential fallback (one thread walks the whole stream from the exact start)
+template <int NW>
+__device__ __forceinline__ void recon_fallback(const ReconArgs& a, const ReconStream& S, int pair, ReconState<NW>& st,
+                                           const u32* F, const u32* R, int dw, int lgV, u32* H, int W, int ow,
+                                           u32 topmask, const BiasFix& bfx, bool& bad) {
+  MW<NW> mask, zero;
+#pragma unroll
+  for (int i = 0; i < NW; i++) { mask.w[i] = 0xffffffffu; zero.w[i] = 0u; }
+  mw_mask(mask, topmask);
+  if (a.diag) atomicAdd(a.diag, 1u);
+  st.lo_prev = zero;
+  mw_ld(st.lo_cur, F);
+  mw_ld(st.rj, R);
+  st.fc = 0u;
+  int q0 = 0, q1 = 0;
+  recon_walk<NW, true>(st, 0, S.count - 1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bfx,
+                       pair);
+}
+
 template <int NW>
 __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconStream& S, int pair, const u32* F,
                                                const u32* R, int lgV, int V, const BiasFix& bfx, u32* smw, int* smi,
@@ -1175,13 +1214,7 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
   } else {
     if (tid == 0) {
       *fallback = 1;
-      if (a.diag) atomicAdd(a.diag, 1u);
-      st.lo_prev = zero;
-      st.lo_cur = f0;
-      mw_ld(st.rj, R);
-      st.fc = 0u;
-      int q0 = 0, q1 = 0;
-      recon_walk<NW, true>(st, 0, nsteps, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bfx, pair);
+      recon_fallback<NW>(a, S, pair, st, F, R, dw, lgV, H, W, ow, topmask, bfx, bad);
     }
     __syncthreads();
   }
@@ -1354,15 +1387,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS) k_recon_warp(ReconArgs a) {
     recon_walk<NW, true>(sw, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bf, pair);
   } else {
     fb = true;
-    if (lane == 0) {
-      if (a.diag) atomicAdd(a.diag, 1u);
-      st.lo_prev = zero;
-      st.lo_cur = f0;
-      mw_ld(st.rj, R);
-      st.fc = 0u;
-      int q0 = 0, q1 = 0;
-      recon_walk<NW, true>(st, 0, nsteps, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bf, pair);
-    }
+    if (lane == 0) recon_fallback<NW>(a, S, pair, st, F, R, dw, lgV, H, W, ow, topmask, bf, bad);
   }
   const int owner = fb ? 0 : (nsteps > 0 ? (nsteps - 1) / V : 0);
   if (lane == owner) recon_final(a, S, pair, st, nsteps == 0, F, R, dw, lgV, H, W, ow, topmask, mask, bf);

@@ -281,3 +281,14 @@ def test_host_pipelined_path(kmx, variant):
         want = O.ks_mul_signed(1, [int(x) for x in f[p, :, 0].view(np.int32)],
                                [int(x) for x in g[p, :, 0].view(np.int32)], 32, mode="native")
         assert words_to_ints(h[p], signed=True) == want
+
+
+@pytest.mark.parametrize("n,b", [(8192, 8), (4096, 256), (8192, 64)])
+def test_config5_large_points(kmx, n, b):
+    # long digit streams (CTA reconstruction, thousands of steps) and large products
+    rng = random.Random(n + b)
+    fs = [[rng.randrange(1 << b) for _ in range(n)]]
+    gs = [[rng.randrange(1 << b) for _ in range(n)]]
+    want = {0: O.ks_mul(1, fs[0], gs[0], b, mode="native")}
+    for v in (1, 2, 3, 4):
+        _check_batch(kmx, v, fs, gs, b, want)
