@@ -240,6 +240,11 @@ def run_ours(args, cfg, rank, world, local_rank):
         for _ in range(args.warmup):
             op(fd, gd, out)
         op.status()
+        graph = None
+        if args.graphs:  # CUDA graph of the whole step (no per-kernel launch gaps)
+            graph, out = op.capture(fd, gd, out)
+            graph.replay()
+            op.status()
         L.kmx_prof_enable(1)
         import ctypes
         prof = (ctypes.c_float * 6)()
@@ -256,12 +261,15 @@ def run_ours(args, cfg, rank, world, local_rank):
         for _ in range(args.steps):
             flush_buf.fill_(1)  # L2 flush between timed steps (untimed)
             e0.record(stream)
-            op(fd, gd, out)
+            if graph is not None:
+                graph.replay()
+            else:
+                op(fd, gd, out)
             e1.record(stream)
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
             launches += L.kmx_last_launch_count()
-            if cfg["kind"] == "ks":
+            if cfg["kind"] == "ks" and graph is None:
                 L.kmx_prof_read(prof, 6)
                 for i in range(6):
                     kern[i] += prof[i]
@@ -270,6 +278,17 @@ def run_ours(args, cfg, rank, world, local_rank):
         if mon is not None:
             clocks = mon.stop()
         op.status()
+        if cfg["kind"] == "ks" and graph is not None:
+            # per-kernel durations: CUDA events around each launch (kmx_prof),
+            # eager launches right after the graph-timed region
+            L.kmx_prof_enable(1)
+            for _ in range(args.steps):
+                flush_buf.fill_(1)
+                op(fd, gd, out)
+                L.kmx_prof_read(prof, 6)
+                for i in range(6):
+                    kern[i] += prof[i]
+            L.kmx_prof_enable(0)
         total_ms = mor(total_ms)
         ms = total_ms / args.steps
         rec = {"products_per_s": job_products(B, world) / (ms * 1e-3), "ms_per_step": ms, "launches_per_step": launches / args.steps}
@@ -474,6 +493,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-all-variants", dest="all_variants", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-graphs", dest="graphs", action="store_false",
+                    help="launch kernels eagerly instead of replaying a captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -495,6 +516,7 @@ def main():
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32 limbs (exact integer)",
         "data": "synthetic (seeded numpy PCG64, BASELINE shapes)", "config": config_json(cfg, v),
         "parallelism": f"replicas x{world} (independent pairs, no collective)",
+        "cuda_graph": bool(args.graphs),
     }
     if cfg["kind"] == "ks":
         mul_ms = rec["kernel_ms"].get("mul")

@@ -70,6 +70,24 @@ class KsBatch:
         check(rc, "kmx_ks_mul")
         return out
 
+    def capture(self, f, g, out=None):
+        """Capture this product (fixed buffers) into a CUDA graph; returns
+        (graph, out).  ``graph.replay()`` re-runs pack -> multiply -> finish
+        [-> reconstruct] with no per-kernel launch overhead."""
+        torch = _torch()
+        if out is None:
+            out = self.empty_out()
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self(f, g, out, stream=s)  # warm (attributes, occupancy queries)
+        s.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            self(f, g, out, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return graph, out
+
     def status(self, stream=None):
         """Synchronise and raise the latched device error, if any."""
         torch = _torch()
@@ -129,6 +147,22 @@ class BksBatch:
                                st.cuda_stream)
         check(rc, "kmx_bks_mul")
         return out
+
+    def capture(self, f, g, out=None):
+        """CUDA-graph capture of this bivariate product (see KsBatch.capture)."""
+        torch = _torch()
+        if out is None:
+            out = torch.empty((self.batch, 2 * self.lx - 1, 2 * self.ly - 1), dtype=torch.int64, device=self.device)
+        s = torch.cuda.Stream(self.device)
+        s.wait_stream(torch.cuda.current_stream(self.device))
+        with torch.cuda.stream(s):
+            self(f, g, out, stream=s)
+        s.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph, stream=s):
+            self(f, g, out, stream=s)
+        torch.cuda.current_stream(self.device).wait_stream(s)
+        return graph, out
 
     def status(self, stream=None):
         torch = _torch()

@@ -168,7 +168,8 @@ struct StreamCur {
 __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
   extern __shared__ u32 pk_sc[];
   __shared__ u32 sm_scan[PK_T / 32];
-  __shared__ int sm_order, sm_top;
+  __shared__ int sm_order;
+  __shared__ unsigned long long sm_top;  // (top nonzero digit index + 1) << 32 | its value
   const int T = blockDim.x;  // 32..PK_T, sized to the operand
   __shared__ i64 sm_carry;
   const int tid = threadIdx.x;
@@ -219,7 +220,7 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
     block_prefix_u64(C.cf, C.L, C.biasw, C.bmask, A.op[o].prefix + (long long)pair * A.op[o].prefix_pair_stride);
     __syncthreads();
   }
-  if (tid == 0) { sm_top = 0; sm_order = 1; sm_carry = 0; }
+  if (tid == 0) { sm_top = 0ull; sm_order = 1; sm_carry = 0; }
   const int S = 2 * C.N;
   // negated packs: order of E and O from the most significant differing digit
   if (neg && tid < 32) {
@@ -248,6 +249,7 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
   const int negative = neg ? ((order < 0) != flip ? 1 : 0) : 0;
 
   int my_top = 0;
+  u32 my_topv = 0u;
   if (!neg && C.N >= C.b) {
     // disjoint bit fields (pack.py:66-67): V = E | O, no carries at all --
     // a pure gather, every thread independent
@@ -261,7 +263,7 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
         ce.next(S);
         co.next(S);
         out[q0 + v] = d;
-        if (d) my_top = q0 + v + 1;
+        if (d) { my_top = q0 + v + 1; my_topv = d; }
       }
     }
   } else
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
     for (int v = 0; v < PK_V; v++) {
       d[v] = (u32)(t[v] + c);
       c = cm_apply(mr[v], c);
-      if (q0 + v < m && d[v]) my_top = q0 + v + 1;
+      if (q0 + v < m && d[v]) { my_top = q0 + v + 1; my_topv = d[v]; }
     }
     if (q0 + PK_V <= m) {
       uint4* dst = reinterpret_cast<uint4*>(out + q0);
@@ -311,12 +313,12 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
     __syncthreads();
   }
   if (tid == 0 && sm_carry != 0) raise_err(A.err, ERR_INEXACT);  // operand overflow (cannot happen)
-  atomicMax(&sm_top, my_top);
+  if (my_top) atomicMax(&sm_top, ((unsigned long long)my_top << 32) | my_topv);
   __syncthreads();
   if (tid == 0) {
-    const int top = sm_top;
+    const int top = (int)(sm_top >> 32);
     meta[0] = (u32)negative;
-    meta[1] = top ? (u32)(32 * (top - 1) + 32 - __clz(out[top - 1])) : 0u;
+    meta[1] = top ? (u32)(32 * (top - 1) + 32 - __clz((u32)sm_top)) : 0u;
   }
 }
 

@@ -292,3 +292,24 @@ def test_config5_large_points(kmx, n, b):
     want = {0: O.ks_mul(1, fs[0], gs[0], b, mode="native")}
     for v in (1, 2, 3, 4):
         _check_batch(kmx, v, fs, gs, b, want)
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
+def test_cuda_graph_replay(kmx, variant):
+    # the bench replays a captured CUDA graph of the whole step; results must
+    # match the oracle on every replay, including after new inputs are copied in
+    rng = random.Random(55 + variant)
+    B, n, b = 8, 256, 64
+    fs = [[rng.randrange(1 << b) for _ in range(n)] for _ in range(B)]
+    gs = [[rng.randrange(1 << b) for _ in range(n)] for _ in range(B)]
+    kb = kmx.KsBatch(variant, B, n, n, b)
+    fd, gd = _dev_words(fs, 2), _dev_words(gs, 2)
+    graph, out = kb.capture(fd, gd)
+    for rep in range(2):
+        graph.replay()
+        kb.status()
+        got = _host_ints(out)
+        assert got[rep] == O.ks_mul(1, fs[rep], gs[rep], b, mode="native")
+        fs2 = [[rng.randrange(1 << b) for _ in range(n)] for _ in range(B)]
+        fd.copy_(_dev_words(fs2, 2))
+        fs = fs2
