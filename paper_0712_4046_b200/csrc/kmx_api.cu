@@ -28,6 +28,14 @@ namespace {
 
 int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
+// K2 engine choice: KMX_TC=0 forces the integer-pipe schoolbook, KMX_TC=1 the
+// tcgen05 byte convolution wherever its shape gate admits the operands.
+bool use_tensor_mul(int ma, int mb) {
+  static const int mode = getenv("KMX_TC") ? atoi(getenv("KMX_TC")) : 0;
+  if (mode == 0) return false;
+  return tc_supported(ma, mb);
+}
+
 // ---- tiny host bignum for the four-point bound (ksint.py:282-286)
 typedef std::vector<uint32_t> Big;
 Big big_from_u64(unsigned long long v) { Big r; while (v) { r.push_back((uint32_t)v); v >>= 32; } return r; }
@@ -267,7 +275,11 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
   ma.counter = (int*)(err + 1);
   prof_begin(1, st);
-  if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  if (use_tensor_mul(p.mf, p.mg)) {
+    if ((e = launch_tcmul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  } else {
+    if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  }
   prof_end(1, st);
   g_launches++;
 
