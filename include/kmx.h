@@ -130,6 +130,17 @@ int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits,
  * second, full chip), the roofline denominator for the multiply kernels. */
 double kmx_imad_peak(int iters);
 
+/* Engine the multiply stage (K2) uses for this product shape: 0 = the
+ * integer-pipe schoolbook (IMAD.WIDE.U32, kmx_mul.cu), 1 = the tcgen05 u8
+ * byte convolution with TMEM accumulators (kmx_tc.cu).  KMX_TC=0 in the
+ * environment forces 0.  Negative: error code. */
+int kmx_mul_engine(int variant, int len_f, int len_g, int coeff_bits, unsigned flags);
+
+/* Measured dense u8 x u8 -> s32 tcgen05.mma throughput on the current
+ * device (multiply-accumulates per second, M=128 N=256 K=32 from shared
+ * memory, all SMs): the tensor roofline denominator for K2. */
+double kmx_tc_peak(int iters);
+
 /* Human-readable message for a return code. */
 const char* kmx_error_string(int code);
 

@@ -60,6 +60,8 @@ _SIGS = {
     "kmx_bks_mul": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "kmx_bks_mul_host": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp]),
     "kmx_imad_peak": (ctypes.c_double, [_i]),
+    "kmx_tc_peak": (ctypes.c_double, [_i]),
+    "kmx_mul_engine": (_i, [_i, _i, _i, _i, _u]),
     "kmx_error_string": (ctypes.c_char_p, [_i]),
     "kmx_last_launch_count": (_i, []),
     "kmx_prof_enable": (None, [_i]),

@@ -184,5 +184,18 @@ def imad_peak(iters: int = 4096) -> float:
     return float(lib().kmx_imad_peak(iters))
 
 
+def tc_peak(iters: int = 2000) -> float:
+    """Measured dense tcgen05 u8 MMA multiply-accumulates/s on the current device."""
+    return float(lib().kmx_tc_peak(iters))
+
+
+def mul_engine(variant: int, len_f: int, len_g: int, coeff_bits: int, signed: bool = False) -> str:
+    """Which multiply engine (K2) a product shape runs on: "tensor" or "imad"."""
+    rc = lib().kmx_mul_engine(variant, len_f, len_g, coeff_bits, KMX_SIGNED if signed else 0)
+    if rc < 0:
+        check(rc, "mul_engine")
+    return "tensor" if rc == 1 else "imad"
+
+
 def last_launch_count() -> int:
     return int(lib().kmx_last_launch_count())

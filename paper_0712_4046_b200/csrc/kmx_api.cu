@@ -31,8 +31,8 @@ int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
 // K2 engine choice: KMX_TC=0 forces the integer-pipe schoolbook, KMX_TC=1 the
 // tcgen05 byte convolution wherever its shape gate admits the operands.
 bool use_tensor_mul(int ma, int mb) {
-  static const int mode = getenv("KMX_TC") ? atoi(getenv("KMX_TC")) : 0;
-  if (mode == 0) return false;
+  const char* v = getenv("KMX_TC");
+  if (v && *v && atoi(v) == 0) return false;
   return tc_supported(ma, mb);
 }
 
@@ -599,6 +599,15 @@ int kmx_reconstruct_host(int batch, int count, int width_bits, const uint32_t* f
 }
 
 double kmx_imad_peak(int iters) { return measure_imad_peak(iters > 0 ? iters : 4096); }
+
+double kmx_tc_peak(int iters) { return measure_tc_peak(iters > 0 ? iters : 2000); }
+
+int kmx_mul_engine(int variant, int len_f, int len_g, int coeff_bits, unsigned flags) {
+  KsPlan p;
+  int rc = make_plan(p, variant, 1, len_f, len_g, coeff_bits, 0, flags);
+  if (rc) return rc;
+  return use_tensor_mul(p.mf, p.mg) ? 1 : 0;
+}
 
 const char* kmx_error_string(int code) {
   switch (code) {

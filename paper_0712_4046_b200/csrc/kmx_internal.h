@@ -59,6 +59,7 @@ void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr);
 // K2 on tcgen05 (kmx_tc.cu): same MulArgs contract, zero band spills.
 bool tc_supported(int ma, int mb);
 cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st);
+double measure_tc_peak(int iters);
 
 // Signed inputs (bias lift): the coefficient writers apply
 // h = h' - 2^(b-1) (J*f' + J*g') + 2^(2b-2) (J*J) before storing, from the

@@ -3,31 +3,44 @@
 // product the reference's mul() reduces to) as u8 x u8 -> s32 tcgen05.mma
 // byte convolutions with TMEM accumulators.
 //
-// Formulation (one CTA per sub-product z; a = the longer operand, b = the
-// shorter, both little-endian byte strings of La, Lb bytes):
+// Formulation (a = the longer operand, b = the shorter, both little-endian
+// byte strings of La, Lb bytes):
 //
 //   c[k] = sum_i a[i] b[k-i]   (byte convolution; the product is sum_k c[k] 256^k)
 //
-// An output tile covers byte positions k0 + 16m + n, m < 128 (MMA M), n < 16
-// (MMA N), so D[m][n] = sum_u A[m][u] B[n][u] with
+// One MMA tile (M = 128, N = 16H) covers the byte positions
 //
-//   A[m][u] = a[k0 + 16m + u]   and   B[n][u] = b[n - u].
+//   k0 + alpha_m + beta_n,   alpha_m = 16 (m % 8) + 128H (m / 8),
+//                            beta_n  = (n % 16) + 128 (n / 16),
+//
+// a contiguous run of 2048H positions, as D[m][n] = sum_u A[m][u] B[n][u] with
+//
+//   A[m][u] = a[k0 + alpha_m + u]   and   B[n][u] = b[beta_n - u].
 //
 // A needs no materialisation: in the K-major SWIZZLE_NONE canonical layout
-// ((8,m),(16B,2)) : ((16B,SBO),(1,LBO)) row m of a core matrix sits 16 bytes
-// after row m-1, so a plain zero-padded copy of a in shared memory IS the A
-// operand with LBO = 16 and SBO = 128; stepping K by 32 bytes only moves the
-// descriptor's start address.  B (16 shifted copies of the reversed b) is
-// built once per product and reused by every output tile.  Each tile owns 16
-// TMEM columns of s32 (sums of at most min(La,Lb) <= 33025 byte products, so
-// no overflow) and its own mbarrier, so the epilogue of tile t overlaps the
-// MMAs of tile t+1.
+// ((8,m),(16B,2)) : ((16B,SBO),(1,LBO)) row r of a core matrix sits 16 bytes
+// after row r-1, so a plain zero-padded copy of a in shared memory IS the A
+// operand with LBO = 16 and SBO = 128H; stepping K by 32 bytes (or the tile by
+// 2048H) only moves the descriptor's start address.  B (16H shifted, reversed
+// copies of b) is built per K-chunk from a staged copy of b (half-warp byte
+// permutes), multi-buffered against the MMAs with mbarriers, and shared by all tiles of
+// the CTA (warp 0 issues the MMAs, warps 1-3 build B stages into an mbarrier
+// ring).  In SS mode the MMA is paced by its shared-memory operand reads
+// (~110 B/clk measured: tools/microbench/tc_peak.cu), so a wider N buys more
+// MACs per A byte; the host picks H per shape from that cost model.
 //
-// Epilogue: thread m reads its 16 accumulators (tcgen05.ld 32x32b.x16), forms
-// four 32-bit limb column sums (< 2^56), and one exact block carry scan turns
-// the 512 limbs of the tile into normalised 32-bit digits; the carry out of
-// the tile feeds the next tile.  The product is written in K2's band format
-// (kmx_internal.h MulArgs) with zero band spills, so K3 is unchanged.
+// TMEM: each tile owns 16H columns of 32-bit sums.  A sum has at most
+// min(La,Lb) byte products < 2^16 each; read as u32 (the accumulator wraps, no
+// saturation) it is exact for min(La,Lb) <= 65536.
+//
+// Epilogue: thread m reads its 16H accumulators (tcgen05.ld 32x32b.x16),
+// forms limb column sums (< 2^56), stages them in shared memory in limb
+// order, and one exact block carry scan over {0,1} overflow maps normalises
+// the tile's 512H limbs; the carry feeds the next tile of the CTA and the
+// CTA's last carry becomes the band spill K3 folds in (K2's MulArgs contract).
+#include <cstdio>
+#include <cstdlib>
+
 #include "kmx_internal.h"
 #include "kmx_common.cuh"
 
@@ -35,24 +48,50 @@ namespace kmx {
 
 namespace {
 
-constexpr int TC_THREADS = 128;
-constexpr int TC_M = 128;                  // MMA M (rows of a at 16-byte stride)
-constexpr int TC_N = 16;                   // MMA N (byte shifts of b)
-constexpr int TC_T = TC_M * TC_N;          // output byte positions per tile
-constexpr int TC_LIMBS = TC_T / 4;         // product limbs per tile
-constexpr int TC_MAXT = 16;                // tiles per CTA (TMEM: 16 x 16 columns)
-constexpr int APRE = 2048 + 64;            // zero bytes before a (>= 2032 + 31 + 16)
-constexpr int APOST = 2048 + 64;           // zero bytes after a
-constexpr int BRPRE = 64;                  // zero bytes before reversed b
-constexpr int BRPOST = 96;
+constexpr int TC_EPI = 128;  // warps 0-3: epilogue (TMEM lane quarters)
+constexpr int TC_MAX_COLS = 256;  // TMEM columns per CTA (two CTAs per SM fit)
 
-// idesc: S32 accumulator (bits 4-5 = 2), A/B unsigned 8-bit (0), K-major,
-// N >> 3 at bit 17, M >> 4 at bit 24.
-constexpr uint32_t TC_IDESC = (2u << 4) | ((uint32_t)(TC_N >> 3) << 17) | ((uint32_t)(TC_M >> 4) << 24);
+template <int H>
+struct TcG {
+  static constexpr int N = 16 * H;
+  static constexpr int T = 2048 * H;                 // output byte positions per tile
+  static constexpr int LIMBS = 512 * H;              // product limbs per tile
+  static constexpr int SBO_A = 128 * H;              // A: stride of 8-row groups
+  static constexpr int AMAX = 16 * 7 + SBO_A * 15;   // largest alpha_m
+  static constexpr int APAD = (AMAX + 32 + 64 + 15) & ~15;
+  static constexpr int BMAX = 15 + 128 * (H - 1);    // largest beta_n
+  static constexpr int STEPB = 512 * H;              // B bytes per K-step
+  // idesc: S32 accumulator (bits 4-5 = 2), A/B unsigned 8-bit, K-major,
+  // N >> 3 at bit 17, M >> 4 = 8 at bit 24.
+  static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+};
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
+__host__ __device__ inline int fdiv32(int x) { return x >= 0 ? x / 32 : -((-x + 31) / 32); }
+
+// K-steps u0 = ulo + 32 s, s in [0, S), and the steps tile t needs.
+struct TcDims {
+  int La, Lb, ulo, S, ntiles;
+};
+template <int H>
+__host__ __device__ inline TcDims tc_dims(int mA, int mB) {
+  TcDims d;
+  d.La = 4 * mA;
+  d.Lb = 4 * mB;
+  d.ulo = -32 * ((d.Lb - 1 + 31) / 32);
+  d.S = fdiv32(TcG<H>::BMAX - d.ulo) + 1;
+  d.ntiles = (d.La + d.Lb - 1 + TcG<H>::T - 1) / TcG<H>::T;
+  return d;
 }
+template <int H>
+__host__ __device__ inline void tc_tile_steps(const TcDims& d, int t, int& slo, int& shi) {
+  const int k0 = t * TcG<H>::T;
+  slo = -fdiv32(k0 + TcG<H>::AMAX + 31 + d.ulo);  // ceil((-k0 - AMAX - 31 - ulo) / 32)
+  if (slo < 0) slo = 0;
+  shi = fdiv32(d.La - k0 - 1 - d.ulo) + 1;
+  if (shi > d.S) shi = d.S;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 
 // SWIZZLE_NONE K-major smem matrix descriptor (sm_100: version 1 at bit 46).
 __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
@@ -60,21 +99,22 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t 
          ((uint64_t)((sbo >> 4) & 0x3FFFu) << 32) | (1ull << 46);
 }
 
-__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+__device__ __forceinline__ void mma_i8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                       uint32_t accum) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n"
-      :: "r"(tmem_d), "l"(adesc), "l"(bdesc), "r"(TC_IDESC), "r"(accum));
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
 }
 
 __device__ __forceinline__ void mma_commit(uint32_t mbar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" :: "r"(mbar)
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(mbar)
                : "memory");
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t mbar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(mbar), "r"(count) : "memory");
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(mbar), "r"(count) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
@@ -84,7 +124,9 @@ __device__ __forceinline__ void mbar_wait(uint32_t mbar, uint32_t parity) {
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n\t}\n"
-        : "=r"(done) : "r"(mbar), "r"(parity) : "memory");
+        : "=r"(done)
+        : "r"(mbar), "r"(parity)
+        : "memory");
   } while (!done);
 }
 
@@ -98,7 +140,7 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
-// Carry maps {0,1} -> {0,1}: bit0 = f(0), bit1 = f(1).  compose(later, earlier).
+// Carry maps {0,1} -> {0,1}: bit0 = f(0), bit1 = f(1).  cm2(later, earlier).
 __device__ __forceinline__ uint32_t cm2(uint32_t later, uint32_t earlier) {
   const uint32_t h0 = (later >> (earlier & 1u)) & 1u;
   const uint32_t h1 = (later >> ((earlier >> 1) & 1u)) & 1u;
@@ -106,233 +148,558 @@ __device__ __forceinline__ uint32_t cm2(uint32_t later, uint32_t earlier) {
 }
 constexpr uint32_t CM2_ID = 2u;  // f(0)=0, f(1)=1
 
+constexpr int TC_MAXNB = 4;  // B ring stages
+
 struct TcShared {
-  unsigned long long mbar[TC_MAXT];
+  unsigned long long bar_full[TC_MAXNB];   // B stage built (3 builder warps arrive)
+  unsigned long long bar_empty[TC_MAXNB];  // MMAs that read the stage completed (commit)
+  unsigned long long bar_done;             // all MMAs of the CTA completed
+  unsigned long long s_cout[TC_EPI / 32];
+  unsigned long long carry;                // carry into the next tile
   uint32_t tmem_base;
-  uint32_t warp_map[TC_THREADS / 32];
-  unsigned long long carry;       // carry into the next tile
+  uint32_t warp_map[TC_EPI / 32];
 };
 
-}  // namespace
+struct TcArgs {
+  MulArgs m;
+  int KC;       // K-steps per B stage
+  int NB;       // B stages in the ring (2..TC_MAXNB)
+  int TPC;      // tiles per CTA
+  int nranges;  // CTAs per product = ceil(ntiles / TPC)
+};
 
-// Shape gate: the longer operand slides (A), the shorter one is materialised
-// 16 times (B); TMEM columns and shared memory bound the sizes.
-static void tc_sizes(int ma, int mb, int* la, int* lb, int* steps, int* ntiles, size_t* smem) {
-  const int lA = 4 * (ma > mb ? ma : mb), lB = 4 * (ma > mb ? mb : ma);
-  const int ulo = -32 * ((lB - 1 + 31) / 32);
-  const int S = (32 - ulo) / 32;
-  *la = lA; *lb = lB; *steps = S;
-  *ntiles = (lA + lB - 1 + TC_T - 1) / TC_T;
-  const size_t apad = (size_t)APRE + lA + APOST;
-  const size_t brpad = (size_t)BRPRE + lB + BRPOST;
-  *smem = sizeof(TcShared) + apad + brpad + (size_t)512 * S + 512;
+__host__ __device__ inline size_t round128(size_t x) { return (x + 127) & ~(size_t)127; }
+
+// zero padding around the staged b: the window words read by the B build
+// lie in [(-BMAX - 32) / 4, (Lb + 128H + 96) / 4)
+template <int H>
+struct TcB {
+  static constexpr int BPAD = (TcG<H>::BMAX + 128 + 15) & ~15;
+};
+
+template <int H>
+__host__ __device__ inline size_t tc_smem(int La, int Lb, int KC, int NB) {
+  return round128(sizeof(TcShared)) + round128((size_t)La + 2 * TcG<H>::APAD) +
+         round128((size_t)Lb + 2 * TcB<H>::BPAD) + (size_t)NB * KC * TcG<H>::STEPB;
 }
 
-bool tc_supported(int ma, int mb) {
-  int la, lb, S, nt;
-  size_t smem;
-  tc_sizes(ma, mb, &la, &lb, &S, &nt, &smem);
-  return nt <= TC_MAXT && lb <= 33024 && smem <= 200 * 1024;
+__device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(mbar) : "memory");
 }
 
-__global__ void __launch_bounds__(TC_THREADS) k_tcmul(MulArgs a) {
+// ---------------------------------------------------------------- kernel
+// Warp roles: warp 0 lane 0 issues the MMAs; warps 1..NW-1 build the B
+// stages; all warps stage the operands; warps 0-3 run the epilogue (TMEM
+// lanes 32w..32w+31 belong to warp w).  NW = 4 suits CTAs with one or two
+// tiles (occupancy), NW = 8 CTAs whose B build is shared by more tiles.
+template <int H, int NW>
+__global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
+  constexpr int TC_THREADS = 32 * NW;  // warp 0: MMA issue, warps 1..NW-1: B build
+  using G = TcG<H>;
+  const MulArgs& a = ta.m;
   extern __shared__ __align__(128) unsigned char tsm[];
   TcShared& sh = *reinterpret_cast<TcShared*>(tsm);
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int z = blockIdx.x;
+  const int z = blockIdx.x / ta.nranges, rg = blockIdx.x % ta.nranges;
 
   // operand roles: A slides (longer), B is materialised (shorter)
   const bool sw = a.mb > a.ma;
-  const uint32_t* Ag = (sw ? a.B + (long long)z * a.b_stride : a.A + (long long)z * a.a_stride);
-  const uint32_t* Bg = (sw ? a.A + (long long)z * a.a_stride : a.B + (long long)z * a.b_stride);
+  const uint32_t* Ag = sw ? a.B + (long long)z * a.b_stride : a.A + (long long)z * a.a_stride;
+  const uint32_t* Bg = sw ? a.A + (long long)z * a.a_stride : a.B + (long long)z * a.b_stride;
   const int mA = sw ? a.mb : a.ma, mB = sw ? a.ma : a.mb;
-  const int La = 4 * mA, Lb = 4 * mB;
-  const int ulo = -32 * ((Lb - 1 + 31) / 32);
-  const int S = (32 - ulo) / 32;
-  const int ntiles = (La + Lb - 1 + TC_T - 1) / TC_T;
+  const TcDims d = tc_dims<H>(mA, mB);
   const int mp = a.ma + a.mb;
+  const int t0 = rg * ta.TPC;
+  const int t1 = min(d.ntiles, t0 + ta.TPC);
+  const int nt = t1 - t0;
+  const int KC = ta.KC, NB = ta.NB;
 
-  unsigned char* apad = tsm + ((sizeof(TcShared) + 127) & ~(size_t)127);
-  unsigned char* brpad = apad + ((APRE + La + APOST + 127) & ~127);
-  unsigned char* bmat = brpad + ((BRPRE + Lb + BRPOST + 127) & ~127);
+  unsigned char* apad = tsm + round128(sizeof(TcShared));
+  unsigned char* bpad = apad + round128((size_t)d.La + 2 * G::APAD);
+  unsigned char* bring = bpad + round128((size_t)d.Lb + 2 * TcB<H>::BPAD);
 
+  // K-step span of the CTA's tiles
+  int cs_lo = d.S, cs_hi = 0;
+  for (int t = t0; t < t1; t++) {
+    int slo, shi;
+    tc_tile_steps<H>(d, t, slo, shi);
+    if (slo < shi) {
+      cs_lo = min(cs_lo, slo);
+      cs_hi = max(cs_hi, shi);
+    }
+  }
+  const int clo = cs_lo < cs_hi ? cs_lo / KC : 0;
+  const int chi = cs_lo < cs_hi ? (cs_hi + KC - 1) / KC : 0;
+
+  uint32_t cols = 32;
+  while (cols < (uint32_t)(nt * G::N)) cols <<= 1;
   if (warp == 0) {
-    // TMEM: 16 columns per tile, power of two >= 32
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(ntiles * TC_N)) cols <<= 1;
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
                  "r"(cols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
-    for (int t = 0; t < ntiles; t++) mbar_init(smem_u32(&sh.mbar[t]), 1);
+    for (int i = 0; i < TC_MAXNB; i++) {
+      mbar_init(smem_u32(&sh.bar_full[i]), TC_THREADS / 32 - 1);
+      mbar_init(smem_u32(&sh.bar_empty[i]), 1);
+    }
+    mbar_init(smem_u32(&sh.bar_done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     sh.carry = 0ull;
   }
-
-  // A: zero-padded copy of the longer operand (word copies; APRE, La multiples of 4)
+  // A: zero-padded copy of the longer operand; b: zero-padded copy of the shorter
   {
-    uint32_t* aw = reinterpret_cast<uint32_t*>(apad);
-    const int nw = (APRE + La + APOST) / 4;
-    for (int w = tid; w < nw; w += TC_THREADS) {
-      const int j = w - APRE / 4;
-      aw[w] = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
+    uint4* aw = reinterpret_cast<uint4*>(apad);
+    const int nq = (d.La + 2 * G::APAD) / 16;
+    const int qa = G::APAD / 16;
+    const bool al = (mA & 3) == 0 && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+    for (int w = tid; w < nq; w += TC_THREADS) {
+      const int j = 4 * (w - qa);
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (j >= 0 && j < mA) {
+        if (al) {
+          v = __ldg(reinterpret_cast<const uint4*>(Ag + j));
+        } else {
+          v.x = __ldg(Ag + j);
+          v.y = j + 1 < mA ? __ldg(Ag + j + 1) : 0u;
+          v.z = j + 2 < mA ? __ldg(Ag + j + 2) : 0u;
+          v.w = j + 3 < mA ? __ldg(Ag + j + 3) : 0u;
+        }
+      }
+      aw[w] = v;
     }
-    // reversed b: brpad[BRPRE + x] = b[Lb - 1 - x]
-    uint32_t* bw = reinterpret_cast<uint32_t*>(brpad);
-    const int nb = (BRPRE + Lb + BRPOST) / 4;
-    for (int w = tid; w < nb; w += TC_THREADS) {
-      const int j = w - BRPRE / 4;
-      bw[w] = (j >= 0 && j < mB) ? __byte_perm(__ldg(Bg + (mB - 1 - j)), 0u, 0x0123) : 0u;
+    uint32_t* bw = reinterpret_cast<uint32_t*>(bpad);
+    const int nbw = (d.Lb + 2 * TcB<H>::BPAD) / 4;
+    const int ba = TcB<H>::BPAD / 4;
+    for (int w = tid; w < nbw; w += TC_THREADS) {
+      const int j = w - ba;
+      bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
     }
   }
-  __syncthreads();
-  // B: for K-step s, a 512-byte block [g(2)][j(2)][r(8)][16 B] holding
-  // B[n = 8g + r][u = ulo + 32s + 16j + kk] = brpad[BRPRE + Lb - 1 - n + u]
-  {
-    const uint32_t* bw = reinterpret_cast<const uint32_t*>(brpad);
-    uint4* dst = reinterpret_cast<uint4*>(bmat);
-    const int nchunks = 32 * S;
-    for (int ci = tid; ci < nchunks; ci += TC_THREADS) {
-      const int s = ci >> 5, g = (ci >> 4) & 1, j = (ci >> 3) & 1, r = ci & 7;
-      const int n = 8 * g + r;
-      const int o = BRPRE + Lb - 1 - n + ulo + 32 * s + 16 * j;
-      const int w = o >> 2, sh8 = (o & 3) * 8;
-      const uint32_t x0 = bw[w], x1 = bw[w + 1], x2 = bw[w + 2], x3 = bw[w + 3], x4 = bw[w + 4];
-      dst[ci] = make_uint4(__funnelshift_r(x0, x1, sh8), __funnelshift_r(x1, x2, sh8),
-                           __funnelshift_r(x2, x3, sh8), __funnelshift_r(x3, x4, sh8));
-    }
-  }
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = sh.tmem_base;
 
-  // ---- MMA issue: one thread, tile by tile, one commit per tile
-  if (tid == 0) {
-    const uint32_t abase = smem_u32(apad) + APRE;
-    const uint32_t bbase = smem_u32(bmat);
-    for (int t = 0; t < ntiles; t++) {
-      const int k0 = t * TC_T;
-      // valid u: a side  -k0 - 2032 <= u <= La - k0 - 1, b side ulo <= u < 32
-      int slo = (-k0 - (TC_M - 1) * 16 - ulo);
-      slo = slo <= 0 ? 0 : slo / 32;
-      int shi = (La - k0 - 1 - ulo);
-      shi = shi < 0 ? 0 : shi / 32 + 1;
-      if (shi > S) shi = S;
-      for (int s = slo; s < shi; s++) {
-        const uint64_t ad = sdesc(abase + k0 + ulo + 32 * s, 16, 128);
-        const uint64_t bd = sdesc(bbase + 512 * s, 128, 256);
-        mma_i8(tmem + t * TC_N, ad, bd, s > slo ? 1u : 0u);
+  if (warp == 0) {
+    // ---- MMA issuer
+    if (lane == 0) {
+      const uint32_t sA = smem_u32(apad) + G::APAD;
+      uint32_t started = 0u;
+      for (int c = clo; c < chi; c++) {
+        const int k = c - clo, st = k % NB;
+        mbar_wait(smem_u32(&sh.bar_full[st]), (uint32_t)((k / NB) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int sb = c * KC, se = min(d.S, sb + KC);
+        const uint32_t sB = smem_u32(bring + (size_t)st * KC * G::STEPB);
+        for (int t = t0; t < t1; t++) {
+          int slo, shi;
+          tc_tile_steps<H>(d, t, slo, shi);
+          const int s0 = max(slo, sb), s1 = min(shi, se);
+          const uint32_t dcol = tmem + (uint32_t)((t - t0) * G::N);
+          const uint32_t abase = sA + (uint32_t)(t * G::T + d.ulo);
+          for (int s = s0; s < s1; s++) {
+            const uint64_t ad = sdesc(abase + 32u * (uint32_t)s, 16, G::SBO_A);
+            const uint64_t bd = sdesc(sB + (uint32_t)((s - sb) * G::STEPB), 128, 256);
+            mma_i8(dcol, ad, bd, G::IDESC, (started >> (t - t0)) & 1u);
+            started |= 1u << (t - t0);
+          }
+        }
+        mma_commit(smem_u32(&sh.bar_empty[st]));
       }
-      mma_commit(smem_u32(&sh.mbar[t]));  // empty tiles complete immediately
+      mma_commit(smem_u32(&sh.bar_done));
+    }
+    __syncwarp();
+  } else {
+    // ---- B builders: half-warp hb owns items hb, hb + 6, ...; an item is
+    // (step, kc, j) and lane nl writes row n = nl + 16j of it:
+    //   B[n][u0 + 16kc + kk] = b[nl + 128j - u0 - 16kc - kk]
+    //     = byte (16 + nl - kk) of the 32-byte window at w0 = 128j - u0 - 16kc - 16
+    const int hb = 2 * (warp - 1) + (lane >> 4), nl = lane & 15;
+    const int A0 = (13 + nl) >> 2, r0 = (13 + nl) & 3;
+    const uint32_t psel = (uint32_t)(r0 + 3) | ((uint32_t)(r0 + 2) << 4) | ((uint32_t)(r0 + 1) << 8) |
+                          ((uint32_t)r0 << 12);
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(bpad) + TcB<H>::BPAD / 4;
+    constexpr int NHB = 2 * (TC_THREADS / 32 - 1);
+    for (int c = clo; c < chi; c++) {
+      const int k = c - clo, st = k % NB;
+      if (k >= NB) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((k / NB) - 1) & 1));
+      unsigned char* bb = bring + (size_t)st * KC * G::STEPB;
+      const int sb = c * KC, se = min(d.S, sb + KC);
+      const int nitems = (se - sb) * 2 * H;
+      for (int ib = 0; ib < nitems; ib += 2 * NHB) {
+        uint32_t wv[2];
+        int doff[2];
+        bool valid[2];
+#pragma unroll
+        for (int x = 0; x < 2; x++) {
+          const int it = ib + x * NHB + hb;
+          valid[x] = it < nitems;
+          const int sl = valid[x] ? it / (2 * H) : 0;
+          const int rem = valid[x] ? it - sl * 2 * H : 0;
+          const int kc = rem & 1, j = rem >> 1;
+          const int u0 = d.ulo + 32 * (sb + sl);
+          const int w0 = 128 * j - u0 - 16 * kc - 16;
+          wv[x] = bw[(w0 >> 2) + nl];
+          doff[x] = sl * G::STEPB + 256 * ((nl >> 3) + 2 * j) + 128 * kc + 16 * (nl & 7);
+        }
+#pragma unroll
+        for (int x = 0; x < 2; x++) {
+          uint32_t W[5];
+#pragma unroll
+          for (int q = 0; q < 5; q++) W[q] = __shfl_sync(0xffffffffu, wv[x], A0 - 3 + q, 16);
+          if (valid[x]) {
+            uint4 o;
+            o.x = __byte_perm(W[3], W[4], psel);
+            o.y = __byte_perm(W[2], W[3], psel);
+            o.z = __byte_perm(W[1], W[2], psel);
+            o.w = __byte_perm(W[0], W[1], psel);
+            *reinterpret_cast<uint4*>(bb + doff[x]) = o;
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sh.bar_full[st]));
     }
   }
+  mbar_wait(smem_u32(&sh.bar_done), 0);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
-  // ---- epilogue: limb sums, exact carry scan, digits
+  // ---- epilogue: limb sums -> staged in limb order -> exact carry scan
+  unsigned long long* stg = reinterpret_cast<unsigned long long*>(bring);  // 4096H bytes (NB*KC >= 8)
   uint32_t* Pz = a.P + (long long)z * a.p_stride;
-  for (int t = 0; t < ntiles; t++) {
-    const int k0 = t * TC_T;
-    int slo = (-k0 - (TC_M - 1) * 16 - ulo);
-    slo = slo <= 0 ? 0 : slo / 32;
-    int shi = (La - k0 - 1 - ulo);
-    shi = shi < 0 ? 0 : shi / 32 + 1;
-    if (shi > S) shi = S;
-    uint32_t v[16];
-    mbar_wait(smem_u32(&sh.mbar[t]), 0);
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (shi > slo) {
-      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(t * TC_N), v);
-    } else {
+  const int m = tid;
+  const bool epi = warp < TC_EPI / 32;
+  for (int t = t0; t < t1; t++) {
+    int slo, shi;
+    tc_tile_steps<H>(d, t, slo, shi);
+    __syncthreads();  // previous tile's readers are done with stg / s_cout / warp_map
+    if (epi) {
 #pragma unroll
-      for (int i = 0; i < 16; i++) v[i] = 0u;
-    }
-    // four limb column sums (< 2^56) and local digits with carry-in 0
-    uint32_t d[4];
-    unsigned long long x = 0ull;
+      for (int j = 0; j < H; j++) {
+        uint32_t v[16];
+        if (slo < shi) {
+          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((t - t0) * G::N + 16 * j), v);
+        } else {
 #pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const unsigned long long sq = (unsigned long long)v[4 * q] + ((unsigned long long)v[4 * q + 1] << 8) +
-                                    ((unsigned long long)v[4 * q + 2] << 16) +
-                                    ((unsigned long long)v[4 * q + 3] << 24);
-      x = (x >> 32) + sq;
-      d[q] = (uint32_t)x;
+          for (int q = 0; q < 16; q++) v[q] = 0u;
+        }
+        unsigned long long* dst = stg + 4 * (m & 7) + 32 * j + 32 * H * (m >> 3);
+#pragma unroll
+        for (int q = 0; q < 4; q++)
+          dst[q] = (unsigned long long)v[4 * q] + ((unsigned long long)v[4 * q + 1] << 8) +
+                   ((unsigned long long)v[4 * q + 2] << 16) + ((unsigned long long)v[4 * q + 3] << 24);
+      }
     }
-    const unsigned long long cout = x >> 32;
-    // carry-in value from the previous thread (tile carry for thread 0)
-    unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
-    __shared__ unsigned long long s_cout[TC_THREADS / 32];
-    if (lane == 31) s_cout[warp] = cout;
     __syncthreads();
-    if (lane == 0) xin = warp ? s_cout[warp - 1] : sh.carry;
-    // overflow map of (D + xin + o) past 2^128, o in {0,1}
-    const bool ones = (d[1] & d[2] & d[3]) == 0xFFFFFFFFu;
-    const unsigned long long s0 = (unsigned long long)d[0] + xin;
-    const uint32_t g = ones && (s0 >> 32) != 0ull;
-    const uint32_t p = ones && ((s0 + 1ull) >> 32) != 0ull;
-    uint32_t F = g | (p << 1);
+    // thread m: limbs [4H m, 4H m + 4H) of the tile, local digits with carry-in 0
+    uint32_t dg[4 * H];
+    unsigned long long cout = 0ull, xin = 0ull;
+    uint32_t ones = 0xFFFFFFFFu;
+    if (epi) {
+      unsigned long long x = 0ull;
 #pragma unroll
-    for (int dd = 1; dd < 32; dd <<= 1) {
-      const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
-      if (lane >= dd) F = cm2(F, y);
+      for (int q = 0; q < 4 * H; q++) {
+        x = (x >> 32) + stg[4 * H * m + q];
+        dg[q] = (uint32_t)x;
+      }
+      cout = x >> 32;
+      xin = __shfl_up_sync(0xffffffffu, cout, 1);
+      if (lane == 31) sh.s_cout[warp] = cout;
+#pragma unroll
+      for (int q = 1; q < 4 * H; q++) ones &= dg[q];
     }
-    if (lane == 31) sh.warp_map[warp] = F;
     __syncthreads();
-    uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
-    uint32_t W = CM2_ID;
-    for (int w = 0; w < warp; w++) W = cm2(sh.warp_map[w], W);
-    E = lane ? cm2(E, W) : W;
-    const uint32_t oin = E & 1u;  // overflow of the previous thread (its o)
-    const uint32_t Fin = cm2(F, W);  // block-inclusive: this thread's own o
-    // final digits: D + xin + oin (mod 2^128)
-    unsigned long long acc = s0 + oin;
-    d[0] = (uint32_t)acc;
+    uint32_t F = 0u;
+    unsigned long long s0 = 0ull;
+    if (epi) {
+      if (lane == 0) xin = warp ? sh.s_cout[warp - 1] : sh.carry;
+      // overflow of (D + xin + o) past 2^(128H), o in {0,1} from the previous thread
+      s0 = (unsigned long long)dg[0] + xin;
+      const bool all1 = ones == 0xFFFFFFFFu;
+      const uint32_t g = all1 && (s0 >> 32) != 0ull;
+      const uint32_t p = all1 && ((s0 + 1ull) >> 32) != 0ull;
+      F = g | (p << 1);
 #pragma unroll
-    for (int q = 1; q < 4; q++) {
-      acc = (acc >> 32) + d[q];
-      d[q] = (uint32_t)acc;
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
+        if (lane >= dd) F = cm2(F, y);
+      }
+      if (lane == 31) sh.warp_map[warp] = F;
     }
-    const int L = t * TC_LIMBS + 4 * tid;
-    if (L + 4 <= mp) {
-      *reinterpret_cast<uint4*>(Pz + L) = make_uint4(d[0], d[1], d[2], d[3]);
-    } else {
+    __syncthreads();
+    if (epi) {
+      uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
+      uint32_t Wm = CM2_ID;
+      for (int w = 0; w < warp; w++) Wm = cm2(sh.warp_map[w], Wm);
+      E = lane ? cm2(E, Wm) : Wm;
+      const uint32_t Fin = cm2(F, Wm);
+      unsigned long long acc = s0 + (E & 1u);
+      dg[0] = (uint32_t)acc;
 #pragma unroll
-      for (int q = 0; q < 4; q++)
-        if (L + q < mp) Pz[L + q] = d[q];
+      for (int q = 1; q < 4 * H; q++) {
+        acc = (acc >> 32) + dg[q];
+        dg[q] = (uint32_t)acc;
+      }
+      const int L = t * G::LIMBS + 4 * H * m;
+      if (L + 4 * H <= mp) {
+#pragma unroll
+        for (int q = 0; q < H; q++)
+          *reinterpret_cast<uint4*>(Pz + L + 4 * q) =
+              make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4 * H; q++)
+          if (L + q < mp) Pz[L + q] = dg[q];
+      }
+      if (tid == TC_EPI - 1) sh.carry = cout + (Fin & 1u);
     }
-    __syncthreads();  // everyone has read sh.carry / s_cout / warp_map
-    if (tid == TC_THREADS - 1) sh.carry = cout + (Fin & 1u);
   }
-  for (int bi = tid; bi < a.nbands; bi += TC_THREADS) {
-    unsigned long long* sp = a.spill + ((long long)z * a.nbands + bi) * 2;
-    sp[0] = 0ull;
-    sp[1] = 0ull;
+  __syncthreads();
+  // band spills: zero inside the range, the range's carry on its top band
+  {
+    const int b0 = 2 * H * t0, b1 = min(a.nbands, 2 * H * t1);
+    for (int bi = b0 + tid; bi < b1; bi += TC_THREADS) {
+      unsigned long long* sp = a.spill + ((long long)z * a.nbands + bi) * 2;
+      sp[0] = bi == 2 * H * t1 - 1 ? sh.carry : 0ull;
+      sp[1] = 0ull;
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0) {
-    uint32_t cols = 32;
-    while (cols < (uint32_t)(ntiles * TC_N)) cols <<= 1;
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
+// ---------------------------------------------------------------- planning
+struct TcPlan {
+  int H, NW, KC, NB, TPC, nranges, ntiles;
+  size_t smem;
+  double cost;  // modelled cycles per product
+};
+
+int env_int_tc(const char* n, int dflt) {
+  const char* v = getenv(n);
+  return v && *v ? atoi(v) : dflt;
+}
+
+int tc_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// Cost model (cycles per product on one SM), calibrated by tools/tc_sweep.py:
+// the SS-mode MMA is paced by its shared-memory operand reads, ~110 B/clk
+// (tools/microbench/tc_peak.cu: M=128 N=16..128 -> 45/46/56/74 cycles), and
+// never faster than the tensor floor 8H cycles per N=16H MMA; the B build
+// costs ~38H cycles per K-step with 3 builder warps and ~17H with 7, shared
+// by the CTA's tiles; a range takes the larger of the two.
+template <int H>
+double tc_cost(const TcDims& d, int TPC, int NW) {
+  const double mma = (4096.0 + 512.0 * H) / 110.0 > 8.0 * H ? (4096.0 + 512.0 * H) / 110.0 : 8.0 * H;
+  const double bld = (NW == 4 ? 38.0 : 17.0) * H;
+  double cost = 0.0;
+  for (int r0 = 0; r0 < d.ntiles; r0 += TPC) {
+    int lo = d.S, hi = 0;
+    long long steps = 0;
+    for (int t = r0; t < min(d.ntiles, r0 + TPC); t++) {
+      int slo, shi;
+      tc_tile_steps<H>(d, t, slo, shi);
+      if (shi > slo) {
+        steps += shi - slo;
+        lo = min(lo, slo);
+        hi = max(hi, shi);
+      }
+    }
+    const double m = (double)steps * mma, b = hi > lo ? (double)(hi - lo) * bld : 0.0;
+    cost += m > b ? m : b;
+  }
+  return cost;
+}
+
+template <int H>
+bool tc_plan_h(int ma, int mb, long long nprod, TcPlan& p) {
+  const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
+  if (4LL * mB > 65536) return false;  // u32 accumulator exactness
+  const TcDims d = tc_dims<H>(mA, mB);
+  int KC = env_int_tc("KMX_TC_KC", 16);
+  if (KC < 4) KC = 4;
+  int NB = env_int_tc("KMX_TC_NB", 2);
+  if (NB < 2) NB = 2;
+  if (NB > TC_MAXNB) NB = TC_MAXNB;
+  if (NB * KC < 8) KC = (8 + NB - 1) / NB;  // epilogue staging needs 4096H bytes
+  const size_t cap = 200 * 1024;
+  while (tc_smem<H>(d.La, d.Lb, KC, NB) > cap && (NB > 2 || KC > 8)) {
+    if (NB > 2) NB--;
+    else KC /= 2;
+  }
+  if (tc_smem<H>(d.La, d.Lb, KC, NB) > cap) return false;
+  int TPC = TC_MAX_COLS / TcG<H>::N;
+  if (TPC > d.ntiles) TPC = d.ntiles;
+  const int tpc_env = env_int_tc("KMX_TC_TPC", 0);
+  if (tpc_env > 0 && tpc_env < TPC) TPC = tpc_env;
+  // enough CTAs to cover the SMs twice over
+  while (TPC > 1 && nprod * ((d.ntiles + TPC - 1) / TPC) < 2LL * tc_num_sms()) TPC--;
+  p.H = H;
+  p.NW = env_int_tc("KMX_TC_NW", TPC <= 2 ? 4 : 8) == 4 ? 4 : 8;
+  if (p.NW == 4 && env_int_tc("KMX_TC_KC", 0) == 0 && H <= 2) KC = 8;
+  p.KC = KC;
+  p.NB = NB;
+  p.TPC = TPC;
+  p.ntiles = d.ntiles;
+  p.nranges = (d.ntiles + TPC - 1) / TPC;
+  p.smem = tc_smem<H>(d.La, d.Lb, KC, NB);
+  p.cost = tc_cost<H>(d, TPC, p.NW);
+  return true;
+}
+
+bool tc_plan(int ma, int mb, long long nprod, TcPlan& best) {
+  const int force = env_int_tc("KMX_TC_H", 0);
+  bool ok = false;
+  TcPlan p;
+#define KMX_TRY_H(HH)                                                   \
+  if ((force == 0 || force == HH) && tc_plan_h<HH>(ma, mb, nprod, p)) { \
+    if (!ok || p.cost < best.cost) best = p;                            \
+    ok = true;                                                          \
+  }
+  KMX_TRY_H(1) KMX_TRY_H(2) KMX_TRY_H(3) KMX_TRY_H(4) KMX_TRY_H(6) KMX_TRY_H(8)
+#undef KMX_TRY_H
+  return ok;
+}
+
+template <int H, int NW>
+cudaError_t launch_hw(const TcArgs& ta, size_t smem, cudaStream_t st) {
+  static size_t s_set = 0;
+  if (smem > 48 * 1024 && smem > s_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_tcmul<H, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    s_set = smem;
+  }
+  const long long grid = (long long)ta.m.nprod * ta.nranges;
+  k_tcmul<H, NW><<<(unsigned)grid, 32 * NW, smem, st>>>(ta);
+  return cudaGetLastError();
+}
+template <int H>
+cudaError_t launch_h(const TcArgs& ta, int nw, size_t smem, cudaStream_t st) {
+  return nw == 4 ? launch_hw<H, 4>(ta, smem, st) : launch_hw<H, 8>(ta, smem, st);
+}
+
+// ---------------------------------------------------------------- peak
+// Dense tcgen05 u8 MMA throughput (M=128, N=256, K=32, SS): one elected
+// thread per CTA issues back-to-back MMAs over 8 resident K-steps into one
+// TMEM accumulator, committing every 32; the roofline denominator for K2.
+__global__ void __launch_bounds__(128) k_tc_peak(int iters, unsigned long long* sink) {
+  extern __shared__ __align__(128) unsigned char pk[];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) unsigned long long bar;
+  constexpr int N = 256, KS = 8;
+  constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+  unsigned char* A = pk;
+  unsigned char* B = pk + KS * 4096;
+  for (int i = threadIdx.x; i < (KS * 4096 + KS * N * 32) / 4; i += 128)
+    reinterpret_cast<uint32_t*>(pk)[i] = (uint32_t)i * 2654435761u;
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tbase)), "r"(256));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tm = tbase;
+  if (threadIdx.x == 0) {
+    for (int it = 0; it < iters; it++) {
+      for (int k = 0; k < 32; k++) {
+        const int s = k % KS;
+        mma_i8(tm, sdesc(smem_u32(A) + 4096 * s, 128, 256), sdesc(smem_u32(B) + N * 32 * s, 128, 256), IDESC,
+               (it | k) ? 1u : 0u);
+      }
+      mma_commit(smem_u32(&bar));
+      mbar_wait(smem_u32(&bar), (uint32_t)(it & 1));
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (threadIdx.x < 32) {
+    uint32_t v[16];
+    tmem_ld16(tm, v);
+    if (v[0] == 0x12345678u && v[1] == 0x9abcdef0u) sink[0] = v[2];
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tm), "r"(256));
   }
 }
 
-cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st) {
-  int la, lb, S, nt;
-  size_t smem;
-  tc_sizes(a.ma, a.mb, &la, &lb, &S, &nt, &smem);
-  if (!tc_supported(a.ma, a.mb)) return cudaErrorNotSupported;
-  if (a.nprod == 0) return cudaSuccess;
-  static size_t s_max_set = 0;
-  if (smem > 48 * 1024 && smem > s_max_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_tcmul, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    s_max_set = smem;
+}  // namespace
+
+double measure_tc_peak(int iters) {
+  const size_t smem = 8 * 4096 + 8 * 256 * 32;
+  if (cudaFuncSetAttribute(k_tc_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return -1.0;
+  unsigned long long* sink = nullptr;
+  if (cudaMalloc(&sink, 8) != cudaSuccess) return -1.0;
+  const int grid = tc_num_sms();
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k_tc_peak<<<grid, 128, smem>>>(8, sink);
+  float best = 1e30f;
+  for (int rep = 0; rep < 3; rep++) {
+    cudaEventRecord(e0);
+    k_tc_peak<<<grid, 128, smem>>>(iters, sink);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best) best = ms;
   }
-  k_tcmul<<<a.nprod, TC_THREADS, smem, st>>>(a);
-  g_launches++;
-  return cudaGetLastError();
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(sink);
+  if (cudaGetLastError() != cudaSuccess) return -1.0;
+  return (double)grid * iters * 32 * 128.0 * 256 * 32 / (best * 1e-3);
+}
+
+namespace {
+}  // namespace
+
+bool tc_supported(int ma, int mb) {
+  TcPlan p;
+  return tc_plan(ma, mb, 1 << 20, p);
+}
+
+cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st) {
+  TcPlan p;
+  if (!tc_plan(a.ma, a.mb, a.nprod, p)) return cudaErrorNotSupported;
+  if (a.nprod == 0) return cudaSuccess;
+  if (env_int_tc("KMX_TC_VERBOSE", 0))
+    fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d smem=%zu cost=%.0f\n",
+            a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.smem, p.cost);
+  TcArgs ta;
+  ta.m = a;
+  ta.KC = p.KC;
+  ta.NB = p.NB;
+  ta.TPC = p.TPC;
+  ta.nranges = p.nranges;
+  cudaError_t e;
+  switch (p.H) {
+    case 1: e = launch_h<1>(ta, p.NW, p.smem, st); break;
+    case 2: e = launch_h<2>(ta, p.NW, p.smem, st); break;
+    case 3: e = launch_h<3>(ta, p.NW, p.smem, st); break;
+    case 4: e = launch_h<4>(ta, p.NW, p.smem, st); break;
+    case 6: e = launch_h<6>(ta, p.NW, p.smem, st); break;
+    default: e = launch_h<8>(ta, p.NW, p.smem, st); break;
+  }
+  return e;
 }
 
 }  // namespace kmx
