@@ -2,7 +2,9 @@
 """Benchmark of the multipoint Kronecker-substitution hot path on B200.
 
 Metric (BASELINE.json): polynomial products per second per KS variant, with
-the fraction of the measured IMAD.WIDE.U32 peak for the multiply kernel.
+the multiply kernel's fraction of its measured peak: the dense tcgen05 u8 MMA
+rate when it runs on the tensor cores (kmx_tc.cu), the IMAD.WIDE.U32 rate
+when it runs on the integer pipe (kmx_mul.cu).
 Default workload = BASELINE config 2 (configs[1]): Z[x], signed int32
 coefficients, batch 1024 pairs, n = 1024.  A step = one pass of the hot path
 (pack -> multiply -> finish [-> reconstruct] -> bias) over the whole batch.
@@ -30,7 +32,7 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-METRIC = "poly products/sec per KS variant; fraction of IMAD peak and HBM roofline"
+METRIC = "poly products/sec per KS variant; fraction of the tensor (or IMAD) peak and HBM roofline"
 VNAME = {1: "ks1", 2: "ks2", 3: "ks3", 4: "ks4"}
 VDESC = {1: "standard 2^N", 2: "reciprocal 2^N,2^-N", 3: "negated +-2^N", 4: "four-point +-2^N,+-2^-N"}
 CONFIGS = {
@@ -221,6 +223,7 @@ def run_ours(args, cfg, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     L = _lib.lib()
     peak = kmx.imad_peak(4096)  # live IMAD.WIDE.U32 microbenchmark, same process and clocks
+    tpeak = kmx.tc_peak(2000)   # live dense tcgen05 u8 MMA microbenchmark (MAC/s)
 
     variants = [args.variant] + [v for v in (1, 2, 3, 4) if v != args.variant] if args.all_variants else [args.variant]
     per_variant = {}
@@ -299,11 +302,16 @@ def run_ours(args, cfg, rank, world, local_rank):
             mul_ms = kern[1] / args.steps
             rec["mul_limb_products_per_s"] = prods / (mul_ms * 1e-3) if mul_ms > 0 else None
             rec["mul_frac_of_imad_peak"] = rec["mul_limb_products_per_s"] / peak if mul_ms > 0 else None
+            rec["mul_engine"] = kmx.mul_engine(v, cfg["n"], cfg["n"], cfg["b"], signed=signed)
+            if rec["mul_engine"] == "tensor" and mul_ms > 0:
+                # algorithmic byte MACs of the u8 convolution: 16 per 32x32 limb product
+                rec["mul_frac_of_tensor_peak"] = 16.0 * rec["mul_limb_products_per_s"] / tpeak
         per_variant[VNAME[v]] = rec
         if vi == 0:
             headline = (v, rec, op, fd, gd, out, launches)
         del op
     v, rec, op, fd, gd, out, launches = headline
+    peaks = {"imad": peak, "tensor": tpeak}
 
     # ---- end to end through the public host API (pinned host buffers)
     e2e = None
@@ -355,7 +363,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             want = O.bks(v, fh[0].tolist(), gh[0].tolist())
             check = out[0].cpu().tolist() == want
 
-    result = dict(rec=rec, per_variant=per_variant, e2e=e2e, peak=peak, clocks=clocks, variant=v,
+    result = dict(rec=rec, per_variant=per_variant, e2e=e2e, peak=peak, tpeak=tpeak, clocks=clocks, variant=v,
                   launches=launches, check=check)
     if dist is not None:
         dist.destroy_process_group()
@@ -474,11 +482,11 @@ def config_json(cfg, v):
     return c
 
 
-def load_traffic(config_name, variant):
+def load_traffic(config_name, variant, key="mul_dram_bytes"):
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         d = json.load(open(path))
-        return d[config_name][VNAME[variant]]["mul_dram_bytes"]
+        return d[config_name][VNAME[variant]][key]
     except Exception:
         return None
 
@@ -522,13 +530,27 @@ def main():
         mul_ms = rec["kernel_ms"].get("mul")
         prods = algorithmic_products(cfg, v) * cfg["batch"]
         ach = prods / (mul_ms * 1e-3) / 1e9
-        line["roofline"] = {"bound": "imad", "kernel": "k_mul (IMAD.WIDE.U32 schoolbook)",
-                            "achieved": ach, "peak": r["peak"] / 1e9, "unit": "G limb-products/s",
-                            "frac": ach * 1e9 / r["peak"],
-                            "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
-                            "algorithmic_work": f"{prods} 32x32->64 limb products per launch "
-                                                f"({algorithmic_products(cfg, v)} per pair x {cfg['batch']})",
-                            "traffic": load_traffic(args.config, v)}
+        imad_view = {"bound": "imad", "kernel": "k_mul (IMAD.WIDE.U32 schoolbook)",
+                     "achieved": ach, "peak": r["peak"] / 1e9, "unit": "G limb-products/s",
+                     "frac": ach * 1e9 / r["peak"],
+                     "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
+                     "algorithmic_work": f"{prods} 32x32->64 limb products per launch "
+                                         f"({algorithmic_products(cfg, v)} per pair x {cfg['batch']})"}
+        if rec.get("mul_engine") == "tensor":
+            tops = 2.0 * 16.0 * prods / (mul_ms * 1e-3) / 1e12
+            tpk = 2.0 * r["tpeak"] / 1e12
+            line["roofline"] = {
+                "bound": "tensor", "kernel": "k_tcmul (tcgen05.mma kind::i8 byte convolution, TMEM s32)",
+                "achieved": tops, "peak": tpk, "unit": "TOPS (int8, 2 ops per MAC)", "frac": tops / tpk,
+                "peak_source": "kmx_tc_peak() live: dense tcgen05 u8 MMA M=128 N=256 K=32 from smem, all SMs",
+                "algorithmic_work": f"{16 * prods} byte MACs per launch (16 per 32x32 limb product; "
+                                    f"{algorithmic_products(cfg, v)} limb products per pair x {cfg['batch']})",
+                "traffic": load_traffic(args.config, v, "tcmul_dram_bytes"),
+                "same_kernel_in_imad_units": {"achieved": ach, "unit": "G limb-products/s",
+                                              "frac_of_imad_peak": ach * 1e9 / r["peak"]}}
+        else:
+            imad_view["traffic"] = load_traffic(args.config, v)
+            line["roofline"] = imad_view
         pu = pack_unpack_bytes(cfg, v)
         try:
             peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -538,10 +560,13 @@ def main():
             hbm, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
         km = rec["kernel_ms"]
         line["roofline_hbm"] = {"bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
-                                "pack": {"achieved": pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9,
-                                         "frac": pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9 / hbm},
                                 "finish": {"achieved": pu["finish_bytes"] / (km["finish"] * 1e-3) / 1e9,
                                            "frac": pu["finish_bytes"] / (km["finish"] * 1e-3) / 1e9 / hbm}}
+        if "pack" in km:
+            line["roofline_hbm"]["pack"] = {"achieved": pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9,
+                                            "frac": pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9 / hbm}
+        else:
+            line["roofline_hbm"]["pack"] = "fused into the tensor-core multiply (operands packed in shared memory)"
     else:
         line["roofline"] = {"bound": "imad", "kernel": "k_conv", "achieved": None, "peak": r["peak"] / 1e9,
                             "unit": "G MAC/s", "frac": None, "traffic": None}

@@ -263,10 +263,23 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     bfix.pf = scr; bfix.pair_stride = p.lf + p.lg + 2;
     bfix.lf = p.lf; bfix.lg = p.lg; bfix.b = p.b; bfix.enabled = 1; bfix.lgpad = -1;
   }
-  prof_begin(0, st);
-  if ((e = launch_pack(pa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
-  prof_end(0, st);
-  g_launches++;
+  // K2 engine; with the tensor cores K1 can be fused into K2's prologue when
+  // the coefficient vectors can be staged in shared memory (KMX_FUSE=1).  Off
+  // by default: with one-shot CTAs the pack latency is exposed in front of
+  // the MMAs (c2 ks4: 0.27 ms fused vs 0.08 + 0.12 ms separate).
+  const bool tc = use_tensor_mul(p.mf, p.mg);
+  int lmax = p.lf > p.lg ? p.lf : p.lg;
+  const size_t stage = (size_t)(lmax + PK_PAD_WORDS) * p.in_words * 4;
+  const char* fz = getenv("KMX_FUSE");
+  const bool fuse = tc && (fz && *fz && atoi(fz) == 1) &&
+                    (size_t)(lmax + PK_PAD_WORDS) * p.in_words <= (size_t)PK_STAGE_LIMIT_WORDS &&
+                    tc_supported(p.mf, p.mg, stage);
+  if (!fuse) {
+    prof_begin(0, st);
+    if ((e = launch_pack(pa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+    prof_end(0, st);
+    g_launches++;
+  }
 
   MulArgs ma;
   ma.A = opf; ma.a_stride = p.mfs; ma.ma = p.mf;
@@ -275,8 +288,8 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
   ma.counter = (int*)(err + 1);
   prof_begin(1, st);
-  if (use_tensor_mul(p.mf, p.mg)) {
-    if ((e = launch_tcmul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  if (tc) {
+    if ((e = launch_tcmul(ma, st, fuse ? &pa : nullptr, p.P)) != cudaSuccess) return KMX_ECUDA;
   } else {
     if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
   }

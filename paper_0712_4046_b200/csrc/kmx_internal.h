@@ -56,9 +56,15 @@ struct ConvArgs {
   int* counter;                                   // work-unit counter, zeroed before launch
 };
 void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr);
+// K1 staging limits (kmx_pack.cuh PK_PAD / PK_STAGE_WORDS), visible to the host
+constexpr int PK_PAD_WORDS = 64;
+constexpr int PK_STAGE_LIMIT_WORDS = 12288;
 // K2 on tcgen05 (kmx_tc.cu): same MulArgs contract, zero band spills.
-bool tc_supported(int ma, int mb);
-cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st);
+bool tc_supported(int ma, int mb, size_t stage_bytes = 0);
+// pk != nullptr: fused pack -- each product's CTA packs its two operands
+// (pack ops s and P + s of its pair) straight into shared memory; the packed
+// operands never reach global memory (MulArgs A/B unused).
+cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk = nullptr, int P = 1);
 double measure_tc_peak(int iters);
 
 // Signed inputs (bias lift): the coefficient writers apply

@@ -1,0 +1,337 @@
+// kmx_pack.cuh -- K1, the pack of one operand (pack.py:55-110), shared by the
+// standalone pack kernel (kmx_ks.cu, operands to global memory for the
+// integer-pipe multiply) and the tensor-core multiply (kmx_tc.cu), which
+// packs its two operands straight into shared memory.
+#pragma once
+
+#include "kmx_common.cuh"
+#include "kmx_internal.h"
+
+namespace kmx {
+
+// ========================================================================
+// K1: pack.  One block per (pair, operand) (or per product when fused).  The packed value is
+// V = sum_i s_i d_i 2^(iN) (d_i = c_i, or c_(L-1-i) for the reversed packs;
+// s_i = (-1)^i for the negated packs, times -1 for pack_negated_reversed at
+// even L, pack.py:62-110).  Because 2N >= b (pack.py:55-59) the even- and
+// odd-position coefficients each form a clean bitstream E, O, so digit q of
+// V is e_q + o_q (positive packs, carries in {0,1}) or |e_q - o_q| with the
+// larger stream first (negated packs; the order is decided up front by a
+// top-down warp compare of E and O, so the magnitude is produced in one pass
+// -- sign-magnitude as SignedBig, bignat.py:218-277).  Each thread owns
+// PK_V consecutive digits and walks the coefficient windows incrementally;
+// carries are resolved with one block scan of carry maps per chunk.
+// ========================================================================
+static __device__ void block_prefix_u64(const u32* x, int n, u32 bias, u32 bmask, unsigned long long* out) {
+  // out[0] = 0, out[i+1] = sum_{k<=i} ((x[k] + bias) & bmask)
+  __shared__ unsigned long long wsum[8];
+  __shared__ unsigned long long run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { run = 0; out[0] = 0; }
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int i = i0 + tid;
+    unsigned long long v = i < n ? (unsigned long long)((x[i] + bias) & bmask) : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += o;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    unsigned long long pre = run;
+    for (int k = 0; k < warp; k++) pre += wsum[k];
+    if (i < n) out[i + 1] = pre + v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) run = pre + v;
+    __syncthreads();
+  }
+}
+
+// Prefix sums of n staged values in natural order (x[i] at x[rev ? n-1-i : i]):
+// out[0] = 0, out[i+1] = sum_{k<=i} x[k].  Each thread owns a contiguous
+// segment; one block scan of the segment sums.
+static __device__ void block_prefix_staged(const u32* x, int n, bool rev, unsigned long long* out) {
+  __shared__ unsigned long long wsum[32];
+  const int T = blockDim.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int seg = (n + T - 1) / T;
+  const int a = min(n, tid * seg), e = min(n, a + seg);
+  unsigned long long s = 0ull;
+  for (int i = a; i < e; i++) s += x[rev ? n - 1 - i : i];
+  unsigned long long v = s;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const unsigned long long o = __shfl_up_sync(0xffffffffu, v, off);
+    if (lane >= off) v += o;
+  }
+  if (lane == 31) wsum[warp] = v;
+  __syncthreads();
+  unsigned long long run = v - s;
+  for (int k = 0; k < warp; k++) run += wsum[k];
+  if (tid == 0) out[0] = 0ull;
+  for (int i = a; i < e; i++) {
+    run += x[rev ? n - 1 - i : i];
+    out[i + 1] = run;
+  }
+  __syncthreads();
+}
+
+constexpr int PK_T = 256;
+constexpr int PK_V = 8;
+
+template <bool STAGED>
+struct PackCtx {
+  const u32* cf;
+  const u32* sc;   // staged coefficients in position order (reversal and bias applied)
+  int L, N, b, iw;
+  bool rev, bias;
+  u32 biasw, bmask;
+  __device__ __forceinline__ u32 word(int i, int w) const {  // word w of the coefficient at position i
+    if (STAGED) return w < iw ? sc[i * iw + w] : 0u;  // zero-padded past L (staged)
+    return gword(i, w);
+  }
+  __device__ __forceinline__ u32 gword(int i, int w) const {  // unstaged (very long vectors)
+    if (i >= L || w >= iw) return 0u;
+    const int ci = rev ? (L - 1 - i) : i;
+    u32 x = __ldg(cf + (long long)ci * iw + w);
+    if (bias) x = (x + biasw) & bmask;  // signed inputs: lift by 2^(b-1) (iw == 1)
+    return x;
+  }
+};
+constexpr int PK_STAGE_WORDS = 12288;  // stage coefficient vectors up to 48 KB
+constexpr int PK_PAD = 64;             // zero positions past L (window reads beyond the top)
+
+// Cursor over one parity stream: coefficients at positions i = 2m + par start
+// at bit off + m*S (S = 2N >= b, so they never overlap inside a stream).
+// Invariant for the current digit q: m = the last coefficient starting at or
+// below bit 32q (m may be -1), t = 32q - start(m).
+struct StreamCur {
+  int m, t;
+  __device__ __forceinline__ void init(int q, int off, int S) {
+    const int x = 32 * q - off;
+    m = x >= 0 ? x / S : -((-x + S - 1) / S);
+    t = x - m * S;
+  }
+  __device__ __forceinline__ void next(int S) {
+    t += 32;
+    while (t >= S) { t -= S; m++; }
+  }
+  // the 32 bits of this stream in the current digit window
+  template <class Ctx>
+  __device__ __forceinline__ u32 bits(const Ctx& C, int par, int S) const {
+    u32 v = 0u;
+    if (m >= 0 && t < C.b) {
+      const int wq = t >> 5, sb = t & 31;
+      const int i = 2 * m + par;
+      const u32 lo = C.word(i, wq);
+      v = sb ? ((lo >> sb) | (C.word(i, wq + 1) << (32 - sb))) : lo;
+    }
+    for (int k = 1, sh = S - t; sh < 32; k++, sh += S) {  // coefficients starting inside the window
+      if (m + k >= 0) v |= C.word(2 * (m + k) + par, 0) << sh;
+    }
+    return v;
+  }
+};
+
+// One packed operand (pack op o of pair `pair`) into `out` (global or shared
+// memory), its [sign, bitlen] meta, and -- on the ops that carry them -- the
+// range check and the signed prefix sums.  Called by every thread of the
+// block (block-wide barriers); pk_sc: (len + PK_PAD) * in_words words of
+// shared memory for the staged vector.  out == nullptr: the op's own
+// global operand slot.  side_effects = false skips the meta, prefix and range
+// check writes (another block of the same product does them).
+template <bool STAGED>
+__device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32* pk_sc, u32* out_override,
+                                        bool side_effects = true) {
+  __shared__ u32 sm_scan[PK_T / 32];
+  __shared__ int sm_order, sm_bad;
+  __shared__ unsigned long long sm_top;  // (top nonzero digit index + 1) << 32 | its value
+  const int T = blockDim.x;  // 32..PK_T, sized to the operand
+  __shared__ i64 sm_carry;
+  const int tid = threadIdx.x;
+  PackCtx<STAGED> C;
+  C.cf = A.op[o].coeffs + (long long)pair * A.op[o].coeff_pair_stride;
+  u32* out = out_override ? out_override : A.op[o].out + (long long)pair * A.op[o].out_pair_stride;
+  u32* meta = A.op[o].meta + (long long)pair * A.op[o].meta_pair_stride;
+  const int kind = A.op[o].kind, m = A.op[o].m;
+  C.L = A.op[o].len; C.N = A.N; C.b = A.b; C.iw = A.in_words;
+  C.rev = (kind & 2) != 0;
+  C.bias = A.bias != 0;
+  C.bmask = C.b >= 32 ? 0xffffffffu : ((1u << C.b) - 1u);
+  C.biasw = A.bias ? (1u << (C.b - 1)) : 0u;
+  const bool neg = kind & 1;
+  const bool flip = (kind == 3) && ((C.L & 1) == 0);  // pack.py:106-109
+  const bool validate = side_effects && A.op[o].validate != 0;
+  unsigned long long* prefix = side_effects ? A.op[o].prefix : nullptr;
+  C.sc = pk_sc;
+  if (tid == 0) sm_bad = 0;
+  if (STAGED) {
+    // stage the vector in position order with zero padding: every load of
+    // the CTA in flight at once, the range check (pack.py:36-46) on the raw
+    // words, then the bias lift and the reversal
+    const int L = C.L, iw = C.iw, nw = L * iw;
+    __syncthreads();
+    bool bad = false;
+    auto put = [&](int x, u32 raw) {
+      const int i = iw == 1 ? x : x / iw, w = iw == 1 ? 0 : x - i * iw;
+      if (validate) {
+        if (C.bias) {
+          const int v = (int)raw;
+          if (C.b < 32) bad |= (v < -(1 << (C.b - 1))) || (v >= (1 << (C.b - 1)));
+        } else {
+          const int lo_bit = 32 * w;
+          if (lo_bit >= C.b) bad |= raw != 0u;
+          else if (C.b - lo_bit < 32) bad |= (raw >> (C.b - lo_bit)) != 0u;
+        }
+      }
+      const u32 v = C.bias ? ((raw + C.biasw) & C.bmask) : raw;
+      const int p = C.rev ? L - 1 - i : i;
+      pk_sc[p * iw + w] = v;
+    };
+    if ((nw & 3) == 0 && (reinterpret_cast<uintptr_t>(C.cf) & 15) == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(C.cf);
+#pragma unroll 4
+      for (int x4 = tid; x4 < nw / 4; x4 += T) {
+        const uint4 r = __ldg(s4 + x4);
+        put(4 * x4, r.x);
+        put(4 * x4 + 1, r.y);
+        put(4 * x4 + 2, r.z);
+        put(4 * x4 + 3, r.w);
+      }
+    } else {
+#pragma unroll 4
+      for (int x = tid; x < nw; x += T) put(x, __ldg(C.cf + x));
+    }
+    for (int x = nw + tid; x < (L + PK_PAD) * iw; x += T) pk_sc[x] = 0u;
+    if (bad) sm_bad = 1;
+    __syncthreads();
+    if (tid == 0 && sm_bad) raise_err(A.err, ERR_INVAL);
+    if (prefix)  // signed path: prefix sums of the lifted coefficients (iw == 1)
+      block_prefix_staged(pk_sc, L, C.rev, prefix + (long long)pair * A.op[o].prefix_pair_stride);
+  } else {
+    if (validate) {  // CoeffVec invariant 0 <= c < 2^b (pack.py:36-46)
+      for (int i = tid; i < C.L; i += T) {
+        const u32* c = C.cf + (long long)i * C.iw;
+        bool bad = false;
+        if (A.bias) {
+          const int v = (int)c[0];
+          if (C.b < 32) bad = (v < -(1 << (C.b - 1))) || (v >= (1 << (C.b - 1)));
+        } else {
+          for (int w = 0; w < C.iw; w++) {
+            const int lo_bit = 32 * w;
+            if (lo_bit >= C.b) bad |= c[w] != 0u;
+            else if (C.b - lo_bit < 32) bad |= (c[w] >> (C.b - lo_bit)) != 0u;
+          }
+        }
+        if (bad) raise_err(A.err, ERR_INVAL);
+      }
+    }
+    if (prefix) {  // signed path: prefix sums of the lifted coefficients
+      block_prefix_u64(C.cf, C.L, C.biasw, C.bmask, prefix + (long long)pair * A.op[o].prefix_pair_stride);
+      __syncthreads();
+    }
+  }
+  if (tid == 0) { sm_top = 0ull; sm_order = 1; sm_carry = 0; }
+  const int S = 2 * C.N;
+  // negated packs: order of E and O from the most significant differing digit
+  if (neg && tid < 32) {
+    int order = 0;  // +1: E > O, -1: E < O, 0: equal
+    for (int base = m - 1; base >= 0 && order == 0; base -= 32) {
+      const int q = base - tid;
+      u32 e = 0u, ov = 0u;
+      if (q >= 0) {
+        StreamCur ce, co;
+        ce.init(q, 0, S);
+        co.init(q, C.N, S);
+        e = ce.bits(C, 0, S);
+        ov = co.bits(C, 1, S);
+      }
+      const unsigned diff = __ballot_sync(0xffffffffu, e != ov);
+      if (diff) {
+        const int l = __ffs(diff) - 1;  // lowest lane = highest digit
+        const int gt = __shfl_sync(0xffffffffu, e > ov ? 1 : 0, l);
+        order = gt ? 1 : -1;
+      }
+    }
+    if (tid == 0) sm_order = order >= 0 ? 1 : -1;
+  }
+  __syncthreads();
+  const int order = sm_order;  // E - O (order 1) or O - E (order -1)
+  const int negative = neg ? ((order < 0) != flip ? 1 : 0) : 0;
+
+  int my_top = 0;
+  u32 my_topv = 0u;
+  if (!neg && C.N >= C.b) {
+    // disjoint bit fields (pack.py:66-67): V = E | O, no carries at all --
+    // a pure gather, every thread independent
+    for (int q0 = tid * PK_V; q0 < m; q0 += T * PK_V) {
+      StreamCur ce, co;
+      ce.init(q0, 0, S);
+      co.init(q0, C.N, S);
+#pragma unroll 1
+      for (int v = 0; v < PK_V && q0 + v < m; v++) {
+        const u32 d = ce.bits(C, 0, S) | co.bits(C, 1, S);
+        ce.next(S);
+        co.next(S);
+        out[q0 + v] = d;
+        if (d) { my_top = q0 + v + 1; my_topv = d; }
+      }
+    }
+  } else
+  for (int c0 = 0; c0 < m; c0 += T * PK_V) {
+    const int q0 = c0 + tid * PK_V;
+    StreamCur ce, co;
+    ce.init(q0, 0, S);
+    co.init(q0, C.N, S);
+    i64 t[PK_V];
+    u32 M = CM_IDENT, mr[PK_V];
+#pragma unroll
+    for (int v = 0; v < PK_V; v++) {
+      const int q = q0 + v;
+      u32 e = 0u, ov = 0u;
+      if (q < m) {
+        e = ce.bits(C, 0, S);
+        ov = co.bits(C, 1, S);
+      }
+      ce.next(S);
+      co.next(S);
+      t[v] = !neg ? (i64)e + ov : (order > 0 ? (i64)e - ov : (i64)ov - e);
+      mr[v] = cm_make(t[v]);
+      M = cm_compose(M, mr[v]);
+    }
+    u32 tot;
+    const u32 exc = cm_seg_scan(M, T, sm_scan, &tot);
+    const int cin = (int)sm_carry;
+    int c = cm_apply(exc, cin);
+    u32 d[PK_V];
+#pragma unroll
+    for (int v = 0; v < PK_V; v++) {
+      d[v] = (u32)(t[v] + c);
+      c = cm_apply(mr[v], c);
+      if (q0 + v < m && d[v]) { my_top = q0 + v + 1; my_topv = d[v]; }
+    }
+    if (q0 + PK_V <= m) {
+      uint4* dst = reinterpret_cast<uint4*>(out + q0);
+      dst[0] = make_uint4(d[0], d[1], d[2], d[3]);
+      dst[1] = make_uint4(d[4], d[5], d[6], d[7]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++)
+        if (q0 + v < m) out[q0 + v] = d[v];
+    }
+    __syncthreads();
+    if (tid == 0) sm_carry = cm_apply(tot, cin);
+    __syncthreads();
+  }
+  if (tid == 0 && sm_carry != 0) raise_err(A.err, ERR_INEXACT);  // operand overflow (cannot happen)
+  if (my_top) atomicMax(&sm_top, ((unsigned long long)my_top << 32) | my_topv);
+  __syncthreads();
+  if (tid == 0 && side_effects) {
+    const int top = (int)(sm_top >> 32);
+    meta[0] = (u32)negative;
+    meta[1] = top ? (u32)(32 * (top - 1) + 32 - __clz((u32)sm_top)) : 0u;
+  }
+}
+
+
+}  // namespace kmx

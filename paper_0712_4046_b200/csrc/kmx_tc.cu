@@ -43,6 +43,7 @@
 
 #include "kmx_internal.h"
 #include "kmx_common.cuh"
+#include "kmx_pack.cuh"
 
 namespace kmx {
 
@@ -166,6 +167,10 @@ struct TcArgs {
   int NB;       // B stages in the ring (2..TC_MAXNB)
   int TPC;      // tiles per CTA
   int nranges;  // CTAs per product = ceil(ntiles / TPC)
+  int fuse;     // pack the operands in the prologue (pk, P)
+  int P;        // products per pair
+  size_t ring;  // bytes of the B ring (>= the pack staging area when fused)
+  PackArgs pk;
 };
 
 __host__ __device__ inline size_t round128(size_t x) { return (x + 127) & ~(size_t)127; }
@@ -178,9 +183,14 @@ struct TcB {
 };
 
 template <int H>
-__host__ __device__ inline size_t tc_smem(int La, int Lb, int KC, int NB) {
+__host__ __device__ inline size_t tc_ring(int KC, int NB, size_t stage) {
+  const size_t r = (size_t)NB * KC * TcG<H>::STEPB;
+  return r > stage ? r : round128(stage);
+}
+template <int H>
+__host__ __device__ inline size_t tc_smem(int La, int Lb, int KC, int NB, size_t stage) {
   return round128(sizeof(TcShared)) + round128((size_t)La + 2 * TcG<H>::APAD) +
-         round128((size_t)Lb + 2 * TcB<H>::BPAD) + (size_t)NB * KC * TcG<H>::STEPB;
+         round128((size_t)Lb + 2 * TcB<H>::BPAD) + tc_ring<H>(KC, NB, stage);
 }
 
 __device__ __forceinline__ void mbar_arrive(uint32_t mbar) {
@@ -247,8 +257,29 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     sh.carry = 0ull;
   }
-  // A: zero-padded copy of the longer operand; b: zero-padded copy of the shorter
-  {
+  if (ta.fuse) {
+    // fused K1: pack this product's two operands (pack ops s and P + s of the
+    // pair) straight into the padded A and b buffers; the B ring stages the
+    // coefficient vector meanwhile
+    uint32_t* aw = reinterpret_cast<uint32_t*>(apad);
+    uint32_t* bw = reinterpret_cast<uint32_t*>(bpad);
+    constexpr int AP = G::APAD / 4, BP = TcB<H>::BPAD / 4;
+    for (int w = tid; w < AP; w += TC_THREADS) {
+      aw[w] = 0u;
+      aw[AP + mA + w] = 0u;
+    }
+    for (int w = tid; w < BP; w += TC_THREADS) {
+      bw[w] = 0u;
+      bw[BP + mB + w] = 0u;
+    }
+    const int pair = z / ta.P, s = z - pair * ta.P;
+    const int oa = sw ? ta.P + s : s, ob = sw ? s : ta.P + s;
+    uint32_t* stage = reinterpret_cast<uint32_t*>(bring);
+    pack_op<true>(ta.pk, pair, oa, stage, aw + AP, rg == 0);
+    pack_op<true>(ta.pk, pair, ob, stage, bw + BP, rg == 0);
+    __syncthreads();  // the ring is free again before the builders use it
+  } else {
+    // A: zero-padded copy of the longer operand; b: zero-padded copy of the shorter
     uint4* aw = reinterpret_cast<uint4*>(apad);
     const int nq = (d.La + 2 * G::APAD) / 16;
     const int qa = G::APAD / 16;
@@ -524,7 +555,7 @@ double tc_cost(const TcDims& d, int TPC, int NW) {
 }
 
 template <int H>
-bool tc_plan_h(int ma, int mb, long long nprod, TcPlan& p) {
+bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
   if (4LL * mB > 65536) return false;  // u32 accumulator exactness
   const TcDims d = tc_dims<H>(mA, mB);
@@ -535,11 +566,11 @@ bool tc_plan_h(int ma, int mb, long long nprod, TcPlan& p) {
   if (NB > TC_MAXNB) NB = TC_MAXNB;
   if (NB * KC < 8) KC = (8 + NB - 1) / NB;  // epilogue staging needs 4096H bytes
   const size_t cap = 200 * 1024;
-  while (tc_smem<H>(d.La, d.Lb, KC, NB) > cap && (NB > 2 || KC > 8)) {
+  while (tc_smem<H>(d.La, d.Lb, KC, NB, stage) > cap && (NB > 2 || KC > 8)) {
     if (NB > 2) NB--;
     else KC /= 2;
   }
-  if (tc_smem<H>(d.La, d.Lb, KC, NB) > cap) return false;
+  if (tc_smem<H>(d.La, d.Lb, KC, NB, stage) > cap) return false;
   int TPC = TC_MAX_COLS / TcG<H>::N;
   if (TPC > d.ntiles) TPC = d.ntiles;
   const int tpc_env = env_int_tc("KMX_TC_TPC", 0);
@@ -554,17 +585,17 @@ bool tc_plan_h(int ma, int mb, long long nprod, TcPlan& p) {
   p.TPC = TPC;
   p.ntiles = d.ntiles;
   p.nranges = (d.ntiles + TPC - 1) / TPC;
-  p.smem = tc_smem<H>(d.La, d.Lb, KC, NB);
+  p.smem = tc_smem<H>(d.La, d.Lb, KC, NB, stage);
   p.cost = tc_cost<H>(d, TPC, p.NW);
   return true;
 }
 
-bool tc_plan(int ma, int mb, long long nprod, TcPlan& best) {
+bool tc_plan(int ma, int mb, long long nprod, size_t stage, TcPlan& best) {
   const int force = env_int_tc("KMX_TC_H", 0);
   bool ok = false;
   TcPlan p;
 #define KMX_TRY_H(HH)                                                   \
-  if ((force == 0 || force == HH) && tc_plan_h<HH>(ma, mb, nprod, p)) { \
+  if ((force == 0 || force == HH) && tc_plan_h<HH>(ma, mb, nprod, stage, p)) { \
     if (!ok || p.cost < best.cost) best = p;                            \
     ok = true;                                                          \
   }
@@ -576,7 +607,7 @@ bool tc_plan(int ma, int mb, long long nprod, TcPlan& best) {
 template <int H, int NW>
 cudaError_t launch_hw(const TcArgs& ta, size_t smem, cudaStream_t st) {
   static size_t s_set = 0;
-  if (smem > 48 * 1024 && smem > s_set) {
+  if (smem > 32 * 1024 && smem > s_set) {  // + static shared memory (fused pack) past 48 KB
     cudaError_t e = cudaFuncSetAttribute(k_tcmul<H, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     s_set = smem;
@@ -672,14 +703,20 @@ double measure_tc_peak(int iters) {
 namespace {
 }  // namespace
 
-bool tc_supported(int ma, int mb) {
+bool tc_supported(int ma, int mb, size_t stage_bytes) {
   TcPlan p;
-  return tc_plan(ma, mb, 1 << 20, p);
+  return tc_plan(ma, mb, 1 << 20, stage_bytes, p);
 }
 
-cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st) {
+cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, int P) {
   TcPlan p;
-  if (!tc_plan(a.ma, a.mb, a.nprod, p)) return cudaErrorNotSupported;
+  size_t stage = 0;
+  if (pk) {
+    int lmax = 0;
+    for (int i = 0; i < pk->nops; i++) lmax = pk->op[i].len > lmax ? pk->op[i].len : lmax;
+    stage = (size_t)(lmax + PK_PAD) * pk->in_words * 4;
+  }
+  if (!tc_plan(a.ma, a.mb, a.nprod, stage, p)) return cudaErrorNotSupported;
   if (a.nprod == 0) return cudaSuccess;
   if (env_int_tc("KMX_TC_VERBOSE", 0))
     fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d smem=%zu cost=%.0f\n",
@@ -688,6 +725,13 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st) {
   ta.m = a;
   ta.KC = p.KC;
   ta.NB = p.NB;
+  ta.fuse = pk != nullptr;
+  ta.P = P;
+  ta.ring = 0;
+  if (pk) {
+    ta.pk = *pk;
+    ta.pk.stage = 1;
+  }
   ta.TPC = p.TPC;
   ta.nranges = p.nranges;
   cudaError_t e;

@@ -18,7 +18,7 @@ from tests.test_gpu_parity import _check_batch, _dev_words, _host_ints  # noqa: 
 
 pytestmark = pytest.mark.gpu
 
-_KEYS = ("KMX_TC", "KMX_TC_H", "KMX_TC_TPC", "KMX_TC_KC")
+_KEYS = ("KMX_TC", "KMX_TC_H", "KMX_TC_TPC", "KMX_TC_KC", "KMX_FUSE")
 
 
 @pytest.fixture(scope="module")
@@ -119,3 +119,24 @@ def test_all_ones_accumulators_past_2_31(kmx, env):
 def test_tc_peak_is_measured(kmx):
     peak = kmx.tc_peak(200)
     assert 1e14 < peak < 5e15
+
+
+@pytest.mark.parametrize("variant", [1, 2, 3, 4])
+def test_fused_pack_multiply(kmx, env, variant):
+    # K1 fused into the tensor-core prologue (KMX_FUSE=1): operands packed in
+    # shared memory, meta/prefix/range checks from the product's first CTA
+    env.update(KMX_TC="1", KMX_FUSE="1")
+    rng = random.Random(31 + variant)
+    for lf, lg, b, fs, gs in _cases(rng, [(256, 256, 64), (1024, 1024, 64), (300, 77, 17), (5, 700, 96)]):
+        want = {p: O.ks_mul(1, fs[p], gs[p], b, mode="native") for p in range(2)}
+        _check_batch(kmx, variant, fs, gs, b, want)
+    B, n = 8, 1024
+    fs = [[rng.randrange(-2**31, 2**31) for _ in range(n)] for _ in range(B)]
+    gs = [[rng.randrange(-2**31, 2**31) for _ in range(n)] for _ in range(B)]
+    want = {p: O.ks_mul_signed(1, fs[p], gs[p], 32, mode="native") for p in (0, 7)}
+    _check_batch(kmx, variant, fs, gs, 32, want, signed=True)
+    # a bad coefficient is still caught by the fused range check
+    bad = [[0] * 16]
+    bad[0][3] = 1 << 20
+    with pytest.raises(ValueError):
+        _check_batch(kmx, variant, bad, [[1] * 16], 16, {})

@@ -9,6 +9,7 @@ absolute cold-cache, serialised ncu durations).
 """
 import csv
 import json
+import re
 import sys
 from collections import OrderedDict
 
@@ -25,16 +26,19 @@ def summarise(path):
         rows.append((r["Kernel Name"], v * scale.get(r["Metric Unit"], 1e-3)))
     agg = OrderedDict()
     for name, us in rows:
-        short = name.split("(")[0].replace("kmx::", "").replace("void ", "")
+        base = name.split("(")[0]
+        mk = re.search(r"(k_\w+(<[^>]*>)?)", base)
+        short = mk.group(1) if mk else base.replace("void ", "")
         a = agg.setdefault(short, {"launches": 0, "total_us": 0.0})
         a["launches"] += 1
         a["total_us"] += us
-    kmx_total = sum(a["total_us"] for k, a in agg.items() if k.startswith("k_") and k != "k_imad_peak")
+    peaks = ("k_imad_peak", "k_tc_peak")
+    kmx_total = sum(a["total_us"] for k, a in agg.items() if k.startswith("k_") and k not in peaks)
     out = []
     for k, a in agg.items():
         e = {"kernel": k, "launches": a["launches"], "total_us": round(a["total_us"], 2),
              "mean_us": round(a["total_us"] / a["launches"], 2)}
-        if k.startswith("k_") and k != "k_imad_peak" and kmx_total > 0:
+        if k.startswith("k_") and k not in peaks and kmx_total > 0:
             e["share_of_kmx_time"] = round(a["total_us"] / kmx_total, 4)
         out.append(e)
     return {"source": path, "total_launches": len(rows), "kernels": out}
