@@ -272,7 +272,7 @@ def run_ours(args, cfg, rank, world, local_rank):
             e1.synchronize()
             total_ms += e0.elapsed_time(e1)
             launches += L.kmx_last_launch_count()
-            if cfg["kind"] == "ks" and graph is None:
+            if graph is None:
                 L.kmx_prof_read(prof, 6)
                 for i in range(6):
                     kern[i] += prof[i]
@@ -281,7 +281,7 @@ def run_ours(args, cfg, rank, world, local_rank):
         if mon is not None:
             clocks = mon.stop()
         op.status()
-        if cfg["kind"] == "ks" and graph is not None:
+        if graph is not None:
             # per-kernel durations: CUDA events around each launch (kmx_prof),
             # eager launches right after the graph-timed region
             L.kmx_prof_enable(1)
@@ -295,6 +295,13 @@ def run_ours(args, cfg, rank, world, local_rank):
         total_ms = mor(total_ms)
         ms = total_ms / args.steps
         rec = {"products_per_s": job_products(B, world) / (ms * 1e-3), "ms_per_step": ms, "launches_per_step": launches / args.steps}
+        if cfg["kind"] == "bks":
+            names = ["beval", "conv", "brecover"]
+            rec["kernel_ms"] = {nm: kern[i] / args.steps for i, nm in enumerate(names) if kern[i] > 0}
+            conv_ms = kern[1] / args.steps
+            if conv_ms > 0:  # one IMAD.WIDE (int32 x int32 -> int64) per coefficient MAC
+                rec["conv_macs_per_s"] = algorithmic_products(cfg, v) * B / (conv_ms * 1e-3)
+                rec["conv_frac_of_imad_peak"] = rec["conv_macs_per_s"] / peak
         if cfg["kind"] == "ks":
             names = ["pack", "mul", "finish", "recon", "bias"]
             rec["kernel_ms"] = {nm: kern[i] / args.steps for i, nm in enumerate(names) if kern[i] > 0}
@@ -568,8 +575,16 @@ def main():
         else:
             line["roofline_hbm"]["pack"] = "fused into the tensor-core multiply (operands packed in shared memory)"
     else:
-        line["roofline"] = {"bound": "imad", "kernel": "k_conv", "achieved": None, "peak": r["peak"] / 1e9,
-                            "unit": "G MAC/s", "frac": None, "traffic": None}
+        macs = algorithmic_products(cfg, v) * cfg["batch"]
+        cms = rec["kernel_ms"].get("conv")
+        ach = macs / (cms * 1e-3) / 1e9 if cms else None
+        line["roofline"] = {"bound": "imad", "kernel": "k_conv (int32 x int32 -> int64 IMAD.WIDE convolution)",
+                            "achieved": ach, "peak": r["peak"] / 1e9, "unit": "G MAC/s",
+                            "frac": ach * 1e9 / r["peak"] if ach else None,
+                            "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
+                            "algorithmic_work": f"{macs} coefficient MACs per launch "
+                                                f"({algorithmic_products(cfg, v)} per pair x {cfg['batch']})",
+                            "traffic": load_traffic(args.config, v, "conv_dram_bytes")}
     pv = r["per_variant"]
     line["per_variant"] = pv
     if all(VNAME[x] in pv for x in (1, 2, 3, 4)):

@@ -14,6 +14,7 @@
  *                        bks_negated / bks_four with ring_z()
  *                        (pkg/src/kronmul/bipoly.py:177-278)
  *   kmx_ks_params     <- kronmul.ksint.derive_params (ksint.py:82-98)
+ *   kmx_mod_mul       <- kronmul.modpoly.mod_mul (modpoly.py:95-115), batched
  *
  * Conventions
  *   - Plain pointers and sizes; no torch types.  Device entry points take
@@ -126,6 +127,20 @@ int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits,
 int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits,
                      const int32_t* f, const int32_t* g, int64_t* h);
 
+/* (Z/nZ)[x] products, 2 <= n < 2^64 (kronmul.modpoly.mod_mul,
+ * modpoly.py:95-115): f [batch][len_f], g [batch][len_g] u64 coefficients in
+ * [0, n) (checked -> KMX_EINVAL, modpoly.py:47-58); h [batch][len_f+len_g-1]
+ * u64 = the coefficients of f*g reduced mod n.  The lift uses b =
+ * max(1, bitlen(n-1)) (modpoly.py:104) and KS variant 1..4 (AUTO is resolved
+ * by the caller, modpoly.py:105-106). */
+size_t kmx_mod_workspace_bytes(int variant, int batch, int len_f, int len_g, uint64_t modulus);
+int kmx_mod_mul(int variant, int batch, int len_f, int len_g, uint64_t modulus,
+                const uint64_t* f, const uint64_t* g, uint64_t* h,
+                void* workspace, size_t ws_bytes, void* stream);
+int kmx_mod_mul_host(int variant, int batch, int len_f, int len_g, uint64_t modulus,
+                     const uint64_t* f, const uint64_t* g, uint64_t* h,
+                     uint64_t* limb_products64 /* nullable: MulStats count */);
+
 /* Measured IMAD.WIDE.U32 throughput on device 0 (32x32->64 products per
  * second, full chip), the roofline denominator for the multiply kernels. */
 double kmx_imad_peak(int iters);
@@ -151,7 +166,8 @@ int kmx_last_launch_count(void);
 /* Per-kernel CUDA-event timing of kmx_ks_mul on the calling thread (events
  * recorded on the caller's stream around each launch).  kmx_prof_read
  * synchronises on the last call's events and writes the durations in ms to
- * ms[0..4] = pack, multiply, finish, reconstruct, bias (0 if not launched);
+ * ms[0..5] = pack, multiply, finish, reconstruct, bias, mod reduction (0 if
+ * not launched; for kmx_bks_mul: 0 evaluation, 1 convolution, 2 recovery);
  * returns the number of kernels timed. */
 void kmx_prof_enable(int on);
 int kmx_prof_read(float* ms, int nslots);

@@ -432,6 +432,51 @@ def ks_mul_signed(variant: int, f, g, b: int, mode: str = "karatsuba") -> list[i
 
 
 # --------------------------------------------------------------------------
+# (Z/nZ)[x]  (modpoly.py:79-115, oracle.py:30-40)
+# --------------------------------------------------------------------------
+
+def mod_coeff_bits(n: int) -> int:
+    """modpoly.py:104: the lift's bound comes from the modulus, not the data."""
+    return max(1, (n - 1).bit_length())
+
+
+def choose_variant(length: int, coeff_bits: int, ks1_max: int = 48, ks3_max: int = 512) -> int:
+    """modpoly.py:79-92 (band lookup; defaults modpoly.py:74-75)."""
+    if length < 1 or coeff_bits < 1:
+        raise ValueError("length and coefficient bits must be >= 1")
+    if length <= ks1_max:
+        return 1
+    if length <= ks3_max:
+        return 3
+    return 4
+
+
+def mod_mul(variant: int, f, g, n: int, mode: str = "karatsuba", stats=None,
+            classical_only: bool = False) -> list[int]:
+    """modpoly.py:95-115: lift to Z with b = bitlen(n-1), KS product, reduce
+    every coefficient mod n.  variant 0 = AUTO (reference thresholds)."""
+    if n < 2:
+        raise ValueError("modulus must be >= 2")
+    for c in list(f) + list(g):
+        if not 0 <= c < n:
+            raise ValueError("coefficient outside [0, n)")
+    b = mod_coeff_bits(n)
+    if variant == 0:
+        variant = choose_variant(max(len(f), len(g)), b)
+    return [c % n for c in ks_mul(variant, f, g, b, mode, stats, classical_only)]
+
+
+def schoolbook_mod(f, g, n: int) -> list[int]:
+    """oracle.py:30-40: word-modular convolution."""
+    out = [0] * (len(f) + len(g) - 1)
+    for i, a in enumerate(f):
+        if a:
+            for j, c in enumerate(g):
+                out[i + j] = (out[i + j] + a * c) % n
+    return out
+
+
+# --------------------------------------------------------------------------
 # brute-force convolution  (oracle.py:19-27, :58-69)
 # --------------------------------------------------------------------------
 

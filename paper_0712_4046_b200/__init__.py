@@ -10,6 +10,8 @@ from ._lib import ReconstructionError
 from .batch import BksBatch, KsBatch, bks_mul_host, imad_peak, ks_mul_host, mul_engine, tc_peak
 from .bipoly import (BiPoly, MissingHalveError, RingOps, bks_four, bks_negated, bks_reciprocal,
                      bks_standard, ring_z, ring_zmod)
+from .modpoly import (DEFAULT_THRESHOLDS, GPU_THRESHOLDS, AutoThresholds, ModMulBatch, ModPoly, Variant,
+                      choose_variant, mod_mul, mod_mul_host)
 from .ksint import (derive_params, ks1_mul, ks2_mul, ks3_mul, ks4_mul, reconstruct_overlapped)
 from .kstypes import (DEFAULT_MUL_CONFIG, CoeffVec, KsParams, MulConfig, MulStats, OverlapDigits)
 
@@ -21,4 +23,6 @@ __all__ = [
     "reconstruct_overlapped", "BiPoly", "RingOps", "MissingHalveError", "ring_z", "ring_zmod",
     "bks_standard", "bks_reciprocal", "bks_negated", "bks_four", "KsBatch", "BksBatch",
     "ks_mul_host", "bks_mul_host", "imad_peak", "tc_peak", "mul_engine", "__version__",
+    "ModPoly", "Variant", "AutoThresholds", "DEFAULT_THRESHOLDS", "GPU_THRESHOLDS", "choose_variant",
+    "mod_mul", "ModMulBatch", "mod_mul_host",
 ]

@@ -110,6 +110,16 @@ void prof_begin(int slot, cudaStream_t st) {
 void prof_end(int slot, cudaStream_t st) {
   if (g_prof.on) cudaEventRecord(g_prof.ev[slot][1], st);
 }
+}  // namespace
+
+namespace kmx {
+void prof_mark(int slot, bool begin, cudaStream_t st) {
+  if (begin) prof_begin(slot, st); else prof_end(slot, st);
+}
+void prof_reset() { for (int i = 0; i < 6; i++) g_prof.used[i] = false; }
+}  // namespace kmx
+
+namespace {
 
 int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_words, unsigned flags) {
   memset(&p, 0, sizeof p);
@@ -544,6 +554,81 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
   return rc;
 }
 
+
+// ---------------------------------------------------------- (Z/nZ)[x] front end
+// kronmul.modpoly.mod_mul (modpoly.py:95-115): lift with b = bitlen(n-1)
+// (:103-104), run the KS variant, reduce every coefficient mod n (:115).
+static int mod_plan(KsPlan& p, int variant, int batch, int lf, int lg, uint64_t n) {
+  if (n < 2) return KMX_EINVAL;  // modpoly.py:50-51
+  int b = bitlen_u64(n - 1);
+  if (b < 1) b = 1;              // max(1, (n-1).bit_length()) (:104)
+  int rc = make_plan(p, variant, batch, lf, lg, b, 2, 0);
+  if (rc) return rc;
+  return p.out_words_min <= 8 ? KMX_OK : KMX_EINVAL;
+}
+static size_t mod_prod_bytes(const KsPlan& p) { return (size_t)p.batch * p.out_len * p.out_words_min * 4; }
+
+size_t kmx_mod_workspace_bytes(int variant, int batch, int len_f, int len_g, uint64_t modulus) {
+  KsPlan p;
+  if (mod_plan(p, variant, batch, len_f, len_g, modulus)) return 0;
+  return align256(p.total) + align256(mod_prod_bytes(p));
+}
+
+int kmx_mod_mul(int variant, int batch, int len_f, int len_g, uint64_t modulus, const uint64_t* f,
+                const uint64_t* g, uint64_t* h, void* workspace, size_t ws_bytes, void* stream) {
+  KsPlan p;
+  int rc = mod_plan(p, variant, batch, len_f, len_g, modulus);
+  if (rc) return rc;
+  if (ws_bytes < align256(p.total) + align256(mod_prod_bytes(p)) || !workspace) return KMX_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* prod = (uint32_t*)((char*)workspace + align256(p.total));
+  rc = run_plan(p, (const uint32_t*)f, (const uint32_t*)g, prod, p.out_words_min, workspace, p.total, st);
+  if (rc || batch == 0) return rc;
+  ModRedArgs a;
+  memset(&a, 0, sizeof a);
+  a.prod = prod; a.ow = p.out_words_min; a.count = (long long)batch * p.out_len;
+  a.n = modulus;
+  unsigned __int128 t = 1 % modulus;
+  for (int q = 0; q < 8; q++) { a.tpow[q] = (unsigned long long)t; t = (t << 32) % modulus; }
+  a.out = (unsigned long long*)h;
+  a.f = (const unsigned long long*)f; a.nf = (long long)batch * len_f;
+  a.g = (const unsigned long long*)g; a.ng = (long long)batch * len_g;
+  a.err = (uint32_t*)((char*)workspace + p.off_err);
+  prof_begin(5, st);
+  if (launch_modred(a, st) != cudaSuccess) return KMX_ECUDA;
+  prof_end(5, st);
+  g_launches++;
+  return KMX_OK;
+}
+
+int kmx_mod_mul_host(int variant, int batch, int len_f, int len_g, uint64_t modulus, const uint64_t* f,
+                     const uint64_t* g, uint64_t* h, uint64_t* limb_products64) {
+  KsPlan p;
+  int rc = mod_plan(p, variant, batch, len_f, len_g, modulus);
+  if (rc) return rc;
+  HostCtx* c = host_ctx(&rc);
+  if (!c) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (batch == 0) return KMX_OK;
+  const size_t fb = (size_t)batch * len_f * 8, gb = (size_t)batch * len_g * 8;
+  const size_t hb = (size_t)batch * p.out_len * 8;
+  const size_t wb = align256(p.total) + align256(mod_prod_bytes(p));
+  if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+  if ((rc = ensure(*c, 0, align256(fb) + gb + 256))) return rc;
+  if ((rc = ensure(*c, 1, hb))) return rc;
+  if ((rc = ensure(*c, 2, wb))) return rc;
+  uint64_t* df = (uint64_t*)c->buf[0];
+  uint64_t* dg = (uint64_t*)((char*)c->buf[0] + align256(fb));
+  if (cudaMemcpyAsync(df, f, fb, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaMemcpyAsync(dg, g, gb, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  rc = kmx_mod_mul(variant, batch, len_f, len_g, modulus, df, dg, (uint64_t*)c->buf[1], c->buf[2], c->cap[2], c->st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(h, c->buf[1], hb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
+  rc = kmx_ws_status(c->buf[2], c->st);
+  if (rc == KMX_OK && limb_products64)  // the KS workspace leads the mod workspace
+    rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, p.b, 0, limb_products64, c->st);
+  return rc;
+}
 
 size_t kmx_reconstruct_workspace_bytes(int batch, int count, int dwords) {
   if (batch < 0 || count < 1 || dwords < 1) return 0;

@@ -142,10 +142,13 @@ __global__ void __launch_bounds__(128) k_brecover(BivarPlan p, const int64_t* pr
 cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h, int32_t* evals,
                          int64_t* prods, uint32_t* err, cudaStream_t st, int* nlaunch) {
   *nlaunch = 0;
+  prof_reset();
   const long long ne = (long long)p.batch * p.P * 2 * p.Lu;
   int grid = (int)std::min<long long>((ne + 255) / 256, 148LL * 32);
   if (grid < 1) grid = 1;
+  prof_mark(0, true, st);
   k_beval<<<grid, 256, 0, st>>>(p, f, g, evals);
+  prof_mark(0, false, st);
   (*nlaunch)++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
@@ -160,9 +163,13 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   ca.P = prods; ca.p_stride = ps;
   ca.nprod = p.batch * p.P; ca.nbands = nbands; ca.G = split; ca.TI = tr;
   ca.counter = (int*)(err + 1);
+  prof_mark(1, true, st);
   if ((e = launch_conv(ca, st)) != cudaSuccess) return e;
+  prof_mark(1, false, st);
   (*nlaunch)++;
+  prof_mark(2, true, st);
   k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err);
+  prof_mark(2, false, st);
   (*nlaunch)++;
   return cudaGetLastError();
 }

@@ -135,6 +135,23 @@ struct BiasArgs {
   int batch;
 };
 
+// per-kernel CUDA-event timing (kmx_prof_*): slots 0 pack / beval, 1 mul / conv,
+// 2 finish / brecover, 3 recon, 4 bias, 5 modred
+void prof_mark(int slot, bool begin, cudaStream_t st);
+void prof_reset();
+
+// ------------------------------------------------------------- (Z/nZ)[x]
+// K9: h[i] = (sum_q prod[i][q] 2^(32q)) mod n, tpow[q] = 2^(32q) mod n
+struct ModRedArgs {
+  const uint32_t* prod; int ow; long long count;
+  unsigned long long n; unsigned long long tpow[8];
+  unsigned long long* out;
+  const unsigned long long* f; long long nf;   // inputs: 0 <= c < n check
+  const unsigned long long* g; long long ng;
+  uint32_t* err;
+};
+cudaError_t launch_modred(const ModRedArgs& a, cudaStream_t st);
+
 // kernels launched by the last C-ABI call on this thread (bench gpu_launches)
 extern thread_local int g_launches;
 

@@ -42,3 +42,12 @@ def bivar_cases():
 
 def signed_cases():
     return [(c["f"], c["g"], [int(v) for v in c["h"]]) for c in _load("signed_golden.json.gz")]
+
+
+def mod_golden():
+    d = _load("mod_golden.json.gz")
+    cases = []
+    for c in d["cases"]:
+        cases.append((c["tag"], [int(x) for x in c["f"]], [int(x) for x in c["g"]], int(c["n"]),
+                      [int(x) for x in c["h"]], c.get("limb_products_classical")))
+    return cases, [tuple(r) for r in d["choose_variant"]]
