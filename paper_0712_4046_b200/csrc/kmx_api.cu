@@ -28,11 +28,16 @@ namespace {
 
 int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
 
-// K2 engine choice: KMX_TC=0 forces the integer-pipe schoolbook, KMX_TC=1 the
-// tcgen05 byte convolution wherever its shape gate admits the operands.
+// K2 engine choice.  Default: the tcgen05 byte convolution wherever its shape
+// gate admits the operands and the shorter one has more than 144 limbs; below
+// that the integer-pipe schoolbook is faster (config-5 sweep with KMX_TC=0 vs
+// default: the crossover sits at 134..145 limbs).  KMX_TC=0 forces the
+// integer pipe, KMX_TC=1 the tensor cores wherever supported.
 bool use_tensor_mul(int ma, int mb) {
   const char* v = getenv("KMX_TC");
-  if (v && *v && atoi(v) == 0) return false;
+  const int force = v && *v ? atoi(v) : -1;
+  if (force == 0) return false;
+  if (force < 0 && (ma < mb ? ma : mb) <= 144) return false;
   return tc_supported(ma, mb);
 }
 

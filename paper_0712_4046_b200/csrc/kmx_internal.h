@@ -107,6 +107,9 @@ struct FinishArgs {
 };
 constexpr int FIN_THREADS = 256;
 constexpr int FIN_HALO = 32;
+// warp-per-stream finish (kmx_finish.cu) for short streams / many streams
+bool finish_use_warp(const FinishArgs& a, int batch);
+cudaError_t launch_finish_w(const FinishArgs& a, int batch, cudaStream_t st);
 
 // --------------------------------------------------------- reconstruction
 struct ReconStream { int fslot, rslot, count, pos0, pstride; };

@@ -15,6 +15,7 @@
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
 #include "kmx_pack.cuh"
+#include "kmx_store.cuh"
 
 namespace kmx {
 
@@ -40,36 +41,6 @@ __device__ __forceinline__ u32 block_resolve1(i64 y, i64 cin, u32* sm_scan, i64*
   *cout = (i64)cm_apply(tot, 0) + hlast;
   __syncthreads();
   return (u32)(z + c);
-}
-
-// ---- signed-input bias correction applied at store time (see BiasFix)
-__device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int128 hp, long long k, const BiasFix& bf,
-                                               long long pair) {
-  u64 lo = (u64)hp, hi = (u64)(hp >> 64);
-  if (bf.enabled) {
-    const unsigned long long* PF = bf.pf + pair * bf.pair_stride;
-    const long long lf = bf.lf, lg = bf.lg;
-    const long long i0 = k - lg + 1 > 0 ? k - lg + 1 : 0, i1 = k < lf - 1 ? k : lf - 1;
-    const long long j0 = k - lf + 1 > 0 ? k - lf + 1 : 0, j1 = k < lg - 1 ? k : lg - 1;
-    // staged copies are padded: entry i at i + (i >> lgpad) (PG follows PF)
-    auto pe = [&](long long i) -> u64 { return PF[bf.lgpad >= 0 ? i + (i >> bf.lgpad) : i]; };
-    const long long g0 = lf + 1;
-    const u64 S = (pe(i1 + 1) - pe(i0)) + (pe(g0 + j1 + 1) - pe(g0 + j0));
-    const u64 cnt = (u64)(i1 - i0 + 1);
-    const int sh1 = bf.b - 1, sh2 = 2 * bf.b - 2;       // 0..31, 0..62
-    const u64 a_lo = S << sh1, a_hi = sh1 ? (S >> (64 - sh1)) : 0ull;
-    const u64 c_lo = cnt << sh2, c_hi = sh2 ? (cnt >> (64 - sh2)) : 0ull;
-    const u64 l1 = lo - a_lo;                          // v - S 2^(b-1)
-    const u64 h1 = hi - a_hi - (l1 > lo ? 1ull : 0ull);
-    lo = l1 + c_lo;                                    // + cnt 2^(2b-2)
-    hi = h1 + c_hi + (lo < l1 ? 1ull : 0ull);
-  }
-  const u32 ext = (hi >> 63) ? 0xffffffffu : 0u;
-  dst[0] = (u32)lo;
-  if (ow > 1) dst[1] = (u32)(lo >> 32);
-  if (ow > 2) dst[2] = (u32)hi;
-  if (ow > 3) dst[3] = (u32)(hi >> 32);
-  for (int w = 4; w < ow; w++) dst[w] = ext;
 }
 
 template <bool STAGED>
@@ -284,6 +255,7 @@ __global__ void __launch_bounds__(FN_T) k_finish(FinishArgs a) {
 }
 
 cudaError_t launch_finish(const FinishArgs& a, int batch, cudaStream_t st) {
+  if (finish_use_warp(a, batch)) return launch_finish_w(a, batch, st);  // kmx_finish.cu
   k_finish<<<batch * a.ns, FN_T, 0, st>>>(a);
   return cudaGetLastError();
 }

@@ -201,10 +201,16 @@ __global__ void __launch_bounds__(32 * MUL_WARPS) k_mul(MulArgs a) {
   u32* wsm = smem + warp * 2 * (2 * a.TI + CW + 8);
   const int mp = a.ma + a.mb;
   const int nunits = a.nprod * a.nbands;
-  for (;;) {
-    int u = 0;
-    if (lane == 0) u = atomicAdd(a.counter, 1);
-    u = __shfl_sync(0xffffffffu, u, 0);
+  // single-band products (mp <= CW): equal-cost units, assigned statically
+  // (grid-stride over warps) -- no work counter to contend on
+  const bool stat = a.nbands == 1;
+  int u = stat ? blockIdx.x * MUL_WARPS + warp : 0;
+  const int ustep = gridDim.x * MUL_WARPS;
+  for (;; u += ustep) {
+    if (!stat) {
+      if (lane == 0) u = atomicAdd(a.counter, 1);
+      u = __shfl_sync(0xffffffffu, u, 0);
+    }
     if (u >= nunits) break;
     const int z = u % a.nprod;
     const int bi = middle_out(u / a.nprod, a.nbands);
@@ -308,8 +314,10 @@ void mul_geometry(int ma, int mb, int* split, int* cw, int* nbands, int* tr) {
   *cw = CW;
   *nbands = (mp + CW - 1) / CW;
   // rows per staged chunk (double-buffered per warp): the whole row span of a
-  // band when it is short
+  // band when it is short; a single-band product (mp <= CW) walks at most
+  // max(ma, mb) + 8 steps, so it stages just that
   int T = ((m + CW + 7) & ~7);
+  if (mp <= CW) T = ((ma > mb ? ma : mb) + 8 + 7 + 7) & ~7;
   int cap = 512;
   const int te = env_int("KMX_TR", 0);
   if (te >= 8) cap = te & ~7;

@@ -283,8 +283,13 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
     StreamCur ce, co;
     ce.init(q0, 0, S);
     co.init(q0, C.N, S);
-    i64 t[PK_V];
-    u32 M = CM_IDENT, mr[PK_V];
+    // t_v = e_v +- o_v lies in (-2^32, 2^33), so carries stay in {-1, 0, 1}.
+    // Resolve this thread's digits with carry-in 0; a carry-in of +1 (-1)
+    // alters the carry-out only when those digits are all ones (all zeros),
+    // so the thread's carry map is (c0 - all0, c0, c0 + allF).
+    u32 d[PK_V];
+    int c = 0;
+    u32 allF = 0xffffffffu, any = 0u;
 #pragma unroll
     for (int v = 0; v < PK_V; v++) {
       const int q = q0 + v;
@@ -295,21 +300,29 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
       }
       ce.next(S);
       co.next(S);
-      t[v] = !neg ? (i64)e + ov : (order > 0 ? (i64)e - ov : (i64)ov - e);
-      mr[v] = cm_make(t[v]);
-      M = cm_compose(M, mr[v]);
+      const i64 x = (!neg ? (i64)e + ov : (order > 0 ? (i64)e - ov : (i64)ov - e)) + c;
+      d[v] = (u32)x;
+      c = (int)(x >> 32);
+      allF &= d[v];
+      any |= d[v];
     }
+    const u32 M = (u32)(c - (any == 0u ? 1 : 0) + 1) | ((u32)(c + 1) << 2) |
+                  ((u32)(c + (allF == 0xffffffffu ? 1 : 0) + 1) << 4);
     u32 tot;
     const u32 exc = cm_seg_scan(M, T, sm_scan, &tot);
     const int cin = (int)sm_carry;
-    int c = cm_apply(exc, cin);
-    u32 d[PK_V];
+    int k = cm_apply(exc, cin);
+    if (k) {  // ripple the carry-in through this thread's digits
 #pragma unroll
-    for (int v = 0; v < PK_V; v++) {
-      d[v] = (u32)(t[v] + c);
-      c = cm_apply(mr[v], c);
-      if (q0 + v < m && d[v]) { my_top = q0 + v + 1; my_topv = d[v]; }
+      for (int v = 0; v < PK_V; v++) {
+        const u32 old = d[v];
+        d[v] = old + (u32)k;
+        k = k > 0 ? (d[v] == 0u ? 1 : 0) : (k < 0 && old == 0u ? -1 : 0);
+      }
     }
+#pragma unroll
+    for (int v = 0; v < PK_V; v++)
+      if (q0 + v < m && d[v]) { my_top = q0 + v + 1; my_topv = d[v]; }
     if (q0 + PK_V <= m) {
       uint4* dst = reinterpret_cast<uint4*>(out + q0);
       dst[0] = make_uint4(d[0], d[1], d[2], d[3]);

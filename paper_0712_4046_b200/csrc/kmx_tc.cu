@@ -31,7 +31,10 @@
 //
 // TMEM: each tile owns 16H columns of 32-bit sums.  A sum has at most
 // min(La,Lb) byte products < 2^16 each; read as u32 (the accumulator wraps, no
-// saturation) it is exact for min(La,Lb) <= 65536.
+// saturation) it is exact for min(La,Lb) <= 65536.  Longer operands split
+// the K-steps into segments of TC_SEG_STEPS (32 * 2048 = 65536 bytes of b):
+// each segment accumulates into its own TMEM columns and the epilogue adds
+// the segments' exact partial sums in 64-bit.
 //
 // Epilogue: thread m reads its 16H accumulators (tcgen05.ld 32x32b.x16),
 // forms limb column sums (< 2^56), stages them in shared memory in limb
@@ -51,6 +54,10 @@ namespace {
 
 constexpr int TC_EPI = 128;  // warps 0-3: epilogue (TMEM lane quarters)
 constexpr int TC_MAX_COLS = 256;  // TMEM columns per CTA (two CTAs per SM fit)
+constexpr int TC_SEG_LOG = 11;    // K-steps per exact accumulation segment: 2^11 * 32 B = 64 KB
+__host__ __device__ inline int tc_nseg(int Lb, int S) {
+  return Lb <= 65536 ? 1 : (S + (1 << TC_SEG_LOG) - 1) >> TC_SEG_LOG;
+}
 
 template <int H>
 struct TcG {
@@ -167,6 +174,7 @@ struct TcArgs {
   int NB;       // B stages in the ring (2..TC_MAXNB)
   int TPC;      // tiles per CTA
   int nranges;  // CTAs per product = ceil(ntiles / TPC)
+  int nseg;     // exact accumulation segments of the K-steps (tc_nseg)
   int fuse;     // pack the operands in the prologue (pk, P)
   int P;        // products per pair
   size_t ring;  // bytes of the B ring (>= the pack staging area when fused)
@@ -241,8 +249,9 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
   const int clo = cs_lo < cs_hi ? cs_lo / KC : 0;
   const int chi = cs_lo < cs_hi ? (cs_hi + KC - 1) / KC : 0;
 
+  const int nseg = ta.nseg;
   uint32_t cols = 32;
-  while (cols < (uint32_t)(nt * G::N)) cols <<= 1;
+  while (cols < (uint32_t)(nt * nseg * G::N)) cols <<= 1;
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
                  "r"(cols));
@@ -327,13 +336,14 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
           int slo, shi;
           tc_tile_steps<H>(d, t, slo, shi);
           const int s0 = max(slo, sb), s1 = min(shi, se);
-          const uint32_t dcol = tmem + (uint32_t)((t - t0) * G::N);
           const uint32_t abase = sA + (uint32_t)(t * G::T + d.ulo);
           for (int s = s0; s < s1; s++) {
+            const int cell = (t - t0) + (nseg > 1 ? (s >> TC_SEG_LOG) * nt : 0);  // (tile, segment)
+            const uint32_t dcol = tmem + (uint32_t)(cell * G::N);
             const uint64_t ad = sdesc(abase + 32u * (uint32_t)s, 16, G::SBO_A);
             const uint64_t bd = sdesc(sB + (uint32_t)((s - sb) * G::STEPB), 128, 256);
-            mma_i8(dcol, ad, bd, G::IDESC, (started >> (t - t0)) & 1u);
-            started |= 1u << (t - t0);
+            mma_i8(dcol, ad, bd, G::IDESC, (started >> cell) & 1u);
+            started |= 1u << cell;
           }
         }
         mma_commit(smem_u32(&sh.bar_empty[st]));
@@ -409,18 +419,22 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
     if (epi) {
 #pragma unroll
       for (int j = 0; j < H; j++) {
-        uint32_t v[16];
-        if (slo < shi) {
-          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((t - t0) * G::N + 16 * j), v);
-        } else {
+        unsigned long long ls[4] = {0ull, 0ull, 0ull, 0ull};
+        for (int g = 0; g < nseg; g++) {
+          // segment g of this tile: K-steps [max(slo, g 2^SEG), min(shi, (g+1) 2^SEG))
+          const int glo = nseg > 1 ? max(slo, g << TC_SEG_LOG) : slo;
+          const int ghi = nseg > 1 ? min(shi, (g + 1) << TC_SEG_LOG) : shi;
+          if (glo >= ghi) continue;
+          uint32_t v[16];
+          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(((t - t0) + g * nt) * G::N + 16 * j), v);
 #pragma unroll
-          for (int q = 0; q < 16; q++) v[q] = 0u;
+          for (int q = 0; q < 4; q++)
+            ls[q] += (unsigned long long)v[4 * q] + ((unsigned long long)v[4 * q + 1] << 8) +
+                     ((unsigned long long)v[4 * q + 2] << 16) + ((unsigned long long)v[4 * q + 3] << 24);
         }
         unsigned long long* dst = stg + 4 * (m & 7) + 32 * j + 32 * H * (m >> 3);
 #pragma unroll
-        for (int q = 0; q < 4; q++)
-          dst[q] = (unsigned long long)v[4 * q] + ((unsigned long long)v[4 * q + 1] << 8) +
-                   ((unsigned long long)v[4 * q + 2] << 16) + ((unsigned long long)v[4 * q + 3] << 24);
+        for (int q = 0; q < 4; q++) dst[q] = ls[q];
       }
     }
     __syncthreads();
@@ -504,7 +518,7 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
 
 // ---------------------------------------------------------------- planning
 struct TcPlan {
-  int H, NW, KC, NB, TPC, nranges, ntiles;
+  int H, NW, KC, NB, TPC, nranges, ntiles, nseg;
   size_t smem;
   double cost;  // modelled cycles per product
 };
@@ -557,8 +571,9 @@ double tc_cost(const TcDims& d, int TPC, int NW) {
 template <int H>
 bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
-  if (4LL * mB > 65536) return false;  // u32 accumulator exactness
   const TcDims d = tc_dims<H>(mA, mB);
+  const int nseg = tc_nseg(d.Lb, d.S);  // u32 accumulator exactness: <= 64 KB of b per segment
+  if (nseg * TcG<H>::N > TC_MAX_COLS) return false;
   int KC = env_int_tc("KMX_TC_KC", 16);
   if (KC < 4) KC = 4;
   int NB = env_int_tc("KMX_TC_NB", 2);
@@ -571,7 +586,7 @@ bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p) {
     else KC /= 2;
   }
   if (tc_smem<H>(d.La, d.Lb, KC, NB, stage) > cap) return false;
-  int TPC = TC_MAX_COLS / TcG<H>::N;
+  int TPC = TC_MAX_COLS / (TcG<H>::N * nseg);
   if (TPC > d.ntiles) TPC = d.ntiles;
   const int tpc_env = env_int_tc("KMX_TC_TPC", 0);
   if (tpc_env > 0 && tpc_env < TPC) TPC = tpc_env;
@@ -585,6 +600,7 @@ bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p) {
   p.TPC = TPC;
   p.ntiles = d.ntiles;
   p.nranges = (d.ntiles + TPC - 1) / TPC;
+  p.nseg = nseg;
   p.smem = tc_smem<H>(d.La, d.Lb, KC, NB, stage);
   p.cost = tc_cost<H>(d, TPC, p.NW);
   return true;
@@ -719,8 +735,8 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
   if (!tc_plan(a.ma, a.mb, a.nprod, stage, p)) return cudaErrorNotSupported;
   if (a.nprod == 0) return cudaSuccess;
   if (env_int_tc("KMX_TC_VERBOSE", 0))
-    fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d smem=%zu cost=%.0f\n",
-            a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.smem, p.cost);
+    fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d nseg=%d smem=%zu cost=%.0f\n",
+            a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.nseg, p.smem, p.cost);
   TcArgs ta;
   ta.m = a;
   ta.KC = p.KC;
@@ -734,6 +750,7 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
   }
   ta.TPC = p.TPC;
   ta.nranges = p.nranges;
+  ta.nseg = p.nseg;
   cudaError_t e;
   switch (p.H) {
     case 1: e = launch_h<1>(ta, p.NW, p.smem, st); break;

@@ -1,0 +1,32 @@
+"""Every kernel-selection path of the CUDA pipeline is parity-tested, not
+only the one the shape heuristics pick: tools/paths_check.py runs in a
+subprocess per forced setting (the library reads its KMX_* switches once per
+process) and compares golden + BASELINE-shaped cases bit-exactly with the
+oracle."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+torch = pytest.importorskip("torch")
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SETTINGS = [
+    {"KMX_FINISH_WARP": "1"},   # warp-per-stream finish everywhere (incl. c4 long streams)
+    {"KMX_FINISH_WARP": "0"},   # block finish everywhere
+    {"KMX_TC": "0"},            # integer-pipe multiply everywhere
+    {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands)
+]
+
+
+@pytest.mark.parametrize("env", SETTINGS, ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()))
+def test_forced_kernel_path(env):
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "paths_check.py")],
+                       env={**os.environ, **env}, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
