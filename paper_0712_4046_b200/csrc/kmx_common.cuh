@@ -103,6 +103,33 @@ __device__ __forceinline__ void mac96(u32& c0, u32& c1, u32& c2, u32 a, u32 b) {
 __host__ __device__ __forceinline__ int cdiv(int a, int b) { return (a + b - 1) / b; }
 __host__ __device__ __forceinline__ long long cdivll(long long a, long long b) { return (a + b - 1) / b; }
 
+// Block prefix sums (signed inputs' bias lift; used by K1 and the bias kernel).
+static __device__ void block_prefix_u64(const u32* x, int n, u32 bias, u32 bmask, unsigned long long* out) {
+  // out[0] = 0, out[i+1] = sum_{k<=i} ((x[k] + bias) & bmask)
+  __shared__ unsigned long long wsum[8];
+  __shared__ unsigned long long run;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) { run = 0; out[0] = 0; }
+  __syncthreads();
+  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
+    const int i = i0 + tid;
+    unsigned long long v = i < n ? (unsigned long long)((x[i] + bias) & bmask) : 0ull;
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const unsigned long long o = __shfl_up_sync(0xffffffffu, v, off);
+      if (lane >= off) v += o;
+    }
+    if (lane == 31) wsum[warp] = v;
+    __syncthreads();
+    unsigned long long pre = run;
+    for (int k = 0; k < warp; k++) pre += wsum[k];
+    if (i < n) out[i + 1] = pre + v;
+    __syncthreads();
+    if (tid == blockDim.x - 1) run = pre + v;
+    __syncthreads();
+  }
+}
+
 // Read 32 bits starting at bit `bit` of a little-endian word array of
 // `nwords` words (bits beyond the array read as zero).
 __device__ __forceinline__ u32 bits32(const u32* w, int nwords, long long bit) {

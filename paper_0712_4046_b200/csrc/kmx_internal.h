@@ -128,6 +128,7 @@ struct ReconArgs {
   int stage;                  // k_recon_par: stream digits staged in shared memory
   uint32_t* diag;             // optional counter of sequential fallbacks
   int rw_slice;               // k_recon_warp: shared-memory words per warp
+  int bias_smem;              // k_recon_par: stage the signed path's prefix sums in shared memory
 };
 
 // ---------------------------------------------------------- signed (bias)

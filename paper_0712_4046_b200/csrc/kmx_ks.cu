@@ -1,7 +1,6 @@
 // Batched multipoint Kronecker substitution kernels for B200 (sm_100a).
 //
-//   k_pack    evaluation of coefficient vectors at +-2^N, +-2^-N
-//             (pack.py:62-110 / bignat._pack_ints bignat.py:411-428)
+//   (k_pack: kmx_pack.cu)
 //   (k_mul / k_conv: kmx_mul.cu)
 //   k_finish  half-sum / half-difference, exact halving and shifts, digit
 //             extraction (ksint.py:219-279, :305-345; bignat.py:265-274,
@@ -14,7 +13,6 @@
 
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
-#include "kmx_pack.cuh"
 #include "kmx_store.cuh"
 
 namespace kmx {
@@ -43,36 +41,6 @@ __device__ __forceinline__ u32 block_resolve1(i64 y, i64 cin, u32* sm_scan, i64*
   return (u32)(z + c);
 }
 
-template <bool STAGED>
-__global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
-  extern __shared__ u32 pk_sc[];
-  const int pair = blockIdx.x / A.nops;
-  pack_op<STAGED>(A, pair, blockIdx.x - pair * A.nops, pk_sc, nullptr);
-}
-
-cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
-  int mmax = 0;
-  for (int i = 0; i < a.nops; i++) mmax = a.op[i].m > mmax ? a.op[i].m : mmax;
-  int T = ((mmax + PK_V - 1) / PK_V + 31) & ~31;  // sized to the operand
-  if (T < 32) T = 32;
-  if (T > PK_T) T = PK_T;
-  int lmax = 0;
-  for (int i = 0; i < a.nops; i++) lmax = a.op[i].len > lmax ? a.op[i].len : lmax;
-  PackArgs b = a;
-  const int nw = (lmax + PK_PAD) * a.in_words;
-  b.stage = nw <= PK_STAGE_WORDS;
-  const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;
-  if (b.stage) {
-    if (smem > 44 * 1024) {  // + static shared memory must fit the opt-in limit
-      cudaError_t e = cudaFuncSetAttribute(k_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-    }
-    k_pack<true><<<batch * a.nops, T, smem, st>>>(b);
-  } else {
-    k_pack<false><<<batch * a.nops, T, 0, st>>>(b);
-  }
-  return cudaGetLastError();
-}
 
 // ========================================================================
 // K3: finish.  One CTA per (pair, output stream).  Streams through the
@@ -979,8 +947,10 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
   const int V = 1 << lgV;
   if (a.stage) {  // whole stream resident in shared memory (padded), cp.async all in flight
     const int slot = stage_stream(rst, F, R, S.count, a.dwords, lgV, threadIdx.x, blockDim.x);
-    BiasFix bfx = a.bias;  // signed inputs: prefix sums staged next to the digits, fused into the output walk
-    if (a.bias.enabled) stage_prefix(rst + 2 * slot, bfx, pair, lgV, S.pstride, threadIdx.x, blockDim.x);
+    // signed inputs: the correction is fused into the output walk, reading the
+    // prefix sums from L2 (or a copy staged next to the digits: bias_smem)
+    BiasFix bfx = a.bias;
+    if (a.bias.enabled && a.bias_smem) stage_prefix(rst + 2 * slot, bfx, pair, lgV, S.pstride, threadIdx.x, blockDim.x);
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
@@ -1160,7 +1130,11 @@ static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStre
   if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;
   ReconArgs b = a;
   size_t smem = (size_t)(2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4) * sizeof(u32);
-  if (a.bias.enabled) smem += (size_t)(4 * (a.bias.lf + a.bias.lg + 2) + 4) * sizeof(u32);
+  // signed path: prefix sums staged in shared memory (default; c2 ks4 recon 68 us)
+  // or read from L2 (KMX_RECON_BIAS_SMEM=0: 78 us, the occupancy gain does not pay)
+  static const int bias_smem = getenv("KMX_RECON_BIAS_SMEM") ? atoi(getenv("KMX_RECON_BIAS_SMEM")) : 1;
+  b.bias_smem = bias_smem;
+  if (a.bias.enabled && bias_smem) smem += (size_t)(4 * (a.bias.lf + a.bias.lg + 2) + 4) * sizeof(u32);
   b.stage = smem <= 160 * 1024;
   if (b.stage && smem > 32 * 1024) {  // dynamic + ~5 KB static must fit the opt-in limit
     cudaError_t e = cudaFuncSetAttribute(k_recon_par<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

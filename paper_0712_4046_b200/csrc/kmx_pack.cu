@@ -1,0 +1,42 @@
+// kmx_pack.cu -- K1, the standalone pack kernel: evaluation of the
+// coefficient vectors at +-2^N, +-2^-N (pack.py:62-110, bignat._pack_ints
+// bignat.py:411-428), one block per (pair, pack op); the per-operand body is
+// pack_op in kmx_pack.cuh (shared with the fused tensor-core prologue).
+#include "kmx_common.cuh"
+#include "kmx_internal.h"
+#include "kmx_pack.cuh"
+
+namespace kmx {
+
+template <bool STAGED>
+__global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
+  extern __shared__ u32 pk_sc[];
+  const int pair = blockIdx.x / A.nops;
+  pack_op<STAGED>(A, pair, blockIdx.x - pair * A.nops, pk_sc, nullptr);
+}
+
+cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
+  int mmax = 0;
+  for (int i = 0; i < a.nops; i++) mmax = a.op[i].m > mmax ? a.op[i].m : mmax;
+  int T = ((mmax + PK_V - 1) / PK_V + 31) & ~31;  // sized to the operand
+  if (T < 32) T = 32;
+  if (T > PK_T) T = PK_T;
+  int lmax = 0;
+  for (int i = 0; i < a.nops; i++) lmax = a.op[i].len > lmax ? a.op[i].len : lmax;
+  PackArgs b = a;
+  const int nw = (lmax + PK_PAD) * a.in_words;
+  b.stage = nw <= PK_STAGE_WORDS;
+  const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;
+  if (b.stage) {
+    if (smem > 44 * 1024) {  // + static shared memory must fit the opt-in limit
+      cudaError_t e = cudaFuncSetAttribute(k_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_pack<true><<<batch * a.nops, T, smem, st>>>(b);
+  } else {
+    k_pack<false><<<batch * a.nops, T, 0, st>>>(b);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace kmx

@@ -22,32 +22,6 @@ namespace kmx {
 // PK_V consecutive digits and walks the coefficient windows incrementally;
 // carries are resolved with one block scan of carry maps per chunk.
 // ========================================================================
-static __device__ void block_prefix_u64(const u32* x, int n, u32 bias, u32 bmask, unsigned long long* out) {
-  // out[0] = 0, out[i+1] = sum_{k<=i} ((x[k] + bias) & bmask)
-  __shared__ unsigned long long wsum[8];
-  __shared__ unsigned long long run;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) { run = 0; out[0] = 0; }
-  __syncthreads();
-  for (int i0 = 0; i0 < n; i0 += blockDim.x) {
-    const int i = i0 + tid;
-    unsigned long long v = i < n ? (unsigned long long)((x[i] + bias) & bmask) : 0ull;
-#pragma unroll
-    for (int off = 1; off < 32; off <<= 1) {
-      const unsigned long long o = __shfl_up_sync(0xffffffffu, v, off);
-      if (lane >= off) v += o;
-    }
-    if (lane == 31) wsum[warp] = v;
-    __syncthreads();
-    unsigned long long pre = run;
-    for (int k = 0; k < warp; k++) pre += wsum[k];
-    if (i < n) out[i + 1] = pre + v;
-    __syncthreads();
-    if (tid == blockDim.x - 1) run = pre + v;
-    __syncthreads();
-  }
-}
-
 // Prefix sums of n staged values in natural order (x[i] at x[rev ? n-1-i : i]):
 // out[0] = 0, out[i+1] = sum_{k<=i} x[k].  Each thread owns a contiguous
 // segment; one block scan of the segment sums.
@@ -337,7 +311,14 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
     __syncthreads();
   }
   if (tid == 0 && sm_carry != 0) raise_err(A.err, ERR_INEXACT);  // operand overflow (cannot happen)
-  if (my_top) atomicMax(&sm_top, ((unsigned long long)my_top << 32) | my_topv);
+  {  // top nonzero digit: warp max first, one shared atomic per warp
+    const unsigned wmax = __reduce_max_sync(0xffffffffu, (unsigned)my_top);
+    if (wmax) {
+      const int src = __ffs(__ballot_sync(0xffffffffu, (unsigned)my_top == wmax)) - 1;
+      const u32 v = __shfl_sync(0xffffffffu, my_topv, src);
+      if ((tid & 31) == 0) atomicMax(&sm_top, ((unsigned long long)wmax << 32) | v);
+    }
+  }
   __syncthreads();
   if (tid == 0 && side_effects) {
     const int top = (int)(sm_top >> 32);

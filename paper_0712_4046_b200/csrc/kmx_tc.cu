@@ -337,13 +337,19 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
           tc_tile_steps<H>(d, t, slo, shi);
           const int s0 = max(slo, sb), s1 = min(shi, se);
           const uint32_t abase = sA + (uint32_t)(t * G::T + d.ulo);
-          for (int s = s0; s < s1; s++) {
-            const int cell = (t - t0) + (nseg > 1 ? (s >> TC_SEG_LOG) * nt : 0);  // (tile, segment)
-            const uint32_t dcol = tmem + (uint32_t)(cell * G::N);
-            const uint64_t ad = sdesc(abase + 32u * (uint32_t)s, 16, G::SBO_A);
-            const uint64_t bd = sdesc(sB + (uint32_t)((s - sb) * G::STEPB), 128, 256);
-            mma_i8(dcol, ad, bd, G::IDESC, (started >> cell) & 1u);
-            started |= 1u << cell;
+          // split [s0, s1) at the exact-accumulation segment boundaries
+          for (int sa = s0; sa < s1;) {
+            const int cell = (t - t0) + (sa >> TC_SEG_LOG) * nt;  // (tile, segment); nt = 0 stride if nseg == 1
+            const int se2 = nseg > 1 ? min(s1, ((sa >> TC_SEG_LOG) + 1) << TC_SEG_LOG) : s1;
+            const uint32_t dcol = tmem + (uint32_t)((nseg > 1 ? cell : t - t0) * G::N);
+            const uint32_t bit = 1u << (nseg > 1 ? cell : t - t0);
+            for (int s = sa; s < se2; s++) {
+              const uint64_t ad = sdesc(abase + 32u * (uint32_t)s, 16, G::SBO_A);
+              const uint64_t bd = sdesc(sB + (uint32_t)((s - sb) * G::STEPB), 128, 256);
+              mma_i8(dcol, ad, bd, G::IDESC, (started & bit) ? 1u : 0u);
+              started |= bit;
+            }
+            sa = se2;
           }
         }
         mma_commit(smem_u32(&sh.bar_empty[st]));
@@ -420,6 +426,16 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
 #pragma unroll
       for (int j = 0; j < H; j++) {
         unsigned long long ls[4] = {0ull, 0ull, 0ull, 0ull};
+        if (nseg == 1) {
+          if (slo < shi) {
+            uint32_t v[16];
+            tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)((t - t0) * G::N + 16 * j), v);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              ls[q] = (unsigned long long)v[4 * q] + ((unsigned long long)v[4 * q + 1] << 8) +
+                      ((unsigned long long)v[4 * q + 2] << 16) + ((unsigned long long)v[4 * q + 3] << 24);
+          }
+        } else
         for (int g = 0; g < nseg; g++) {
           // segment g of this tile: K-steps [max(slo, g 2^SEG), min(shi, (g+1) 2^SEG))
           const int glo = nseg > 1 ? max(slo, g << TC_SEG_LOG) : slo;

@@ -20,6 +20,7 @@ SETTINGS = [
     {"KMX_FINISH_WARP": "0"},   # block finish everywhere
     {"KMX_TC": "0"},            # integer-pipe multiply everywhere
     {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands)
+    {"KMX_RECON_BIAS_SMEM": "0", "KMX_RECON_WARP": "1"},  # signed prefix sums from L2; warp-per-stream recon
 ]
 
 
