@@ -15,6 +15,7 @@
  *                        (pkg/src/kronmul/bipoly.py:177-278)
  *   kmx_ks_params     <- kronmul.ksint.derive_params (ksint.py:82-98)
  *   kmx_mod_mul       <- kronmul.modpoly.mod_mul (modpoly.py:95-115), batched
+ *   kmx_bks_mod_mul   <- kronmul.bipoly.bks_* with ring_zmod(n) (bipoly.py:59-72, :177-278)
  *
  * Conventions
  *   - Plain pointers and sizes; no torch types.  Device entry points take
@@ -140,6 +141,19 @@ int kmx_mod_mul(int variant, int batch, int len_f, int len_g, uint64_t modulus,
 int kmx_mod_mul_host(int variant, int batch, int len_f, int len_g, uint64_t modulus,
                      const uint64_t* f, const uint64_t* g, uint64_t* h,
                      uint64_t* limb_products64 /* nullable: MulStats count */);
+
+/* Bivariate R[x,y] -> R[x] reductions over R = Z/nZ, 2 <= n < 2^64
+ * (bipoly.py:177-278 with ring_zmod(n), :59-72).  f, g: [batch][lx][ly] u64
+ * residues in [0, n) (checked -> KMX_EINVAL); h: [batch][2lx-1][2ly-1] u64.
+ * The univariate products run through kmx_mod_mul.  Variants 3 and 4 need
+ * the ring's halving and return KMX_EINVAL for even n (the reference raises
+ * MissingHalveError, bipoly.py:116-118). */
+size_t kmx_bks_mod_workspace_bytes(int variant, int batch, int lx, int ly, uint64_t modulus);
+int kmx_bks_mod_mul(int variant, int batch, int lx, int ly, uint64_t modulus,
+                    const uint64_t* f, const uint64_t* g, uint64_t* h,
+                    void* workspace, size_t ws_bytes, void* stream);
+int kmx_bks_mod_mul_host(int variant, int batch, int lx, int ly, uint64_t modulus,
+                         const uint64_t* f, const uint64_t* g, uint64_t* h);
 
 /* Measured IMAD.WIDE.U32 throughput on device 0 (32x32->64 products per
  * second, full chip), the roofline denominator for the multiply kernels. */

@@ -623,6 +623,95 @@ def bks(variant: int, f, g, umul=convolve_exact):
     raise ValueError("variant must be 1..4")
 
 
+def bks_mod(variant: int, f, g, n: int, umul=None):
+    """bipoly.py:177-278 with ring_zmod(n) (bipoly.py:59-72): the same steps
+    as ``bks`` in the ring's arithmetic -- additions and subtractions mod n,
+    halving a * (n+1)/2 mod n (odd n only; bipoly.py:64-66, MissingHalveError
+    :116-118) -- with the reference's default UniMul (uni_schoolbook over the
+    ring, oracle.py:58-69) unless ``umul`` is given.  Inputs are ring elements
+    (reduced mod n here, as the ring's own ops would)."""
+    if n < 2:
+        raise ValueError("modulus must be >= 2")
+    lx, ly = len(f), len(f[0])
+    if len(g) != lx or len(g[0]) != ly:
+        raise ValueError("inputs must share both lengths")
+    if variant in (3, 4) and n % 2 == 0:
+        raise ValueError("MissingHalveError: ring does not support exact halving")
+    f = [[c % n for c in row] for row in f]
+    g = [[c % n for c in row] for row in g]
+    inv2 = (n + 1) // 2
+
+    def hv(a):
+        return (a * inv2) % n
+
+    def mul(a, b):
+        if umul is not None:
+            return [c % n for c in umul(a, b)]
+        out = [0] * (len(a) + len(b) - 1)
+        for i, x in enumerate(a):
+            for j, y in enumerate(b):
+                out[i + j] = (out[i + j] + (x * y) % n) % n
+        return out
+
+    def cat(chunks, spacing, chunk_len, reverse=False, alternate=False):
+        v = _concat(chunks, spacing, chunk_len, reverse, alternate)
+        return [c % n for c in v]
+
+    def recover(fwd, rev, count, spacing, chunk_len):
+        fwd, rev = list(fwd), list(rev)
+        out = []
+        low = min(spacing, chunk_len)
+        for k in range(count):
+            fpos, rpos = k * spacing, (count - 1 - k) * spacing
+            chunk = fwd[fpos:fpos + low]
+            if chunk_len > spacing:
+                chunk += rev[rpos + spacing:rpos + chunk_len]
+            for t, c in enumerate(chunk):
+                fwd[fpos + t] = (fwd[fpos + t] - c) % n
+                rev[rpos + t] = (rev[rpos + t] - c) % n
+            out.append(chunk)
+        return out
+
+    cf, cg = _ychunks(f), _ychunks(g)
+    if variant == 1:
+        sp = 2 * lx - 1
+        return _from_ychunks(_split(mul(cat(cf, sp, lx), cat(cg, sp, lx)), sp, 2 * lx - 1, 2 * ly - 1))
+    if variant == 2:
+        pf = mul(cat(cf, lx, lx), cat(cg, lx, lx))
+        pr = mul(cat(cf, lx, lx, reverse=True), cat(cg, lx, lx, reverse=True))
+        return _from_ychunks(recover(pf, pr, 2 * ly - 1, lx, 2 * lx - 1))
+    if variant == 3:
+        pp = mul(cat(cf, lx, lx), cat(cg, lx, lx))
+        pn = mul(cat(cf, lx, lx, alternate=True), cat(cg, lx, lx, alternate=True))
+        ev = [hv((a + c) % n) for a, c in zip(pp, pn)]
+        od = [hv((a - c) % n) for a, c in zip(pp, pn)][lx:]
+        chunks = [None] * (2 * ly - 1)
+        chunks[0::2] = _split(ev, 2 * lx, 2 * lx - 1, ly)
+        chunks[1::2] = _split(od, 2 * lx, 2 * lx - 1, ly - 1)
+        return _from_ychunks(chunks)
+    if variant == 4:
+        if lx == 1 and ly == 1:
+            return [[mul([f[0][0]], [g[0][0]])[0]]]
+        h = (lx + 1) // 2
+
+        def points(ch):
+            return (cat(ch, h, lx), cat(ch, h, lx, alternate=True),
+                    cat(ch, h, lx, reverse=True), cat(ch, h, lx, reverse=True, alternate=True))
+        pa, pb = points(cf), points(cg)
+        pp, pn, prp, prn = (mul(x, y) for x, y in zip(pa, pb))
+        fe = [hv((a + c) % n) for a, c in zip(pp, pn)]
+        fo = [hv((a - c) % n) for a, c in zip(pp, pn)][h:]
+        re_ = [hv((a + c) % n) for a, c in zip(prp, prn)]
+        ro = [hv((a - c) % n) for a, c in zip(prp, prn)][h:]
+        even = recover(fe, re_, ly, 2 * h, 2 * lx - 1)
+        odd = recover(fo, ro, ly - 1, 2 * h, 2 * lx - 1) if ly > 1 else []
+        chunks = [None] * (2 * ly - 1)
+        chunks[0::2] = even
+        chunks[1::2] = odd
+        return _from_ychunks(chunks)
+    raise ValueError("variant must be 1..4")
+
+
 def schoolbook_bivar(f, g):
     """oracle.py:43-55 over Z."""
     lx, ly = len(f), len(f[0])

@@ -7,7 +7,7 @@ include/kmx.h).  Variant names follow the reference (ksint.py:8-12):
 ks2 = reciprocal (2^N, 2^-N), ks3 = negated (+-2^N).
 """
 from ._lib import ReconstructionError
-from .batch import BksBatch, KsBatch, bks_mul_host, imad_peak, ks_mul_host, mul_engine, tc_peak
+from .batch import BksBatch, BksModBatch, KsBatch, bks_mul_host, imad_peak, ks_mul_host, mul_engine, tc_peak
 from .bipoly import (BiPoly, MissingHalveError, RingOps, bks_four, bks_negated, bks_reciprocal,
                      bks_standard, ring_z, ring_zmod)
 from .modpoly import (DEFAULT_THRESHOLDS, GPU_THRESHOLDS, AutoThresholds, ModMulBatch, ModPoly, Variant,
@@ -21,7 +21,7 @@ __all__ = [
     "CoeffVec", "KsParams", "OverlapDigits", "MulStats", "MulConfig", "DEFAULT_MUL_CONFIG",
     "ReconstructionError", "derive_params", "ks1_mul", "ks2_mul", "ks3_mul", "ks4_mul",
     "reconstruct_overlapped", "BiPoly", "RingOps", "MissingHalveError", "ring_z", "ring_zmod",
-    "bks_standard", "bks_reciprocal", "bks_negated", "bks_four", "KsBatch", "BksBatch",
+    "bks_standard", "bks_reciprocal", "bks_negated", "bks_four", "KsBatch", "BksBatch", "BksModBatch",
     "ks_mul_host", "bks_mul_host", "imad_peak", "tc_peak", "mul_engine", "__version__",
     "ModPoly", "Variant", "AutoThresholds", "DEFAULT_THRESHOLDS", "GPU_THRESHOLDS", "choose_variant",
     "mod_mul", "ModMulBatch", "mod_mul_host",

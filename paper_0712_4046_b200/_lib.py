@@ -62,6 +62,9 @@ _SIGS = {
     "kmx_mod_workspace_bytes": (_sz, [_i, _i, _i, _i, ctypes.c_uint64]),
     "kmx_mod_mul": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "kmx_mod_mul_host": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp, _u64p]),
+    "kmx_bks_mod_workspace_bytes": (_sz, [_i, _i, _i, _i, ctypes.c_uint64]),
+    "kmx_bks_mod_mul": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "kmx_bks_mod_mul_host": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp]),
     "kmx_imad_peak": (ctypes.c_double, [_i]),
     "kmx_tc_peak": (ctypes.c_double, [_i]),
     "kmx_mul_engine": (_i, [_i, _i, _i, _i, _u]),

@@ -179,6 +179,38 @@ def bks_mul_host(variant: int, f: np.ndarray, g: np.ndarray, coeff_bits: int, ou
     return out
 
 
+class BksModBatch:
+    """Batched bivariate reduction over Z/nZ on device tensors: f, g int64
+    [batch, lx, ly] holding u64 residues in [0, n) -> h [batch, 2lx-1, 2ly-1]
+    (u64 residues in int64 storage).  Variants 3 and 4 need odd n."""
+
+    def __init__(self, variant: int, batch: int, lx: int, ly: int, modulus: int, device=None):
+        torch = _torch()
+        self.variant, self.batch, self.lx, self.ly, self.modulus = variant, batch, lx, ly, modulus
+        self.ws_bytes = lib().kmx_bks_mod_workspace_bytes(variant, batch, lx, ly, modulus)
+        if self.ws_bytes == 0:
+            raise ValueError("invalid bivariate Z/nZ problem (shape, modulus, or even n for variants 3/4)")
+        self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        self.workspace = torch.empty(self.ws_bytes, dtype=torch.uint8, device=self.device)
+
+    def __call__(self, f, g, out=None, stream=None):
+        torch = _torch()
+        assert f.dtype == torch.int64 and g.dtype == torch.int64 and f.is_contiguous() and g.is_contiguous()
+        if out is None:
+            out = torch.empty((self.batch, 2 * self.lx - 1, 2 * self.ly - 1), dtype=torch.int64, device=self.device)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        rc = lib().kmx_bks_mod_mul(self.variant, self.batch, self.lx, self.ly, self.modulus, f.data_ptr(),
+                                   g.data_ptr(), out.data_ptr(), self.workspace.data_ptr(), self.ws_bytes,
+                                   st.cuda_stream)
+        check(rc, "kmx_bks_mod_mul")
+        return out
+
+    def status(self, stream=None):
+        torch = _torch()
+        st = stream if stream is not None else torch.cuda.current_stream(self.device)
+        check(lib().kmx_ws_status(self.workspace.data_ptr(), st.cuda_stream), "kmx_bks_mod_mul")
+
+
 def imad_peak(iters: int = 4096) -> float:
     """Measured IMAD.WIDE.U32 products/s on the current device."""
     return float(lib().kmx_imad_peak(iters))

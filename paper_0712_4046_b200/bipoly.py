@@ -4,11 +4,12 @@ Mirrors pkg/src/kronmul/bipoly.py: BiPoly (:75-97), RingOps (:31-44),
 ring_z (:53-56), ring_zmod (:59-72), MissingHalveError (:26-28) and
 bks_standard / bks_reciprocal / bks_negated / bks_four (:177-278).
 
-With ring_z() and the default univariate multiplier, the whole reduction
-(evaluation, univariate products, half-sums and overlap recovery) runs in
-libkmx.so.  Other rings (ring_zmod) and custom univariate multipliers are the
-next rows of SURVEY.md §8(f) and raise NotImplementedError here -- never a
-silent CPU path.
+With ring_z() or ring_zmod(n) and the default univariate multiplier, the
+whole reduction (evaluation, univariate products, half-sums and overlap
+recovery) runs in libkmx.so: over Z through kmx_bks_mul (int32 coefficients,
+int64 products), over Z/nZ through kmx_bks_mod_mul (u64 residues; the
+univariate products go through the integer KS path, kmx_mod_mul).  Custom
+univariate multipliers raise NotImplementedError -- never a silent CPU path.
 """
 from __future__ import annotations
 
@@ -44,6 +45,7 @@ class RingOps:
     eq: Callable[[Any, Any], bool]
     halve: Optional[Callable[[Any], Any]] = None
     name: str = ""
+    modulus: int = 0
 
 
 def _halve_int(a: int) -> int:
@@ -67,7 +69,7 @@ def ring_zmod(n: int) -> RingOps:
         inv2 = (n + 1) // 2
         halve = lambda a: (a * inv2) % n  # noqa: E731
     return RingOps(zero=0, add=lambda a, b: (a + b) % n, sub=lambda a, b: (a - b) % n,
-                   neg=lambda a: (-a) % n, eq=operator.eq, halve=halve, name=f"Z/{n}")
+                   neg=lambda a: (-a) % n, eq=operator.eq, halve=halve, name=f"Z/{n}", modulus=n)
 
 
 @dataclass(frozen=True)
@@ -105,12 +107,22 @@ def _bks(variant: int, f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None,
     _check_shapes(f, g)
     if needs_halve and ring.halve is None:
         raise MissingHalveError("ring does not support exact halving")
-    if ring.name != "Z":
-        raise NotImplementedError("GPU bivariate path covers R = Z (ring_z); "
-                                  "Z/nZ is a next row (SURVEY.md §8(f) #4)")
     if mul is not None:
         raise NotImplementedError("custom univariate multipliers are not routed through the GPU path")
     lx, ly = f.lx, f.ly
+    if ring.modulus:
+        n = ring.modulus
+        if n.bit_length() > 64:
+            raise NotImplementedError("GPU Z/nZ path covers word-sized moduli (n < 2^64)")
+        # ring elements as residues in [0, n) (the ring's own normalisation, bipoly.py:67-71)
+        fu = np.array([[int(c) % n for c in row] for row in f.coeffs], dtype=np.uint64)
+        gu = np.array([[int(c) % n for c in row] for row in g.coeffs], dtype=np.uint64)
+        h = np.zeros((2 * lx - 1, 2 * ly - 1), dtype=np.uint64)
+        rc = lib().kmx_bks_mod_mul_host(variant, 1, lx, ly, n, _lib.ptr(fu), _lib.ptr(gu), _lib.ptr(h))
+        check(rc, "bks")
+        return BiPoly(tuple(tuple(int(v) for v in row) for row in h))
+    if ring.name != "Z":
+        raise NotImplementedError("GPU bivariate path covers R = Z (ring_z) and R = Z/nZ (ring_zmod)")
     fa = np.asarray(f.coeffs, dtype=object)
     ga = np.asarray(g.coeffs, dtype=object)
     mx = max(max(abs(int(c)) for c in fa.reshape(-1)), max(abs(int(c)) for c in ga.reshape(-1)))

@@ -80,3 +80,38 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def main_bivar():
+    """bks_* over ring_zmod(n) with the reference's default UniMul
+    (uni_schoolbook over the ring, bipoly.py:121-125)."""
+    rng = random.Random(20261021)
+    BV = {1: K.bks_standard, 2: K.bks_reciprocal, 3: K.bks_negated, 4: K.bks_four}
+    cases = []
+    for n in (7, 1009, 65537, (1 << 61) - 1, (1 << 64) - 59, 2, 16, 1 << 40):
+        ring = K.ring_zmod(n)
+        for i in range(6):
+            lx, ly = rng.randrange(1, 9), rng.randrange(1, 9)
+            if i == 0:
+                lx = ly = 1
+            f = [[rng.randrange(n) for _ in range(ly)] for _ in range(lx)]
+            g = [[rng.randrange(n) for _ in range(ly)] for _ in range(lx)]
+            F, G = K.BiPoly(tuple(map(tuple, f))), K.BiPoly(tuple(map(tuple, g)))
+            outs = {}
+            for v, fn in BV.items():
+                try:
+                    outs[v] = [list(r) for r in fn(F, G, ring).coeffs]
+                except K.MissingHalveError:
+                    outs[v] = None
+            ok = [o for o in outs.values() if o is not None]
+            assert all(o == ok[0] for o in ok)
+            cases.append({"n": str(n), "f": [[str(c) for c in r] for r in f], "g": [[str(c) for c in r] for r in g],
+                          "h": [[str(c) for c in r] for r in ok[0]],
+                          "missing_halve": [v for v, o in outs.items() if o is None]})
+    with gzip.open(os.path.join(HERE, "bivar_mod_golden.json.gz"), "wt") as fh:
+        json.dump(cases, fh)
+    print("bivar mod cases:", len(cases))
+
+
+if __name__ == "__main__" and "--bivar" in sys.argv:
+    main_bivar()

@@ -51,3 +51,11 @@ def mod_golden():
         cases.append((c["tag"], [int(x) for x in c["f"]], [int(x) for x in c["g"]], int(c["n"]),
                       [int(x) for x in c["h"]], c.get("limb_products_classical")))
     return cases, [tuple(r) for r in d["choose_variant"]]
+
+
+def bivar_mod_cases():
+    out = []
+    for c in _load("bivar_mod_golden.json.gz"):
+        out.append((int(c["n"]), [[int(x) for x in r] for r in c["f"]], [[int(x) for x in r] for r in c["g"]],
+                    [[int(x) for x in r] for r in c["h"]], c["missing_halve"]))
+    return out
