@@ -33,6 +33,24 @@ int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
 // that the integer-pipe schoolbook is faster (config-5 sweep with KMX_TC=0 vs
 // default: the crossover sits at 134..145 limbs).  KMX_TC=0 forces the
 // integer pipe, KMX_TC=1 the tensor cores wherever supported.
+}  // namespace
+namespace kmx {
+// chunked single-tile tensor-core multiply (kmx_tcj.cu)
+bool tcj_plan(int ma, int mb, double* cost);
+cudaError_t launch_tcmulj(const MulArgs& a, cudaStream_t st);
+}  // namespace kmx
+namespace {
+
+// KMX_TCJ=1 selects the chunked single-tile kernel (kmx_tcj.cu) for every
+// tensor-core product whose shape it admits.  Opt-in: bit-exact, but slower
+// than the tiled kernel at the BASELINE shapes so far (c2 ks4 K2 0.18-0.33 ms
+// vs 0.117 ms; profiles/r01_tcj_sweep_c2.json).
+bool use_tcj(int ma, int mb) {
+  const char* v = getenv("KMX_TCJ");
+  if (!(v && *v && atoi(v) == 1)) return false;
+  return tcj_plan(ma, mb, nullptr);
+}
+
 bool use_tensor_mul(int ma, int mb) {
   const char* v = getenv("KMX_TC");
   const int force = v && *v ? atoi(v) : -1;
@@ -303,7 +321,9 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
   ma.counter = (int*)(err + 1);
   prof_begin(1, st);
-  if (tc) {
+  if (tc && !fuse && use_tcj(p.mf, p.mg)) {
+    if ((e = launch_tcmulj(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  } else if (tc) {
     if ((e = launch_tcmul(ma, st, fuse ? &pa : nullptr, p.P)) != cudaSuccess) return KMX_ECUDA;
   } else {
     if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;

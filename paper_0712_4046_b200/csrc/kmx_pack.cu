@@ -2,6 +2,8 @@
 // coefficient vectors at +-2^N, +-2^-N (pack.py:62-110, bignat._pack_ints
 // bignat.py:411-428), one block per (pair, pack op); the per-operand body is
 // pack_op in kmx_pack.cuh (shared with the fused tensor-core prologue).
+#include <cstdlib>
+
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
 #include "kmx_pack.cuh"
@@ -15,7 +17,28 @@ __global__ void __launch_bounds__(PK_T) k_pack(PackArgs A) {
   pack_op<STAGED>(A, pair, blockIdx.x - pair * A.nops, pk_sc, nullptr);
 }
 
+// ops (2q, 2q+1) = (pack, pack_negated) or (pack_reversed, pack_negated_reversed)
+__global__ void __launch_bounds__(PK_T) k_pack_pair(PackArgs A) {
+  extern __shared__ u32 pk_sc[];
+  const int npairs = A.nops / 2;
+  const int pair = blockIdx.x / npairs;
+  const int q = blockIdx.x - pair * npairs;
+  pack_pair(A, pair, 2 * q, 2 * q + 1, pk_sc);
+}
+
+static bool pairable(const PackArgs& a) {
+  if (a.nops < 4 || (a.nops & 1)) return false;
+  for (int q = 0; 2 * q + 1 < a.nops; q++) {
+    const PackOp &x = a.op[2 * q], &y = a.op[2 * q + 1];
+    if ((x.kind & 1) || y.kind != (x.kind | 1) || x.coeffs != y.coeffs || x.len != y.len ||
+        x.coeff_pair_stride != y.coeff_pair_stride)
+      return false;
+  }
+  return true;
+}
+
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
+  static const int use_pair = getenv("KMX_PACK_PAIR") ? atoi(getenv("KMX_PACK_PAIR")) : 1;
   int mmax = 0;
   for (int i = 0; i < a.nops; i++) mmax = a.op[i].m > mmax ? a.op[i].m : mmax;
   int T = ((mmax + PK_V - 1) / PK_V + 31) & ~31;  // sized to the operand
@@ -27,6 +50,16 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   const int nw = (lmax + PK_PAD) * a.in_words;
   b.stage = nw <= PK_STAGE_WORDS;
   const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;
+  // paired packs halve the block count: only when that still fills the chip
+  // (c1, 64 pairs: 256 paired blocks are slower than 512 single ones)
+  if (b.stage && use_pair && pairable(a) && (use_pair > 1 || (long long)batch * (a.nops / 2) >= 148LL * 8)) {
+    if (smem > 44 * 1024) {
+      cudaError_t e = cudaFuncSetAttribute(k_pack_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    k_pack_pair<<<batch * (a.nops / 2), T, smem, st>>>(b);
+    return cudaGetLastError();
+  }
   if (b.stage) {
     if (smem > 44 * 1024) {  // + static shared memory must fit the opt-in limit
       cudaError_t e = cudaFuncSetAttribute(k_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

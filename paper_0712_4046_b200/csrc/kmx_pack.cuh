@@ -327,5 +327,210 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
   }
 }
 
+// ------------------------------------------------------------------------
+// pack_pair: the two packs that share a coefficient order -- value at +2^N
+// and at -2^N (ops o0: kind 0 or 2, o1: kind 1 or 3; pack.py:79-110) -- from
+// ONE staged copy of the vector: the even / odd bitstreams E, O are extracted
+// once per digit and feed both E + O (carries {0,1}) and |E - O| (sign from
+// the top-down warp compare), each with its own thread-level carry maps and
+// block scan.  Staged vectors only (the caller checks the size).
+// ------------------------------------------------------------------------
+__device__ __forceinline__ void pack_pair(const PackArgs& A, int pair, int o0, int o1, u32* pk_sc) {
+  __shared__ u32 sm_scan[2][PK_T / 32];
+  __shared__ int sm_order, sm_bad;
+  __shared__ unsigned long long sm_top[2];
+  __shared__ i64 sm_carry[2];
+  const int T = blockDim.x;
+  const int tid = threadIdx.x;
+  PackCtx<true> C;
+  const PackOp& P0 = A.op[o0];
+  const PackOp& P1 = A.op[o1];
+  C.cf = P0.coeffs + (long long)pair * P0.coeff_pair_stride;
+  u32* out0 = P0.out + (long long)pair * P0.out_pair_stride;
+  u32* out1 = P1.out + (long long)pair * P1.out_pair_stride;
+  const int m = P0.m > P1.m ? P0.m : P1.m;
+  C.L = P0.len; C.N = A.N; C.b = A.b; C.iw = A.in_words;
+  C.rev = (P0.kind & 2) != 0;
+  C.bias = A.bias != 0;
+  C.bmask = C.b >= 32 ? 0xffffffffu : ((1u << C.b) - 1u);
+  C.biasw = A.bias ? (1u << (C.b - 1)) : 0u;
+  const bool flip = (P1.kind == 3) && ((C.L & 1) == 0);  // pack.py:106-109
+  const bool validate = P0.validate != 0 || P1.validate != 0;
+  unsigned long long* prefix = P0.prefix ? P0.prefix : P1.prefix;
+  const long long pstride = P0.prefix ? P0.prefix_pair_stride : P1.prefix_pair_stride;
+  C.sc = pk_sc;
+  if (tid == 0) sm_bad = 0;
+  {
+    const int L = C.L, iw = C.iw, nw = L * iw;
+    __syncthreads();
+    bool bad = false;
+    auto put = [&](int x, u32 raw) {
+      const int i = iw == 1 ? x : x / iw, w = iw == 1 ? 0 : x - i * iw;
+      if (validate) {
+        if (C.bias) {
+          const int v = (int)raw;
+          if (C.b < 32) bad |= (v < -(1 << (C.b - 1))) || (v >= (1 << (C.b - 1)));
+        } else {
+          const int lo_bit = 32 * w;
+          if (lo_bit >= C.b) bad |= raw != 0u;
+          else if (C.b - lo_bit < 32) bad |= (raw >> (C.b - lo_bit)) != 0u;
+        }
+      }
+      const u32 v = C.bias ? ((raw + C.biasw) & C.bmask) : raw;
+      const int p = C.rev ? L - 1 - i : i;
+      pk_sc[p * iw + w] = v;
+    };
+    if ((nw & 3) == 0 && (reinterpret_cast<uintptr_t>(C.cf) & 15) == 0) {
+      const uint4* s4 = reinterpret_cast<const uint4*>(C.cf);
+#pragma unroll 4
+      for (int x4 = tid; x4 < nw / 4; x4 += T) {
+        const uint4 r = __ldg(s4 + x4);
+        put(4 * x4, r.x);
+        put(4 * x4 + 1, r.y);
+        put(4 * x4 + 2, r.z);
+        put(4 * x4 + 3, r.w);
+      }
+    } else {
+#pragma unroll 4
+      for (int x = tid; x < nw; x += T) put(x, __ldg(C.cf + x));
+    }
+    for (int x = nw + tid; x < (L + PK_PAD) * iw; x += T) pk_sc[x] = 0u;
+    if (bad) sm_bad = 1;
+    __syncthreads();
+    if (tid == 0 && sm_bad) raise_err(A.err, ERR_INVAL);
+    if (prefix) block_prefix_staged(pk_sc, L, C.rev, prefix + (long long)pair * pstride);
+  }
+  if (tid == 0) { sm_top[0] = sm_top[1] = 0ull; sm_order = 1; sm_carry[0] = sm_carry[1] = 0; }
+  const int S = 2 * C.N;
+  if (tid < 32) {  // order of E and O from the most significant differing digit
+    int order = 0;
+    for (int base = m - 1; base >= 0 && order == 0; base -= 32) {
+      const int q = base - tid;
+      u32 e = 0u, ov = 0u;
+      if (q >= 0) {
+        StreamCur ce, co;
+        ce.init(q, 0, S);
+        co.init(q, C.N, S);
+        e = ce.bits(C, 0, S);
+        ov = co.bits(C, 1, S);
+      }
+      const unsigned diff = __ballot_sync(0xffffffffu, e != ov);
+      if (diff) {
+        const int l = __ffs(diff) - 1;
+        const int gt = __shfl_sync(0xffffffffu, e > ov ? 1 : 0, l);
+        order = gt ? 1 : -1;
+      }
+    }
+    if (tid == 0) sm_order = order >= 0 ? 1 : -1;
+  }
+  __syncthreads();
+  const int order = sm_order;
+  const int negative = (order < 0) != flip ? 1 : 0;
+  int top0 = 0, top1 = 0;
+  u32 topv0 = 0u, topv1 = 0u;
+  for (int c0 = 0; c0 < m; c0 += T * PK_V) {
+    const int q0 = c0 + tid * PK_V;
+    StreamCur ce, co;
+    ce.init(q0, 0, S);
+    co.init(q0, C.N, S);
+    u32 d0[PK_V], d1[PK_V];
+    int k0 = 0, k1 = 0;
+    u32 f0 = 0xffffffffu, a0 = 0u, f1 = 0xffffffffu, a1 = 0u;
+#pragma unroll
+    for (int v = 0; v < PK_V; v++) {
+      u32 e = 0u, ov = 0u;
+      if (q0 + v < m) {
+        e = ce.bits(C, 0, S);
+        ov = co.bits(C, 1, S);
+      }
+      ce.next(S);
+      co.next(S);
+      const i64 x0 = (i64)e + ov + k0;
+      const i64 x1 = (order > 0 ? (i64)e - ov : (i64)ov - e) + k1;
+      d0[v] = (u32)x0;
+      k0 = (int)(x0 >> 32);
+      d1[v] = (u32)x1;
+      k1 = (int)(x1 >> 32);
+      f0 &= d0[v]; a0 |= d0[v];
+      f1 &= d1[v]; a1 |= d1[v];
+    }
+    // thread carry maps (c0 - all0, c0, c0 + allF), one block scan per stream
+    const u32 M0 = (u32)(k0 - (a0 == 0u ? 1 : 0) + 1) | ((u32)(k0 + 1) << 2) |
+                   ((u32)(k0 + (f0 == 0xffffffffu ? 1 : 0) + 1) << 4);
+    const u32 M1 = (u32)(k1 - (a1 == 0u ? 1 : 0) + 1) | ((u32)(k1 + 1) << 2) |
+                   ((u32)(k1 + (f1 == 0xffffffffu ? 1 : 0) + 1) << 4);
+    u32 tot0, tot1;
+    const u32 e0 = cm_seg_scan(M0, T, sm_scan[0], &tot0);
+    const u32 e1 = cm_seg_scan(M1, T, sm_scan[1], &tot1);
+    const int cin0 = (int)sm_carry[0], cin1 = (int)sm_carry[1];
+    int r0 = cm_apply(e0, cin0), r1 = cm_apply(e1, cin1);
+    if (r0) {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++) {
+        const u32 old = d0[v];
+        d0[v] = old + (u32)r0;
+        r0 = r0 > 0 ? (d0[v] == 0u ? 1 : 0) : (r0 < 0 && old == 0u ? -1 : 0);
+      }
+    }
+    if (r1) {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++) {
+        const u32 old = d1[v];
+        d1[v] = old + (u32)r1;
+        r1 = r1 > 0 ? (d1[v] == 0u ? 1 : 0) : (r1 < 0 && old == 0u ? -1 : 0);
+      }
+    }
+#pragma unroll
+    for (int v = 0; v < PK_V; v++) {
+      if (q0 + v < P0.m && d0[v]) { top0 = q0 + v + 1; topv0 = d0[v]; }
+      if (q0 + v < P1.m && d1[v]) { top1 = q0 + v + 1; topv1 = d1[v]; }
+    }
+    if (q0 + PK_V <= P0.m) {
+      uint4* dst = reinterpret_cast<uint4*>(out0 + q0);
+      dst[0] = make_uint4(d0[0], d0[1], d0[2], d0[3]);
+      dst[1] = make_uint4(d0[4], d0[5], d0[6], d0[7]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++)
+        if (q0 + v < P0.m) out0[q0 + v] = d0[v];
+    }
+    if (q0 + PK_V <= P1.m) {
+      uint4* dst = reinterpret_cast<uint4*>(out1 + q0);
+      dst[0] = make_uint4(d1[0], d1[1], d1[2], d1[3]);
+      dst[1] = make_uint4(d1[4], d1[5], d1[6], d1[7]);
+    } else {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++)
+        if (q0 + v < P1.m) out1[q0 + v] = d1[v];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      sm_carry[0] = cm_apply(tot0, cin0);
+      sm_carry[1] = cm_apply(tot1, cin1);
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && (sm_carry[0] != 0 || sm_carry[1] != 0)) raise_err(A.err, ERR_INEXACT);
+  {
+    const unsigned w0 = __reduce_max_sync(0xffffffffu, (unsigned)top0);
+    const unsigned w1 = __reduce_max_sync(0xffffffffu, (unsigned)top1);
+    const u32 v0 = __shfl_sync(0xffffffffu, topv0, w0 ? __ffs(__ballot_sync(0xffffffffu, (unsigned)top0 == w0)) - 1 : 0);
+    const u32 v1 = __shfl_sync(0xffffffffu, topv1, w1 ? __ffs(__ballot_sync(0xffffffffu, (unsigned)top1 == w1)) - 1 : 0);
+    if ((tid & 31) == 0) {
+      if (w0) atomicMax(&sm_top[0], ((unsigned long long)w0 << 32) | v0);
+      if (w1) atomicMax(&sm_top[1], ((unsigned long long)w1 << 32) | v1);
+    }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    u32* meta0 = P0.meta + (long long)pair * P0.meta_pair_stride;
+    u32* meta1 = P1.meta + (long long)pair * P1.meta_pair_stride;
+    const int t0 = (int)(sm_top[0] >> 32), t1 = (int)(sm_top[1] >> 32);
+    meta0[0] = 0u;
+    meta0[1] = t0 ? (u32)(32 * (t0 - 1) + 32 - __clz((u32)sm_top[0])) : 0u;
+    meta1[0] = (u32)negative;
+    meta1[1] = t1 ? (u32)(32 * (t1 - 1) + 32 - __clz((u32)sm_top[1])) : 0u;
+  }
+}
 
 }  // namespace kmx
