@@ -342,14 +342,9 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = (long long)p.cnt_max * p.dwords;
   fa.dslots_pair = p.dslots; fa.err = err;
   fa.bias = bfix;
-  prof_begin(2, st);
-  if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
-  prof_end(2, st);
-  g_launches++;
-
+  ReconArgs ra;
+  memset(&ra, 0, sizeof ra);
   if (p.nrs) {
-    ReconArgs ra;
-    memset(&ra, 0, sizeof ra);
     for (int i = 0; i < p.nrs; i++) ra.s[i] = p.rs[i];
     ra.ns = p.nrs; ra.batch = p.batch; ra.W = p.W;
     ra.dbuf = dbuf; ra.dwords = p.dwords; ra.dslot_stride = (long long)p.cnt_max * p.dwords;
@@ -358,6 +353,22 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     ra.err = err;
     ra.bias = bfix;
     ra.diag = err + 2;
+    // ks2 / ks4: finish + reconstruct in one kernel (k_finrec) when both fit it
+    bool fused = false;
+    prof_begin(3, st);
+    if ((e = launch_finrec(fa, ra, p.batch, st, &fused)) != cudaSuccess) return KMX_ECUDA;
+    if (fused) {
+      prof_end(3, st);
+      g_launches++;
+      return KMX_OK;
+    }
+  }
+  prof_begin(2, st);
+  if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+  prof_end(2, st);
+  g_launches++;
+
+  if (p.nrs) {
     prof_begin(3, st);
     if ((e = launch_recon(ra, st)) != cudaSuccess) return KMX_ECUDA;
     prof_end(3, st);

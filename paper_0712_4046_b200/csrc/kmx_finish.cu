@@ -23,206 +23,20 @@
 
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
-#include "kmx_store.cuh"
+#include "kmx_finish.cuh"
 
 namespace kmx {
 
 namespace {
 
-constexpr int FW_WARPS = 4;
-constexpr int FW_V = 8;
-constexpr int FW_CH = 32 * FW_V;  // limbs per warp chunk
-
 __global__ void __launch_bounds__(32 * FW_WARPS, 8) k_finish_w(FinishArgs a, long long nstreams) {
   __shared__ __align__(16) u32 sbuf[FW_WARPS][FIN_HALO + FW_CH];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int wid = threadIdx.x >> 5;
   const long long gs = (long long)blockIdx.x * FW_WARPS + wid;
   if (gs >= nstreams) return;  // warp-uniform
-  u32* buf = sbuf[wid];
   const int pair = (int)(gs / a.ns);
   const int si = (int)(gs - (long long)pair * a.ns);
-  const Stream S = si == 0 ? a.s[0] : (si == 1 ? a.s[1] : (si == 2 ? a.s[2] : a.s[3]));
-  const long long zP = (long long)pair * a.nprod_pair + S.zP;
-  const u32* Pp = a.P + zP * a.p_stride;
-  const unsigned long long* spP = a.spill + zP * a.nbands * 2;
-  const u32* Qp = nullptr;
-  const unsigned long long* spQ = nullptr;
-  int sg = 0;
-  if (S.qsign) {
-    const long long zQ = (long long)pair * a.nprod_pair + S.zQ;
-    Qp = a.P + zQ * a.p_stride;
-    spQ = a.spill + zQ * a.nbands * 2;
-    const u32* mt = a.meta + (long long)pair * a.meta_per_pair;
-    const u32 ngt = mt[2 * S.qmeta] ^ mt[2 * (S.qmeta + a.mf_slot_stride)];  // mul_signed: xor
-    sg = ngt ? -S.qsign : S.qsign;
-  }
-  const long long off = S.off;
-  const int W = S.W;
-  const int Wd = (W + 31) >> 5;
-  const long long E = off + (long long)S.cnt * W;
-  const int lgC = 31 - __clz(a.band_cols);
-  const int cmask = (1 << lgC) - 1;
-  const int mp = a.mp;
-  int Qd = mp + 1;
-  const long long qe = (E + 31) / 32 + 1;
-  if (qe > Qd) Qd = (int)qe;
-  u32* hpair = a.h + (long long)pair * a.h_pair_stride;
-  u32* dslot = a.dbuf + ((long long)pair * a.dslots_pair + S.dslot) * a.dslot_stride;
-  buf[lane] = 0u;  // halo (FIN_HALO == 32)
-  i64 cin_chunk = 0;  // carry + hi of the previous chunk's top limb
-  bool bad = false;
-  for (int q00 = 0; q00 < Qd; q00 += FW_CH) {
-    const int q0 = q00 + lane * FW_V;
-    u32 lo[FW_V];
-    i64 hi[FW_V];
-    {
-      u32 pv[FW_V], qv[FW_V];
-      i64 s0 = 0, s1 = 0;
-      const bool full = q0 + FW_V <= mp;
-      const bool bstart = q0 > 0 && q0 < mp && (q0 & cmask) == 0;
-      const int bidx = (q0 >> lgC) - 1;
-      if (full) {
-        const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(Pp + q0));
-        const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(Pp + q0) + 1);
-        pv[0] = x0.x; pv[1] = x0.y; pv[2] = x0.z; pv[3] = x0.w; pv[4] = x1.x; pv[5] = x1.y; pv[6] = x1.z; pv[7] = x1.w;
-      } else {
-#pragma unroll
-        for (int v = 0; v < FW_V; v++) pv[v] = q0 + v < mp ? Pp[q0 + v] : 0u;
-      }
-      if (bstart) { s0 = (i64)spP[bidx * 2]; s1 = (i64)spP[bidx * 2 + 1]; }
-      if (sg) {
-        if (full) {
-          const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(Qp + q0));
-          const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(Qp + q0) + 1);
-          qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w; qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
-        } else {
-#pragma unroll
-          for (int v = 0; v < FW_V; v++) qv[v] = q0 + v < mp ? Qp[q0 + v] : 0u;
-        }
-        if (bstart) { s0 += sg * (i64)spQ[bidx * 2]; s1 += sg * (i64)spQ[bidx * 2 + 1]; }
-      }
-#pragma unroll
-      for (int v = 0; v < FW_V; v++) {
-        i64 y = (i64)pv[v];
-        if (sg > 0) y += (i64)qv[v];
-        else if (sg < 0) y -= (i64)qv[v];
-        if (v == 0) y += s0;
-        if (v == 1) y += s1;
-        lo[v] = (u32)y;
-        hi[v] = y >> 32;
-      }
-    }
-    i64 hprev = __shfl_up_sync(0xffffffffu, hi[FW_V - 1], 1);
-    if (lane == 0) hprev = cin_chunk;
-    const i64 hlast = __shfl_sync(0xffffffffu, hi[FW_V - 1], 31);
-    // local resolution with carry-in 0
-    u32 d[FW_V];
-    int c = 0;
-    u32 allF = 0xffffffffu, any = 0u;
-#pragma unroll
-    for (int v = 0; v < FW_V; v++) {
-      const i64 t = (i64)lo[v] + (v ? hi[v - 1] : hprev) + c;
-      d[v] = (u32)t;
-      c = (int)(t >> 32);
-      allF &= d[v];
-      any |= d[v];
-    }
-    const int f1 = allF == 0xffffffffu ? 1 : 0, z1 = any == 0u ? 1 : 0;
-    // carry map: cin -1 -> c - all0, 0 -> c, +1 -> c + allF  (6-bit cm_ encoding)
-    u32 inc = (u32)(c - z1 + 1) | ((u32)(c + 1) << 2) | ((u32)(c + f1 + 1) << 4);
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const u32 pm = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc = cm_compose(pm, inc);
-    }
-    u32 exc = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) exc = CM_IDENT;
-    const u32 tot = __shfl_sync(0xffffffffu, inc, 31);
-    int k = cm_apply(exc, 0);
-    if (k) {  // ripple the carry-in through this lane's digits
-#pragma unroll
-      for (int v = 0; v < FW_V; v++) {
-        const u32 old = d[v];
-        d[v] = old + (u32)k;
-        k = k > 0 ? (d[v] == 0u ? 1 : 0) : (k < 0 && old == 0u ? -1 : 0);
-      }
-    }
-    cin_chunk = (i64)cm_apply(tot, 0) + hlast;
-    // exactness checks (bits below off, bits at or above E), chunk-uniform branch
-    if (32LL * q00 < off || 32LL * (q00 + FW_CH) > E) {
-#pragma unroll
-      for (int v = 0; v < FW_V; v++) {
-        const long long bit0 = 32LL * (q0 + v);
-        if (bit0 < off) {
-          const long long nb = off - bit0;
-          const u32 msk = nb >= 32 ? 0xffffffffu : ((1u << nb) - 1u);
-          bad |= (d[v] & msk) != 0u;
-        }
-        if (bit0 + 32 > E && q0 + v < Qd) {
-          const long long from = E - bit0;
-          const u32 msk = from <= 0 ? 0xffffffffu : (0xffffffffu << from);
-          bad |= (d[v] & msk) != 0u;
-        }
-      }
-    }
-    uint4* b4 = reinterpret_cast<uint4*>(buf + FIN_HALO + lane * FW_V);
-    b4[0] = make_uint4(d[0], d[1], d[2], d[3]);
-    b4[1] = make_uint4(d[4], d[5], d[6], d[7]);
-    __syncwarp();
-    // digits whose top bit falls inside this chunk
-    const long long clo = 32LL * q00, chi = 32LL * (q00 + FW_CH);
-    const long long t = clo - off + 1;
-    long long jl = t <= 0 ? 0 : (t + W - 1) / W - 1;
-    if (jl < 0) jl = 0;
-    const long long u = chi - off;
-    long long jh = u <= 0 ? 0 : u / W;
-    if (jh > S.cnt) jh = S.cnt;
-    const long long base = off - 32LL * (q00 - FIN_HALO);
-    for (long long j = jl + lane; j < jh; j += 32) {
-      const long long lb = base + j * W;
-      if (S.mode == 0) {
-        const long long kpos = S.pos0 + j * S.pstride;
-        u32* dst = hpair + kpos * a.out_words;
-        if (a.bias.enabled) {
-          unsigned __int128 hp = 0;
-          for (int w = 0; w < Wd && w < 4; w++) {
-            u32 x = bits32(buf, FIN_HALO + FW_CH, lb + 32 * w);
-            const int rem = W - 32 * w;
-            if (rem < 32) x &= (1u << rem) - 1u;
-            hp |= (unsigned __int128)x << (32 * w);
-          }
-          store_coeff128(dst, a.out_words, hp, kpos, a.bias, pair);
-          continue;
-        }
-        for (int w = 0; w < a.out_words; w++) {
-          u32 x = 0u;
-          if (w < Wd) {
-            x = bits32(buf, FIN_HALO + FW_CH, lb + 32 * w);
-            const int rem = W - 32 * w;
-            if (rem < 32) x &= (1u << rem) - 1u;
-          }
-          dst[w] = x;
-        }
-      } else {
-        const long long idx = S.reversed ? (S.cnt - 1 - j) : j;
-        u32* dst = dslot + idx * a.dwords;
-        for (int w = 0; w < a.dwords; w++) {
-          u32 x = 0u;
-          if (w < Wd) {
-            x = bits32(buf, FIN_HALO + FW_CH, lb + 32 * w);
-            const int rem = W - 32 * w;
-            if (rem < 32) x &= (1u << rem) - 1u;
-          }
-          dst[w] = x;
-        }
-      }
-    }
-    __syncwarp();
-    buf[lane] = buf[FW_CH + lane];
-    __syncwarp();
-  }
-  if (__any_sync(0xffffffffu, bad) && lane == 0) raise_err(a.err, ERR_INEXACT);
-  if (lane == 0 && cin_chunk != 0) raise_err(a.err, ERR_INEXACT);
+  finish_warp_stream(a, pair, si, sbuf[wid], GlobalDigitSink{&a});
 }
 
 }  // namespace

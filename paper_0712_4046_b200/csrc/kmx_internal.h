@@ -165,6 +165,9 @@ cudaError_t launch_mul(const MulArgs& a, cudaStream_t st);
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_recon(const ReconArgs& a, cudaStream_t st);
+// K3 + K4 fused for ks2 / ks4 when both apply (warp finish, staged
+// reconstruction); *used = false: nothing launched, run them separately
+cudaError_t launch_finrec(const FinishArgs& fa, const ReconArgs& ra, int batch, cudaStream_t st, bool* used);
 cudaError_t launch_bias(const BiasArgs& a, cudaStream_t st);
 double measure_imad_peak(int iters);
 

@@ -14,6 +14,7 @@
 #include "kmx_common.cuh"
 #include "kmx_internal.h"
 #include "kmx_store.cuh"
+#include "kmx_finish.cuh"
 
 namespace kmx {
 
@@ -963,6 +964,96 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
       bias_pass(a.bias, pair, a.h + (long long)pair * a.h_pair_stride, a.out_words, S.pos0, S.pstride, S.count,
                 threadIdx.x, blockDim.x);
     }
+  }
+}
+
+// ------------------------------------------------------------------------
+// K3 + K4 fused (ks2 / ks4): one CTA per (pair, reconstruction stream).
+// Warps 0 and 1 run the warp finish (kmx_finish.cuh) of the stream's forward
+// and reversed digit streams straight into the padded shared-memory copy
+// that k_recon_par would stage from the digit buffer; then the whole CTA
+// reconstructs.  The digit streams never round-trip through global memory
+// and one launch (plus its tail) disappears.
+// ------------------------------------------------------------------------
+template <int NW>
+__global__ void __launch_bounds__(RECON_PAR_MAXT) k_finrec(FinishArgs fa, ReconArgs a, int4 fsel) {
+  __shared__ u32 smw[2 * 17 * 32];
+  __shared__ int smi[64];
+  __shared__ uint8_t dend[RECON_PAR_MAXT];
+  __shared__ int fallback;
+  __shared__ __align__(16) u32 fbuf[2][FIN_HALO + FW_CH];
+  extern __shared__ u32 rst[];
+  const int sid = blockIdx.x;
+  const int pair = sid / a.ns, si = sid - pair * a.ns;
+  const ReconStream S = si == 0 ? a.s[0] : a.s[1];
+  const int nsteps = S.count - 1;
+  int lgV = 0;
+  while ((blockDim.x << lgV) < nsteps) lgV++;  // as k_recon_par
+  const int V = 1 << lgV;
+  const int dw = a.dwords;
+  const int slot = dpos(S.count + 1, dw, lgV) + 1;  // as stage_stream
+  const int warp = threadIdx.x >> 5;
+  if (warp < 2) {
+    // fsel: finish-stream indices of (stream 0 fwd, stream 0 rev, stream 1 fwd, stream 1 rev)
+    const int fs = si == 0 ? (warp == 0 ? fsel.x : fsel.y) : (warp == 0 ? fsel.z : fsel.w);
+    finish_warp_stream(fa, pair, fs, fbuf[warp], SmemDigitSink{warp == 0 ? rst : rst + slot, dw, lgV});
+  }
+  BiasFix bfx = a.bias;
+  if (a.bias.enabled && a.bias_smem) stage_prefix(rst + 2 * slot, bfx, pair, lgV, S.pstride, threadIdx.x, blockDim.x);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncthreads();
+  recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback);
+}
+
+template <int NW>
+static cudaError_t launch_finrec_t(const FinishArgs& fa, const ReconArgs& a, int4 fsel, int maxcount, cudaStream_t st,
+                                   bool* used) {
+  const int nsteps = maxcount > 1 ? maxcount - 1 : 1;
+  int T = (nsteps + 7) / 8;
+  T = ((T + 31) / 32) * 32;
+  if (T < 64) T = 64;  // warps 0 and 1 finish the two digit streams
+  if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;
+  ReconArgs b = a;
+  static const int bias_smem = getenv("KMX_RECON_BIAS_SMEM") ? atoi(getenv("KMX_RECON_BIAS_SMEM")) : 1;
+  b.bias_smem = bias_smem;
+  b.stage = 1;
+  size_t smem = (size_t)(2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4) * sizeof(u32);
+  if (a.bias.enabled && bias_smem) smem += (size_t)(4 * (a.bias.lf + a.bias.lg + 2) + 4) * sizeof(u32);
+  if (smem > 160 * 1024) return cudaSuccess;  // not used: too long to stage
+  if (smem > 32 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_finrec<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_finrec<NW><<<a.batch * a.ns, T, smem, st>>>(fa, b, fsel);
+  *used = true;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finrec(const FinishArgs& fa, const ReconArgs& a, int batch, cudaStream_t st, bool* used) {
+  *used = false;
+  // opt-in (KMX_FINREC=1): bit-exact, but the separate kernels keep more warps
+  // in flight -- fused is 0.76-1.03x of them over config 5 and 0.86x on c2 ks4
+  static const int en = getenv("KMX_FINREC") ? atoi(getenv("KMX_FINREC")) : 0;
+  if (!en || a.carries || a.sequential || !finish_use_warp(fa, batch)) return cudaSuccess;
+  int idx[4] = {-1, -1, -1, -1};
+  for (int i = 0; i < fa.ns; i++) {
+    if (fa.s[i].mode != 1 || fa.s[i].dslot < 0 || fa.s[i].dslot > 3) return cudaSuccess;
+    idx[fa.s[i].dslot] = i;
+  }
+  int4 fsel;
+  fsel.x = idx[a.s[0].fslot]; fsel.y = idx[a.s[0].rslot];
+  fsel.z = a.ns > 1 ? idx[a.s[1].fslot] : 0; fsel.w = a.ns > 1 ? idx[a.s[1].rslot] : 0;
+  if (fsel.x < 0 || fsel.y < 0 || fsel.z < 0 || fsel.w < 0) return cudaSuccess;
+  int maxcount = a.s[0].count;
+  if (a.ns > 1 && a.s[1].count > maxcount) maxcount = a.s[1].count;
+  switch (a.dwords) {
+    case 1: return launch_finrec_t<1>(fa, a, fsel, maxcount, st, used);
+    case 2: return launch_finrec_t<2>(fa, a, fsel, maxcount, st, used);
+    case 3: return launch_finrec_t<3>(fa, a, fsel, maxcount, st, used);
+    case 4: return launch_finrec_t<4>(fa, a, fsel, maxcount, st, used);
+    case 5: return launch_finrec_t<5>(fa, a, fsel, maxcount, st, used);
+    default: return cudaSuccess;  // wider digits: separate kernels
   }
 }
 

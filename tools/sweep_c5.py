@@ -89,6 +89,8 @@ def run_point(n, b, steps, warmup, scale, peaks, hbm, flush, dev):
         L.kmx_prof_enable(0)
         op.status()
         km = {nm: kern[i] / steps for i, nm in enumerate(["pack", "mul", "finish", "recon", "bias"]) if kern[i] > 0}
+        if "recon" in km and "finish" not in km:  # K3 + K4 fused (k_finrec)
+            km["finish+recon (fused)"] = km.pop("recon")
         prods = bench.algorithmic_products(cfg, v) * B
         eng = kmx.mul_engine(v, n, n, b)
         rec = {"products_per_s": B / (ms * 1e-3), "ms_per_step": ms, "kernel_ms": km, "mul_engine": eng,
@@ -101,7 +103,8 @@ def run_point(n, b, steps, warmup, scale, peaks, hbm, flush, dev):
         pu = bench.pack_unpack_bytes(cfg, v)
         if "pack" in km:
             rec["pack_hbm_frac"] = pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9 / hbm
-        rec["finish_hbm_frac"] = pu["finish_bytes"] / (km["finish"] * 1e-3) / 1e9 / hbm
+        fin_ms = km.get("finish", km.get("finish+recon (fused)"))
+        rec["finish_hbm_frac"] = pu["finish_bytes"] / (fin_ms * 1e-3) / 1e9 / hbm
         pt["variants"][bench.VNAME[v]] = rec
         outs[v] = out.clone()
         del op, graph, out
