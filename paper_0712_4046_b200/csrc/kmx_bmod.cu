@@ -153,7 +153,7 @@ int bmod_plan(BivarPlan& p, int variant, int batch, int lx, int ly, uint64_t n) 
 
 // KS variant for the univariate (Z/nZ)[x] products: the B200 AUTO bands
 // (paper_0712_4046_b200.modpoly.GPU_THRESHOLDS, from the config-5 sweep)
-int uni_variant(int Lu) { return Lu <= 256 ? 1 : (Lu <= 1024 ? 3 : 4); }
+int uni_variant(int Lu) { return Lu <= 64 ? 1 : (Lu <= 1024 ? 3 : 4); }
 
 struct BmodLayout { size_t ws_mod, off_ef, off_eg, off_pr, total; };
 

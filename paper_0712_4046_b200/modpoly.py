@@ -80,9 +80,10 @@ class AutoThresholds:
 
 DEFAULT_THRESHOLDS = AutoThresholds()
 # B200 bands from the config-5 sweep (tools/calibrate_auto.py over
-# profiles/r01_c5_sweep.json, coefficient widths 8..64 bits): the band edges
-# that minimise the time lost against the per-point fastest variant (1.4%).
-GPU_THRESHOLDS = AutoThresholds(ks1_max_length=256, ks3_max_length=1024)
+# profiles/r01_c5_sweep_final2.json, coefficient widths 8..64 bits): the band
+# edges that minimise the time lost against the per-point fastest variant
+# (2.1% mean loss).
+GPU_THRESHOLDS = AutoThresholds(ks1_max_length=64, ks3_max_length=1024)
 
 
 def choose_variant(length: int, coeff_bits: int, thresholds: AutoThresholds | None = None) -> Variant:
