@@ -36,19 +36,24 @@ int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
 }  // namespace
 namespace kmx {
 // chunked single-tile tensor-core multiply (kmx_tcj.cu)
-bool tcj_plan(int ma, int mb, double* cost);
+bool tcj_plan(int ma, int mb, double* cost, bool short_only);
 cudaError_t launch_tcmulj(const MulArgs& a, cudaStream_t st);
 }  // namespace kmx
 namespace {
 
-// KMX_TCJ=1 selects the chunked single-tile kernel (kmx_tcj.cu) for every
-// tensor-core product whose shape it admits.  Opt-in: bit-exact, but slower
-// than the tiled kernel at the BASELINE shapes so far (c2 ks4 K2 0.18-0.33 ms
-// vs 0.117 ms; profiles/r01_tcj_sweep_c2.json).
-bool use_tcj(int ma, int mb) {
+// The chunked single-tile kernel (kmx_tcj.cu) for short products (plan with
+// H0 <= 2, J >= 3) when the batch has too few products to fill the chip with
+// the tiled kernel's CTAs (< 4 per SM): one CTA per product with a K span
+// shortened by J is lower-latency there (c1 ks2/ks3 +9-11%, ks4 +8%), while
+// the tiled kernel keeps the edge on full batches (c2 ks4 K2 0.121 vs 0.129 ms)
+// and on long products (profiles/r01_tcj_sweep_*.json, c5 sweep).
+// KMX_TCJ=1 / 0 forces it on / off wherever its shape gate admits the product.
+bool use_tcj(int ma, int mb, long long nprod) {
   const char* v = getenv("KMX_TCJ");
-  if (!(v && *v && atoi(v) == 1)) return false;
-  return tcj_plan(ma, mb, nullptr);
+  const int force = v && *v ? atoi(v) : -1;
+  if (force == 0) return false;
+  if (force < 0 && nprod >= 4LL * 148) return false;
+  return tcj_plan(ma, mb, nullptr, force < 0);
 }
 
 bool use_tensor_mul(int ma, int mb) {
@@ -321,7 +326,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
   ma.counter = (int*)(err + 1);
   prof_begin(1, st);
-  if (tc && !fuse && use_tcj(p.mf, p.mg)) {
+  if (tc && !fuse && use_tcj(p.mf, p.mg, (long long)p.batch * p.P)) {
     if ((e = launch_tcmulj(ma, st)) != cudaSuccess) return KMX_ECUDA;
   } else if (tc) {
     if ((e = launch_tcmul(ma, st, fuse ? &pa : nullptr, p.P)) != cudaSuccess) return KMX_ECUDA;

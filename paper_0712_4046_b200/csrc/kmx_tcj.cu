@@ -97,11 +97,23 @@ __global__ void __launch_bounds__(32 * NW) k_tcmulj(TjArgs ta) {
   }
   {
     // a: zero-padded copy; b: J chunks of mBj limbs at pitch P, zero gaps
-    uint32_t* aw = reinterpret_cast<uint32_t*>(apad);
-    const int naw = ta.sa_bytes / 4, a0 = ta.apad / 4;
-    for (int w = tid; w < naw; w += THREADS) {
-      const int j = w - a0;
-      aw[w] = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
+    uint4* aw = reinterpret_cast<uint4*>(apad);
+    const int naq = ta.sa_bytes / 16, a0 = ta.apad / 4;
+    const bool al = (mA & 3) == 0 && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+    for (int w = tid; w < naq; w += THREADS) {
+      const int j = 4 * w - a0;
+      uint4 v = make_uint4(0u, 0u, 0u, 0u);
+      if (j >= 0 && j < mA) {
+        if (al) {
+          v = __ldg(reinterpret_cast<const uint4*>(Ag + j));
+        } else {
+          v.x = __ldg(Ag + j);
+          v.y = j + 1 < mA ? __ldg(Ag + j + 1) : 0u;
+          v.z = j + 2 < mA ? __ldg(Ag + j + 2) : 0u;
+          v.w = j + 3 < mA ? __ldg(Ag + j + 3) : 0u;
+        }
+      }
+      aw[w] = v;
     }
     uint32_t* bw = reinterpret_cast<uint32_t*>(bpad);
     const int nbw = ta.sb_bytes / 4, b0 = ta.bpad / 4, pw = ta.P / 4;
@@ -158,13 +170,19 @@ __global__ void __launch_bounds__(32 * NW) k_tcmulj(TjArgs ta) {
                           ((uint32_t)r0 << 12);
     const uint32_t* bw = reinterpret_cast<const uint32_t*>(bpad) + ta.bpad / 4;
     constexpr int NHB = 2 * (THREADS / 32 - 1);
+    const int HJ2 = 2 * HJ;
+    const uint32_t invH0 = (65536u + (uint32_t)H0 - 1u) / (uint32_t)H0;  // jq / H0 == (jq * invH0) >> 16 (jq < 256)
     for (int c = clo; c < chi; c++) {
       const int k = c - clo, st = k % NB;
       if (k >= NB) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((k / NB) - 1) & 1));
       unsigned char* bb = bring + (size_t)st * KC * STEPB;
       const int sb = c * KC;
       const int s0 = max(slo, sb), s1 = min(shi, sb + KC);
-      const int nitems = (s1 - s0) * 2 * HJ;
+      const int nitems = (s1 - s0) * HJ2;
+      // item it = sl * 2HJ + rem, decoded incrementally (no integer division)
+      int sl0 = 0, rem0 = hb, sl1 = 0, rem1 = hb + NHB;
+      while (rem0 >= HJ2) { rem0 -= HJ2; sl0++; }
+      while (rem1 >= HJ2) { rem1 -= HJ2; sl1++; }
       for (int ib = 0; ib < nitems; ib += 2 * NHB) {
         uint32_t wv[2];
         int doff[2];
@@ -173,14 +191,19 @@ __global__ void __launch_bounds__(32 * NW) k_tcmulj(TjArgs ta) {
         for (int x = 0; x < 2; x++) {
           const int it = ib + x * NHB + hb;
           valid[x] = it < nitems;
-          const int sl = valid[x] ? it / (2 * HJ) : 0;
-          const int rem = valid[x] ? it - sl * 2 * HJ : 0;
+          const int sl = x ? sl1 : sl0;
+          const int rem = x ? rem1 : rem0;
           const int kc = rem & 1, jq = rem >> 1;
-          const int jc = jq / H0, jj = jq - jc * H0;
+          const int jc = (int)(((uint32_t)jq * invH0) >> 16), jj = jq - jc * H0;
           const int u0 = ta.ulo + 32 * (s0 + sl);
           const int w0 = jc * ta.P + 128 * jj - u0 - 16 * kc - 16;
           wv[x] = bw[(w0 >> 2) + nl];
           doff[x] = (s0 + sl - sb) * STEPB + 256 * ((nl >> 3) + 2 * jq) + 128 * kc + 16 * (nl & 7);
+        }
+#pragma unroll
+        for (int x = 0; x < 2; x++) {  // advance both items by 2 NHB
+          if (x == 0) { rem0 += 2 * NHB; while (rem0 >= HJ2) { rem0 -= HJ2; sl0++; } }
+          else { rem1 += 2 * NHB; while (rem1 >= HJ2) { rem1 -= HJ2; sl1++; } }
         }
 #pragma unroll
         for (int x = 0; x < 2; x++) {
@@ -306,7 +329,7 @@ struct TjPlan {
 bool tj_geometry(int ma, int mb, int H0, int J, TjPlan& p) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
   const int N = 16 * H0 * J;
-  if (N > 256 || J < 1) return false;
+  if (N > env_tj("KMX_TCJ_NMAX", 128) || J < 1) return false;
   const int mBj = (mB + J - 1) / J;
   if ((J - 1) * mBj >= mB) return false;  // every chunk non-empty
   const int La = 4 * mA, Lbj = 4 * mBj;
@@ -320,7 +343,7 @@ bool tj_geometry(int ma, int mb, int H0, int J, TjPlan& p) {
   t.P = (Lbj + BMAX0 + 128 + 15) & ~15;
   t.bpad = (BMAX0 + 160 + 15) & ~15;
   t.apad = (AMAX + 32 + 64 + 15) & ~15;
-  t.sa_bytes = La + 2 * t.apad;
+  t.sa_bytes = ((La + 15) & ~15) + 2 * t.apad;
   t.sb_bytes = t.bpad + J * t.P + t.bpad;
   t.ulo = -32 * ((Lbj - 1 + 31) / 32);
   const int S = fdiv32(BMAX0 - t.ulo) + 1;
@@ -334,7 +357,7 @@ bool tj_geometry(int ma, int mb, int H0, int J, TjPlan& p) {
   t.NB = env_tj("KMX_TCJ_NB", 2);
   if (t.NB < 2) t.NB = 2;
   if (t.NB > TJ_MAXNB) t.NB = TJ_MAXNB;
-  t.KC = env_tj("KMX_TCJ_KC", N >= 256 ? 2 : (N >= 128 ? 4 : 8));
+  t.KC = env_tj("KMX_TCJ_KC", N >= 256 ? 4 : 8);
   size_t ring = (size_t)t.NB * t.KC * 32 * N;
   if (ring < (size_t)t.NL * 8) ring = (size_t)t.NL * 8;
   p.smem = r128(sizeof(TjShared)) + r128(t.sa_bytes) + r128(t.sb_bytes) + ring;
@@ -351,8 +374,11 @@ bool tj_geometry(int ma, int mb, int H0, int J, TjPlan& p) {
 
 }  // namespace
 
-// Best chunked plan for this shape (KMX_TCJ_H / KMX_TCJ_J force); false if none.
-bool tcj_plan(int ma, int mb, double* cost) {
+// Best chunked plan for this shape (KMX_TCJ_H / KMX_TCJ_J force); false if
+// none.  short_only: only plans whose chunking actually shortens the K span
+// of a short product (H0 <= 2, J >= 3) -- the shapes where the config-5 sweep
+// measured a gain over the tiled kernel.
+bool tcj_plan(int ma, int mb, double* cost, bool short_only) {
   const int fh = env_tj("KMX_TCJ_H", 0), fj = env_tj("KMX_TCJ_J", 0);
   bool ok = false;
   double best = 0.0;
@@ -365,6 +391,19 @@ bool tcj_plan(int ma, int mb, double* cost) {
       if (!ok || p.cost < best) best = p.cost;
       ok = true;
     }
+  }
+  if (ok && short_only) {  // the model's best plan must be a short-product one
+    ok = false;
+    double b2 = 0.0;
+    int bh = 0, bj = 0;
+    for (int H0 : {1, 2, 3, 4, 6, 8})
+      for (int J = 1; J <= 16; J++) {
+        TjPlan p;
+        if ((fh && fh != H0) || (fj && fj != J) || !tj_geometry(ma, mb, H0, J, p)) continue;
+        if (!ok || p.cost < b2) { b2 = p.cost; bh = H0; bj = J; }
+        ok = true;
+      }
+    ok = ok && bh <= 2 && bj >= 3;
   }
   if (cost) *cost = best;
   return ok;
