@@ -110,7 +110,8 @@ struct KsPlan {
   int W, dwords, cnt_max, dslots;
   int nrs;
   ReconStream rs[2];
-  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, total;
+  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, off_cmap, total;
+  int fin_chunks;  // 256-limb chunks of the longest finish stream (chunk-parallel finish maps)
 };
 
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -251,6 +252,18 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
   if (p.nrs) o = align256(o + (size_t)batch * p.dslots * p.cnt_max * p.dwords * 4);
   p.off_scr = o;
   if (p.sign) o = align256(o + (size_t)batch * (lf + lg + 2) * 8);
+  {  // chunk-parallel finish: one carry-map byte per (stream, 256-limb chunk)
+    long long qd = 0;
+    for (int i = 0; i < p.ns; i++) {
+      const long long E = p.st[i].off + (long long)p.st[i].cnt * p.st[i].W;
+      long long q = p.mp + 1;
+      if ((E + 31) / 32 + 1 > q) q = (E + 31) / 32 + 1;
+      if (q > qd) qd = q;
+    }
+    p.fin_chunks = (int)((qd + 255) / 256);
+  }
+  p.off_cmap = o;
+  o = align256(o + (size_t)batch * p.ns * p.fin_chunks);
   p.total = o;
   return KMX_OK;
 }
@@ -347,6 +360,8 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = (long long)p.cnt_max * p.dwords;
   fa.dslots_pair = p.dslots; fa.err = err;
   fa.bias = bfix;
+  fa.cmaps = (uint8_t*)(w + p.off_cmap);
+  fa.nchunks = p.fin_chunks;
   ReconArgs ra;
   memset(&ra, 0, sizeof ra);
   if (p.nrs) {

@@ -104,11 +104,13 @@ struct FinishArgs {
   uint32_t* dbuf; int dwords; long long dslot_stride; int dslots_pair;
   BiasFix bias;
   uint32_t* err;
+  uint8_t* cmaps; int nchunks;                    // chunk-parallel finish: [pair*ns + si][nchunks] carry maps
 };
 constexpr int FIN_THREADS = 256;
 constexpr int FIN_HALO = 32;
 // warp-per-stream finish (kmx_finish.cu) for short streams / many streams
 bool finish_use_warp(const FinishArgs& a, int batch);
+bool finish_use_chunks(const FinishArgs& a, int batch);
 cudaError_t launch_finish_w(const FinishArgs& a, int batch, cudaStream_t st);
 
 // --------------------------------------------------------- reconstruction
