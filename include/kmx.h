@@ -61,6 +61,7 @@ extern "C" {
 /* flags */
 #define KMX_SIGNED 1u          /* two's-complement input coefficients        */
 #define KMX_NO_VALIDATE 2u     /* skip the 0 <= c < 2^b range check           */
+#define KMX_NO_SPLIT 4u        /* kmx_ks_mul: do not split the batch over two streams */
 
 /* Derived parameters (ksint.py:82-98).  out[0..7] = e, N1, N2, N4,
  * four_point_safe, out_len, limbs of the packed f operand, limbs of the

@@ -21,6 +21,7 @@ KMX_ENOMEM = -5
 
 KMX_SIGNED = 1
 KMX_NO_VALIDATE = 2
+KMX_NO_SPLIT = 4
 
 
 class ReconstructionError(ArithmeticError):

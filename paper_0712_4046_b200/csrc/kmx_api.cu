@@ -271,7 +271,7 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
 int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KMX_OK : KMX_ECUDA; }
 
 int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h, int out_words,
-             void* ws, size_t ws_bytes, cudaStream_t st) {
+             void* ws, size_t ws_bytes, cudaStream_t st, uint32_t* err_shared = nullptr) {
   g_launches = 0;
   if (out_words < p.out_words_min) return KMX_EINVAL;
   if (ws_bytes < p.total || (!ws && p.total)) return KMX_EINVAL;
@@ -288,6 +288,9 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   unsigned long long* scr = (unsigned long long*)(w + p.off_scr);
   cudaError_t e = cudaMemsetAsync(err, 0, 12, st);  // error flag, multiply work counter, recon fallbacks
   if (e != cudaSuccess) return KMX_ECUDA;
+  uint32_t* const cnt = err + 1;  // multiply work counter
+  uint32_t* const diag = err + 2;
+  if (err_shared) err = err_shared;  // split batch: both halves latch into one flag
 
   PackArgs pa;
   memset(&pa, 0, sizeof pa);
@@ -337,7 +340,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.B = opg; ma.b_stride = p.mgs; ma.mb = p.mg;
   ma.P = prod; ma.p_stride = p.ps; ma.spill = spill;
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
-  ma.counter = (int*)(err + 1);
+  ma.counter = (int*)cnt;
   prof_begin(1, st);
   if (tc && !fuse && use_tcj(p.mf, p.mg, (long long)p.batch * p.P)) {
     if ((e = launch_tcmulj(ma, st)) != cudaSuccess) return KMX_ECUDA;
@@ -372,7 +375,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     ra.h = h; ra.out_words = out_words; ra.h_pair_stride = (long long)p.out_len * out_words;
     ra.err = err;
     ra.bias = bfix;
-    ra.diag = err + 2;
+    ra.diag = diag;
     // ks2 / ks4: finish + reconstruct in one kernel (k_finrec) when both fit it
     bool fused = false;
     prof_begin(3, st);
@@ -506,6 +509,67 @@ int ks_mul_host_pipelined(const KsPlan& pfull, HostCtx* c, const uint32_t* f, co
   return status_from_flag(fl);
 }
 
+// Split a device batch into K parts on K streams (kmx_ks_mul; K = 2 by
+// default, KMX_SPLIT_WAYS up to 4) for batches >= 256 pairs; KMX_SPLIT=0/1
+// forces, the KMX_NO_SPLIT flag disables per call.  The workspace is always
+// sized for the split; the call runs unsplit while per-kernel profiling is on
+// (kmx_prof_*).
+constexpr int SPLIT_MAX = 4;
+int split_ways(int batch, unsigned flags) {
+  static const int force = getenv("KMX_SPLIT") ? atoi(getenv("KMX_SPLIT")) : -1;
+  static const int ways = getenv("KMX_SPLIT_WAYS") ? atoi(getenv("KMX_SPLIT_WAYS")) : 2;
+  if ((flags & KMX_NO_SPLIT) || force == 0) return 1;
+  if (!(force == 1 || batch >= 256)) return 1;
+  int k = ways < 2 ? 2 : (ways > SPLIT_MAX ? SPLIT_MAX : ways);
+  if (k > batch) k = batch;
+  return k;
+}
+bool split_batch(int batch, unsigned flags) { return split_ways(batch, flags) > 1; }
+bool split_run(int batch, unsigned flags) { return split_batch(batch, flags) && !g_prof.on; }
+
+// part i of a K-way split: pairs [start, start + size)
+void split_part(int batch, int k, int i, int* start, int* size) {
+  const int q = batch / k, r = batch % k;
+  *start = i * q + (i < r ? i : r);
+  *size = q + (i < r ? 1 : 0);
+}
+
+struct SplitCtx {
+  cudaStream_t st[SPLIT_MAX] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t fork = nullptr, join[SPLIT_MAX] = {nullptr, nullptr, nullptr, nullptr};
+  int dev = -1;
+};
+thread_local SplitCtx g_split;
+
+SplitCtx& split_ctx(int* rc) {
+  *rc = KMX_OK;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { *rc = KMX_ECUDA; return g_split; }
+  if (g_split.fork && g_split.dev == dev) return g_split;
+  if (cudaEventCreateWithFlags(&g_split.fork, cudaEventDisableTiming) != cudaSuccess) *rc = KMX_ECUDA;
+  for (int i = 1; i < SPLIT_MAX && !*rc; i++)
+    if (cudaStreamCreateWithFlags(&g_split.st[i], cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_split.join[i], cudaEventDisableTiming) != cudaSuccess)
+      *rc = KMX_ECUDA;
+  g_split.dev = dev;
+  return g_split;
+}
+
+// workspace of a K-way split: a 256-byte header (the shared error flag) and
+// the K parts' workspaces
+size_t split_ws_layout(int variant, int batch, int lf, int lg, int b, int iw, unsigned flags, int k,
+                       size_t off[SPLIT_MAX], KsPlan* parts) {
+  size_t o = 256;
+  for (int i = 0; i < k; i++) {
+    int s0, n;
+    split_part(batch, k, i, &s0, &n);
+    if (make_plan(parts[i], variant, n, lf, lg, b, iw, flags)) return 0;
+    off[i] = o;
+    o += align256(parts[i].total);
+  }
+  return o;
+}
+
 }  // namespace
 
 extern "C" {
@@ -528,7 +592,13 @@ int kmx_ks_out_words(int len_f, int len_g, int coeff_bits, unsigned flags) {
 size_t kmx_ks_workspace_bytes(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags) {
   KsPlan p;
   if (make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags)) return 0;
-  return p.total;
+  if (!split_batch(batch, flags)) return p.total;
+  KsPlan parts[SPLIT_MAX];
+  size_t off[SPLIT_MAX];
+  const size_t sp = split_ws_layout(variant, batch, len_f, len_g, coeff_bits, 0, flags, split_ways(batch, flags), off,
+                                    parts);
+  if (!sp) return 0;
+  return sp > p.total ? sp : p.total;
 }
 
 int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits, const uint32_t* f,
@@ -537,7 +607,41 @@ int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits, con
   KsPlan p;
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, in_words, flags);
   if (rc) return rc;
-  return run_plan(p, f, g, h, out_words, workspace, ws_bytes, (cudaStream_t)stream);
+  if (!split_run(batch, flags)) return run_plan(p, f, g, h, out_words, workspace, ws_bytes, (cudaStream_t)stream);
+  // K parts on K streams (fork / join by events; captured as parallel graph
+  // branches): one part's latency-bound stages overlap another's tensor-core
+  // multiply
+  const int k = split_ways(batch, flags);
+  KsPlan parts[SPLIT_MAX];
+  size_t off[SPLIT_MAX];
+  const size_t need = split_ws_layout(variant, batch, len_f, len_g, coeff_bits, in_words, flags, k, off, parts);
+  if (!need || ws_bytes < need || !workspace) return KMX_EINVAL;
+  if (out_words < p.out_words_min) return KMX_EINVAL;
+  cudaStream_t st = (cudaStream_t)stream;
+  SplitCtx& sc = split_ctx(&rc);
+  if (rc) return rc;
+  uint32_t* hdr = (uint32_t*)workspace;  // the shared error flag (read by kmx_ws_status)
+  if (cudaMemsetAsync(hdr, 0, 4, st) != cudaSuccess) return KMX_ECUDA;
+  if (cudaEventRecord(sc.fork, st) != cudaSuccess) return KMX_ECUDA;
+  for (int i = 1; i < k; i++)
+    if (cudaStreamWaitEvent(sc.st[i], sc.fork, 0) != cudaSuccess) return KMX_ECUDA;
+  int nl = 0;
+  for (int i = 0; i < k; i++) {
+    int s0, n;
+    split_part(batch, k, i, &s0, &n);
+    const size_t fo = (size_t)s0 * len_f * p.in_words, go = (size_t)s0 * len_g * p.in_words;
+    const size_t ho = (size_t)s0 * p.out_len * out_words;
+    if ((rc = run_plan(parts[i], f + fo, g + go, h + ho, out_words, (char*)workspace + off[i], parts[i].total,
+                       i ? sc.st[i] : st, hdr)))
+      return rc;
+    nl += g_launches;
+  }
+  g_launches = nl;
+  for (int i = 1; i < k; i++) {
+    if (cudaEventRecord(sc.join[i], sc.st[i]) != cudaSuccess) return KMX_ECUDA;
+    if (cudaStreamWaitEvent(st, sc.join[i], 0) != cudaSuccess) return KMX_ECUDA;
+  }
+  return KMX_OK;
 }
 
 int kmx_ws_status(void* workspace, void* stream) {
@@ -554,6 +658,22 @@ int kmx_ws_limb_products(void* workspace, int variant, int batch, int len_f, int
   KsPlan p;
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);
   if (rc) return rc;
+  if (split_run(batch, flags)) {  // the parts' workspaces after a 256-byte header
+    const int k = split_ways(batch, flags);
+    KsPlan parts[SPLIT_MAX];
+    size_t off[SPLIT_MAX];
+    if (!split_ws_layout(variant, batch, len_f, len_g, coeff_bits, 0, flags, k, off, parts)) return KMX_EINVAL;
+    uint64_t tot = 0;
+    for (int i = 0; i < k; i++) {
+      uint64_t t = 0;
+      if ((rc = kmx_ws_limb_products((char*)workspace + off[i], variant, parts[i].batch, len_f, len_g, coeff_bits,
+                                     flags | KMX_NO_SPLIT, &t, stream)))
+        return rc;
+      tot += t;
+    }
+    *out = tot;
+    return KMX_OK;
+  }
   std::vector<uint32_t> meta((size_t)batch * p.P * 4);
   cudaStream_t st = (cudaStream_t)stream;
   if (!meta.empty()) {

@@ -20,7 +20,7 @@ SETTINGS = [
     {"KMX_FINISH_WARP": "0", "KMX_PACK_PAIR": "0"},   # block finish; one pack block per operand
     {"KMX_FINREC": "1"},        # finish + reconstruction fused (k_finrec)
     {"KMX_FINISH_CHUNKS": "1"},  # chunk-parallel finish (k_finmap + k_finchunk) everywhere
-    {"KMX_FINISH_CHUNKS": "0"},  # warp-per-stream finish wherever the chunked one would run
+    {"KMX_FINISH_CHUNKS": "0", "KMX_SPLIT": "1"},  # warp-per-stream finish; every batch split over two streams
     {"KMX_TC": "0"},            # integer-pipe multiply everywhere
     {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands)
     {"KMX_TC": "1", "KMX_TCJ": "1", "KMX_PACK_PAIR": "2"},  # chunked single-tile tensor-core kernel; paired packs at every batch size
