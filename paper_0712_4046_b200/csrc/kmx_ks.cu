@@ -1215,7 +1215,8 @@ static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStre
     }
   }
   const int nsteps = maxcount > 1 ? maxcount - 1 : 1;
-  int T = (nsteps + 7) / 8;             // ~8 steps per thread
+  static const int vt = getenv("KMX_RECON_V") ? atoi(getenv("KMX_RECON_V")) : 8;  // target steps per thread
+  int T = (nsteps + (vt > 0 ? vt : 8) - 1) / (vt > 0 ? vt : 8);
   T = ((T + 31) / 32) * 32;
   if (T < 32) T = 32;
   if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;

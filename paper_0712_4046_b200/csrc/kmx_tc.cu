@@ -248,12 +248,21 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
       }
       aw[w] = v;
     }
-    uint32_t* bw = reinterpret_cast<uint32_t*>(bpad);
+    // b: 16-byte loads when aligned (BPAD is a multiple of 16 bytes)
     const int nbw = (d.Lb + 2 * TcB<H>::BPAD) / 4;
     const int ba = TcB<H>::BPAD / 4;
-    for (int w = tid; w < nbw; w += TC_THREADS) {
-      const int j = w - ba;
-      bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
+    if ((mB & 3) == 0 && (reinterpret_cast<uintptr_t>(Bg) & 15) == 0 && (nbw & 3) == 0) {
+      uint4* bq = reinterpret_cast<uint4*>(bpad);
+      for (int w = tid; w < nbw / 4; w += TC_THREADS) {
+        const int j = 4 * w - ba;
+        bq[w] = (j >= 0 && j < mB) ? __ldg(reinterpret_cast<const uint4*>(Bg + j)) : make_uint4(0u, 0u, 0u, 0u);
+      }
+    } else {
+      uint32_t* bw = reinterpret_cast<uint32_t*>(bpad);
+      for (int w = tid; w < nbw; w += TC_THREADS) {
+        const int j = w - ba;
+        bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
+      }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
