@@ -14,4 +14,4 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --set full --clock-control none --import-source on -k "regex:k_pack|k_tcmul|k_finish|k_recon" -c 4 \
   -o gpurun_out/fin_prof python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-all-variants > gpurun_out/fin_ncu_f.log 2>&1
 echo done
-tail -2 gpurun_out/fin_tests.log gpurun_out/fin_smoke.log
+tail -n 2 gpurun_out/fin_tests.log; tail -n 2 gpurun_out/fin_smoke.log
