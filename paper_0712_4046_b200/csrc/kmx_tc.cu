@@ -43,6 +43,9 @@
 // CTA's last carry becomes the band spill K3 folds in (K2's MulArgs contract).
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <vector>
 
 #include "kmx_internal.h"
 #include "kmx_common.cuh"
@@ -534,12 +537,12 @@ double tc_cost(const TcDims& d, int TPC, int NW) {
 }
 
 template <int H>
-bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p) {
+bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p, int kc_force = 0, int nw_force = 0) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
   const TcDims d = tc_dims<H>(mA, mB);
   const int nseg = tc_nseg(d.Lb, d.S);  // u32 accumulator exactness: <= 64 KB of b per segment
   if (nseg * TcG<H>::N > TC_MAX_COLS) return false;
-  int KC = env_int_tc("KMX_TC_KC", 16);
+  int KC = kc_force ? kc_force : env_int_tc("KMX_TC_KC", 16);
   if (KC < 4) KC = 4;
   int NB = env_int_tc("KMX_TC_NB", 2);
   if (NB < 2) NB = 2;
@@ -558,8 +561,8 @@ bool tc_plan_h(int ma, int mb, long long nprod, size_t stage, TcPlan& p) {
   // enough CTAs to cover the SMs twice over
   while (TPC > 1 && nprod * ((d.ntiles + TPC - 1) / TPC) < 2LL * tc_num_sms()) TPC--;
   p.H = H;
-  p.NW = env_int_tc("KMX_TC_NW", TPC <= 2 ? 4 : 8) == 4 ? 4 : 8;
-  if (p.NW == 4 && env_int_tc("KMX_TC_KC", 0) == 0 && H <= 2) KC = 8;
+  p.NW = nw_force ? nw_force : (env_int_tc("KMX_TC_NW", TPC <= 2 ? 4 : 8) == 4 ? 4 : 8);
+  if (!kc_force && p.NW == 4 && env_int_tc("KMX_TC_KC", 0) == 0 && H <= 2) KC = 8;
   p.KC = KC;
   p.NB = NB;
   p.TPC = TPC;
@@ -689,6 +692,90 @@ bool tc_supported(int ma, int mb, size_t stage_bytes) {
   return tc_plan(ma, mb, 1 << 20, stage_bytes, p);
 }
 
+namespace {
+cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, const PackArgs* pk, int P);
+
+// Candidate tilings: every feasible H with KC in {8, 16} and NW in {4, 8},
+// keeping those the model puts within 1.6x of its best.
+std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
+  std::vector<TcPlan> v;
+  double best = 1e300;
+  for (int kc : {8, 16})
+    for (int nw : {4, 8}) {
+      TcPlan p;
+#define KMX_CAND_H(HH)                                           \
+  if (tc_plan_h<HH>(ma, mb, nprod, 0, p, kc, nw)) {              \
+    v.push_back(p);                                              \
+    best = p.cost < best ? p.cost : best;                        \
+  }
+      KMX_CAND_H(1) KMX_CAND_H(2) KMX_CAND_H(3) KMX_CAND_H(4) KMX_CAND_H(6) KMX_CAND_H(8)
+#undef KMX_CAND_H
+    }
+  std::vector<TcPlan> out;
+  for (const TcPlan& p : v)
+    if (p.cost <= 1.6 * best) out.push_back(p);
+  return out;
+}
+
+struct TuneKey {
+  int ma, mb;
+  long long nprod;
+  bool operator<(const TuneKey& o) const {
+    return ma != o.ma ? ma < o.ma : (mb != o.mb ? mb < o.mb : nprod < o.nprod);
+  }
+};
+std::mutex g_tune_mu;
+std::map<TuneKey, TcPlan> g_tune;
+
+// Measured plan choice, once per (shape, batch): the first call outside a CUDA
+// graph capture times every candidate tiling on the caller's stream (second of
+// two launches each, CUDA events; every candidate writes the same bit-exact
+// product, so the output is valid whichever runs last) and caches the
+// fastest.  The cost model alone misses by up to 30% on long products
+// (tools/tc_sweep.py).  KMX_TC_AUTOTUNE=0, or any KMX_TC_H/KC/NW/NB/TPC
+// override, keeps the model's choice.
+bool tc_tuned_plan(const MulArgs& a, cudaStream_t st, TcPlan& p, bool* launched) {
+  *launched = false;
+  static const int on = env_int_tc("KMX_TC_AUTOTUNE", 1) && !getenv("KMX_TC_H") && !getenv("KMX_TC_KC") &&
+                        !getenv("KMX_TC_NW") && !getenv("KMX_TC_NB") && !getenv("KMX_TC_TPC");
+  if (!on) return false;
+  const TuneKey key{a.ma, a.mb, a.nprod};
+  std::lock_guard<std::mutex> lk(g_tune_mu);
+  auto it = g_tune.find(key);
+  if (it != g_tune.end()) { p = it->second; return true; }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
+  std::vector<TcPlan> cands = tc_candidates(a.ma, a.mb, a.nprod);
+  if (cands.size() < 2) return false;
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return false;
+  float best_ms = 1e30f;
+  int best = -1;
+  for (size_t i = 0; i < cands.size(); i++) {
+    if (launch_plan(a, cands[i], st, nullptr, 1) != cudaSuccess) continue;
+    cudaEventRecord(e0, st);
+    if (launch_plan(a, cands[i], st, nullptr, 1) != cudaSuccess) continue;
+    cudaEventRecord(e1, st);
+    if (cudaEventSynchronize(e1) != cudaSuccess) continue;
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best_ms) { best_ms = ms; best = (int)i; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (best < 0) return false;
+  p = cands[best];
+  g_tune[key] = p;
+  if (env_int_tc("KMX_TC_VERBOSE", 0))
+    fprintf(stderr, "kmx_tc autotune: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d (%.4f ms of %zu candidates)\n", a.ma,
+            a.mb, a.nprod, p.H, p.NW, p.KC, best_ms, cands.size());
+  // re-run the winner last so the buffers hold its (identical) output in order
+  if (launch_plan(a, p, st, nullptr, 1) != cudaSuccess) return false;
+  *launched = true;
+  return true;
+}
+}  // namespace
+
 cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, int P) {
   TcPlan p;
   size_t stage = 0;
@@ -699,6 +786,15 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
   }
   if (!tc_plan(a.ma, a.mb, a.nprod, stage, p)) return cudaErrorNotSupported;
   if (a.nprod == 0) return cudaSuccess;
+  if (!pk) {
+    bool launched = false;
+    if (tc_tuned_plan(a, st, p, &launched) && launched) return cudaGetLastError();
+  }
+  return launch_plan(a, p, st, pk, P);
+}
+
+namespace {
+cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, const PackArgs* pk, int P) {
   if (env_int_tc("KMX_TC_VERBOSE", 0))
     fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d nseg=%d smem=%zu cost=%.0f\n",
             a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.nseg, p.smem, p.cost);
@@ -727,5 +823,6 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
   }
   return e;
 }
+}  // namespace
 
 }  // namespace kmx

@@ -45,8 +45,12 @@ def main():
     ap.add_argument("--tpcs", default="0")
     ap.add_argument("--nbs", default="2")
     ap.add_argument("--nws", default="4,8")
+    ap.add_argument("--shape", default="", help="batch,n,bits (unsigned) instead of --config")
     args = ap.parse_args()
     cfg = bench.CONFIGS[args.config]
+    if args.shape:
+        B_, n_, b_ = map(int, args.shape.split(","))
+        cfg = dict(kind="ks", batch=B_, n=n_, b=b_, signed=False)
     B, n, b, signed = cfg["batch"], cfg["n"], cfg["b"], cfg["signed"]
     words = 1 if signed else (b + 31) // 32
     rng = np.random.default_rng(1)
@@ -80,7 +84,7 @@ def main():
     torch.cuda.synchronize()
     os.environ.pop("KMX_TC_VERBOSE")
     res.append({"engine": "tensor(default plan)", "k2_ms": k2_ms(kb, f, g, out, args.reps)})
-    print(json.dumps({"config": args.config, "variant": args.variant, "results": res}, indent=1))
+    print(json.dumps({"config": args.shape or args.config, "variant": args.variant, "results": res}, indent=1))
 
 
 if __name__ == "__main__":
