@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstdio>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <vector>
 
@@ -271,7 +272,8 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
 int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KMX_OK : KMX_ECUDA; }
 
 int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h, int out_words,
-             void* ws, size_t ws_bytes, cudaStream_t st, uint32_t* err_shared = nullptr) {
+             void* ws, size_t ws_bytes, cudaStream_t st, uint32_t* err_shared = nullptr,
+             cudaEvent_t after_pack = nullptr) {
   g_launches = 0;
   if (out_words < p.out_words_min) return KMX_EINVAL;
   if (ws_bytes < p.total || (!ws && p.total)) return KMX_EINVAL;
@@ -334,6 +336,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     prof_end(0, st);
     g_launches++;
   }
+  if (after_pack && cudaEventRecord(after_pack, st) != cudaSuccess) return KMX_ECUDA;
 
   MulArgs ma;
   ma.A = opf; ma.a_stride = p.mfs; ma.ma = p.mf;
@@ -515,17 +518,60 @@ int ks_mul_host_pipelined(const KsPlan& pfull, HostCtx* c, const uint32_t* f, co
 // sized for the split; the call runs unsplit while per-kernel profiling is on
 // (kmx_prof_*).
 constexpr int SPLIT_MAX = 4;
-int split_ways(int batch, unsigned flags) {
-  static const int force = getenv("KMX_SPLIT") ? atoi(getenv("KMX_SPLIT")) : -1;
+// A schedule: the batch cut into `ways` parts on `ways` streams, all started
+// at the fork or (stagger) each when the previous part's pack is done.
+struct Sched { int ways, stagger; };
+constexpr Sched SCHEDS[] = {{1, 0}, {2, 0}, {2, 1}, {4, 1}};
+constexpr int NSCHED = 4;
+
+// Default (no measurement): two parts at >= 256 pairs.  KMX_SPLIT=0 forces one
+// part, KMX_SPLIT=1 the default split with KMX_SPLIT_WAYS / KMX_SPLIT_STAGGER.
+int split_force() {
+  static const int f = getenv("KMX_SPLIT") ? atoi(getenv("KMX_SPLIT")) : -1;
+  return f;
+}
+Sched default_sched(int batch, unsigned flags) {
   static const int ways = getenv("KMX_SPLIT_WAYS") ? atoi(getenv("KMX_SPLIT_WAYS")) : 2;
-  if ((flags & KMX_NO_SPLIT) || force == 0) return 1;
-  if (!(force == 1 || batch >= 256)) return 1;
+  static const int stag = getenv("KMX_SPLIT_STAGGER") ? atoi(getenv("KMX_SPLIT_STAGGER")) : 0;
+  if ((flags & KMX_NO_SPLIT) || split_force() == 0) return Sched{1, 0};
+  if (!(split_force() == 1 || batch >= 256)) return Sched{1, 0};
   int k = ways < 2 ? 2 : (ways > SPLIT_MAX ? SPLIT_MAX : ways);
   if (k > batch) k = batch;
-  return k;
+  return Sched{k, stag};
 }
-bool split_batch(int batch, unsigned flags) { return split_ways(batch, flags) > 1; }
-bool split_run(int batch, unsigned flags) { return split_batch(batch, flags) && !g_prof.on; }
+// schedules measured per shape (kmx_ks_mul), keyed by the call's shape
+struct SchedKey {
+  int variant, batch, lf, lg, b, iw;
+  unsigned flags;
+  bool operator<(const SchedKey& o) const {
+    const int x[6] = {variant, batch, lf, lg, b, iw}, y[6] = {o.variant, o.batch, o.lf, o.lg, o.b, o.iw};
+    for (int i = 0; i < 6; i++)
+      if (x[i] != y[i]) return x[i] < y[i];
+    return flags < o.flags;
+  }
+};
+std::mutex g_sched_mu;
+std::map<SchedKey, Sched> g_sched;
+bool tuned_sched(const SchedKey& k, Sched* s) {
+  std::lock_guard<std::mutex> lk(g_sched_mu);
+  auto it = g_sched.find(k);
+  if (it == g_sched.end()) return false;
+  *s = it->second;
+  return true;
+}
+// the schedule a call with this shape runs (or ran) with
+Sched current_sched(const SchedKey& k) {
+  if (g_prof.on || (k.flags & KMX_NO_SPLIT) || split_force() >= 0) return g_prof.on ? Sched{1, 0} : default_sched(k.batch, k.flags);
+  Sched s;
+  if (tuned_sched(k, &s)) return s;
+  return default_sched(k.batch, k.flags);
+}
+int max_ways(int batch, unsigned flags) {
+  if ((flags & KMX_NO_SPLIT) || split_force() == 0 || batch < 2) return 1;
+  int m = default_sched(batch, flags).ways;
+  if (split_force() < 0 && batch >= 64) m = batch < SPLIT_MAX ? batch : SPLIT_MAX;
+  return m;
+}
 
 // part i of a K-way split: pairs [start, start + size)
 void split_part(int batch, int k, int i, int* start, int* size) {
@@ -537,6 +583,7 @@ void split_part(int batch, int k, int i, int* start, int* size) {
 struct SplitCtx {
   cudaStream_t st[SPLIT_MAX] = {nullptr, nullptr, nullptr, nullptr};
   cudaEvent_t fork = nullptr, join[SPLIT_MAX] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t packed[SPLIT_MAX] = {nullptr, nullptr, nullptr, nullptr};
   int dev = -1;
 };
 thread_local SplitCtx g_split;
@@ -551,6 +598,8 @@ SplitCtx& split_ctx(int* rc) {
     if (cudaStreamCreateWithFlags(&g_split.st[i], cudaStreamNonBlocking) != cudaSuccess ||
         cudaEventCreateWithFlags(&g_split.join[i], cudaEventDisableTiming) != cudaSuccess)
       *rc = KMX_ECUDA;
+  for (int i = 0; i < SPLIT_MAX && !*rc; i++)
+    if (cudaEventCreateWithFlags(&g_split.packed[i], cudaEventDisableTiming) != cudaSuccess) *rc = KMX_ECUDA;
   g_split.dev = dev;
   return g_split;
 }
@@ -592,14 +641,20 @@ int kmx_ks_out_words(int len_f, int len_g, int coeff_bits, unsigned flags) {
 size_t kmx_ks_workspace_bytes(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags) {
   KsPlan p;
   if (make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags)) return 0;
-  if (!split_batch(batch, flags)) return p.total;
-  KsPlan parts[SPLIT_MAX];
-  size_t off[SPLIT_MAX];
-  const size_t sp = split_ws_layout(variant, batch, len_f, len_g, coeff_bits, 0, flags, split_ways(batch, flags), off,
-                                    parts);
-  if (!sp) return 0;
-  return sp > p.total ? sp : p.total;
+  size_t best = p.total;
+  for (int k = 2; k <= max_ways(batch, flags); k++) {
+    KsPlan parts[SPLIT_MAX];
+    size_t off[SPLIT_MAX];
+    const size_t sp = split_ws_layout(variant, batch, len_f, len_g, coeff_bits, 0, flags, k, off, parts);
+    if (!sp) return 0;
+    if (sp > best) best = sp;
+  }
+  return best;
 }
+
+static int run_sched(const Sched& sc0, const KsPlan& p, int variant, int batch, int len_f, int len_g, int coeff_bits,
+                     int in_words, unsigned flags, const uint32_t* f, const uint32_t* g, uint32_t* h, int out_words,
+                     void* workspace, size_t ws_bytes, cudaStream_t st);
 
 int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits, const uint32_t* f,
                const uint32_t* g, int in_words, uint32_t* h, int out_words, void* workspace,
@@ -607,32 +662,91 @@ int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits, con
   KsPlan p;
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, in_words, flags);
   if (rc) return rc;
-  if (!split_run(batch, flags)) return run_plan(p, f, g, h, out_words, workspace, ws_bytes, (cudaStream_t)stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  const SchedKey key{variant, batch, len_f, len_g, coeff_bits, p.in_words, flags};
+  const bool tune = !g_prof.on && !(flags & KMX_NO_SPLIT) && split_force() < 0 && batch >= 64;
+  Sched sc0;
+  if (!tune || tuned_sched(key, &sc0)) {
+    if (!tune) sc0 = current_sched(key);
+    return run_sched(sc0, p, variant, batch, len_f, len_g, coeff_bits, in_words, flags, f, g, h, out_words,
+                     workspace, ws_bytes, st);
+  }
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone)
+    return run_sched(default_sched(batch, flags), p, variant, batch, len_f, len_g, coeff_bits, in_words, flags, f, g,
+                     h, out_words, workspace, ws_bytes, st);
+  // first call of this shape: time every schedule (one warm-up run each, which
+  // also settles the tensor-core plan of its part sizes, then one timed run)
+  // and keep the fastest; every run writes the same bit-exact output
+  cudaEvent_t e0, e1;
+  if (cudaEventCreate(&e0) != cudaSuccess || cudaEventCreate(&e1) != cudaSuccess) return KMX_ECUDA;
+  float best_ms = 1e30f;
+  int best = 0, nl = 0, last = -1;
+  for (int i = 0; i < NSCHED; i++) {
+    const Sched c = SCHEDS[i];
+    if (c.ways > batch || (c.ways > 1 && batch < 64)) continue;
+    if ((rc = run_sched(c, p, variant, batch, len_f, len_g, coeff_bits, in_words, flags, f, g, h, out_words, workspace,
+                        ws_bytes, st)))
+      break;
+    cudaEventRecord(e0, st);
+    if ((rc = run_sched(c, p, variant, batch, len_f, len_g, coeff_bits, in_words, flags, f, g, h, out_words, workspace,
+                        ws_bytes, st)))
+      break;
+    cudaEventRecord(e1, st);
+    last = i;
+    if (cudaEventSynchronize(e1) != cudaSuccess) { rc = KMX_ECUDA; break; }
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    if (ms < best_ms) { best_ms = ms; best = i; nl = g_launches; }
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  {
+    std::lock_guard<std::mutex> lk(g_sched_mu);
+    g_sched[key] = SCHEDS[best];
+  }
+  if (getenv("KMX_TC_VERBOSE") && atoi(getenv("KMX_TC_VERBOSE")))
+    fprintf(stderr, "kmx schedule: variant=%d batch=%d len=%d,%d b=%d -> %d ways%s (%.4f ms)\n", variant, batch, len_f,
+            len_g, coeff_bits, SCHEDS[best].ways, SCHEDS[best].stagger ? " staggered" : "", best_ms);
+  // leave the workspace as the chosen schedule lays it out (MulStats reads it)
+  if (best != last &&
+      (rc = run_sched(SCHEDS[best], p, variant, batch, len_f, len_g, coeff_bits, in_words, flags, f, g, h, out_words,
+                      workspace, ws_bytes, st)))
+    return rc;
+  g_launches = nl;
+  return KMX_OK;
+}
+
+static int run_sched(const Sched& sc0, const KsPlan& p, int variant, int batch, int len_f, int len_g, int coeff_bits,
+                     int in_words, unsigned flags, const uint32_t* f, const uint32_t* g, uint32_t* h, int out_words,
+                     void* workspace, size_t ws_bytes, cudaStream_t st) {
+  int rc = KMX_OK;
+  if (sc0.ways <= 1) return run_plan(p, f, g, h, out_words, workspace, ws_bytes, st);
   // K parts on K streams (fork / join by events; captured as parallel graph
   // branches): one part's latency-bound stages overlap another's tensor-core
   // multiply
-  const int k = split_ways(batch, flags);
+  const int k = sc0.ways;
   KsPlan parts[SPLIT_MAX];
   size_t off[SPLIT_MAX];
   const size_t need = split_ws_layout(variant, batch, len_f, len_g, coeff_bits, in_words, flags, k, off, parts);
   if (!need || ws_bytes < need || !workspace) return KMX_EINVAL;
   if (out_words < p.out_words_min) return KMX_EINVAL;
-  cudaStream_t st = (cudaStream_t)stream;
   SplitCtx& sc = split_ctx(&rc);
   if (rc) return rc;
   uint32_t* hdr = (uint32_t*)workspace;  // the shared error flag (read by kmx_ws_status)
+  const int stagger = sc0.stagger;  // part i starts when part i-1's pack is done
   if (cudaMemsetAsync(hdr, 0, 4, st) != cudaSuccess) return KMX_ECUDA;
   if (cudaEventRecord(sc.fork, st) != cudaSuccess) return KMX_ECUDA;
-  for (int i = 1; i < k; i++)
-    if (cudaStreamWaitEvent(sc.st[i], sc.fork, 0) != cudaSuccess) return KMX_ECUDA;
   int nl = 0;
   for (int i = 0; i < k; i++) {
     int s0, n;
     split_part(batch, k, i, &s0, &n);
     const size_t fo = (size_t)s0 * len_f * p.in_words, go = (size_t)s0 * len_g * p.in_words;
     const size_t ho = (size_t)s0 * p.out_len * out_words;
+    if (i && cudaStreamWaitEvent(sc.st[i], stagger ? sc.packed[i - 1] : sc.fork, 0) != cudaSuccess) return KMX_ECUDA;
     if ((rc = run_plan(parts[i], f + fo, g + go, h + ho, out_words, (char*)workspace + off[i], parts[i].total,
-                       i ? sc.st[i] : st, hdr)))
+                       i ? sc.st[i] : st, hdr, stagger ? sc.packed[i] : nullptr)))
       return rc;
     nl += g_launches;
   }
@@ -658,8 +772,9 @@ int kmx_ws_limb_products(void* workspace, int variant, int batch, int len_f, int
   KsPlan p;
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);
   if (rc) return rc;
-  if (split_run(batch, flags)) {  // the parts' workspaces after a 256-byte header
-    const int k = split_ways(batch, flags);
+  const Sched used = current_sched(SchedKey{variant, batch, len_f, len_g, coeff_bits, p.in_words, flags});
+  if (used.ways > 1) {  // the parts' workspaces after a 256-byte header
+    const int k = used.ways;
     KsPlan parts[SPLIT_MAX];
     size_t off[SPLIT_MAX];
     if (!split_ws_layout(variant, batch, len_f, len_g, coeff_bits, 0, flags, k, off, parts)) return KMX_EINVAL;
