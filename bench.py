@@ -314,6 +314,12 @@ def run_ours(args, cfg, rank, world, local_rank):
             rec["mul_limb_products_per_s"] = prods / (mul_ms * 1e-3) if mul_ms > 0 else None
             rec["mul_frac_of_imad_peak"] = rec["mul_limb_products_per_s"] / peak if mul_ms > 0 else None
             rec["mul_engine"] = kmx.mul_engine(v, cfg["n"], cfg["n"], cfg["b"], signed=signed)
+            plan = (ctypes.c_int64 * 8)()
+            if L.kmx_mul_plan(v, B, cfg["n"], cfg["n"], cfg["b"], _lib.KMX_SIGNED if signed else 0, plan) == 0:
+                rec["mul_plan"] = {"engine": ["imad", "tensor tiled", "tensor chunked"][int(plan[0])],
+                                   "H": int(plan[1]), "NW": int(plan[2]), "KC": int(plan[3]), "TPC": int(plan[4]),
+                                   "mmas_per_product": int(plan[5]), "smem_bytes_per_product": int(plan[6]),
+                                   "issued_byte_macs_per_product": int(plan[7])}
             if rec["mul_engine"] == "tensor" and mul_ms > 0:
                 # algorithmic byte MACs of the u8 convolution: 16 per 32x32 limb product
                 rec["mul_frac_of_tensor_peak"] = 16.0 * rec["mul_limb_products_per_s"] / tpeak
@@ -559,6 +565,22 @@ def main():
                 "traffic": load_traffic(args.config, v, "tcmul_dram_bytes"),
                 "same_kernel_in_imad_units": {"achieved": ach, "unit": "G limb-products/s",
                                               "frac_of_imad_peak": ach * 1e9 / r["peak"]}}
+            mp_ = rec.get("mul_plan")
+            if mp_ and mp_["engine"] == "tensor tiled" and mp_["smem_bytes_per_product"]:
+                # what bounds it: the SS-mode MMAs read A (128 x 32 B) and B (16H x 32 B)
+                # from shared memory per MMA; peak = 128 B/clk/SM at the observed SM clock
+                P_ = {1: 1, 2: 2, 3: 2, 4: 4}[v]
+                nprod = cfg["batch"] * P_
+                clk = (r["clocks"] or {}).get("sm_mhz") or 1965.0
+                smem_peak = 148 * 128 * clk * 1e6 / 1e9
+                smem_ach = mp_["smem_bytes_per_product"] * nprod / (mul_ms * 1e-3) / 1e9
+                line["roofline"]["smem_operand_bound"] = {
+                    "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s", "frac": smem_ach / smem_peak,
+                    "bytes_per_launch": mp_["smem_bytes_per_product"] * nprod,
+                    "plan": {k: mp_[k] for k in ("H", "NW", "KC", "TPC", "mmas_per_product")},
+                    "algorithmic_fraction_of_issued_macs": 16.0 * algorithmic_products(cfg, v) / P_ /
+                    mp_["issued_byte_macs_per_product"] if mp_["issued_byte_macs_per_product"] else None,
+                    "note": "peak = 148 SMs x 128 B/clk shared-memory bandwidth at the observed SM clock"}
         else:
             imad_view["traffic"] = load_traffic(args.config, v)
             line["roofline"] = imad_view

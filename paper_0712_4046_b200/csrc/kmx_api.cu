@@ -38,6 +38,7 @@ int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
 namespace kmx {
 // chunked single-tile tensor-core multiply (kmx_tcj.cu)
 bool tcj_plan(int ma, int mb, double* cost, bool short_only);
+bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]);
 cudaError_t launch_tcmulj(const MulArgs& a, cudaStream_t st);
 }  // namespace kmx
 namespace {
@@ -990,6 +991,18 @@ int kmx_reconstruct_host(int batch, int count, int width_bits, const uint32_t* f
 double kmx_imad_peak(int iters) { return measure_imad_peak(iters > 0 ? iters : 4096); }
 
 double kmx_tc_peak(int iters) { return measure_tc_peak(iters > 0 ? iters : 2000); }
+
+int kmx_mul_plan(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags, int64_t* out8) {
+  KsPlan p;
+  int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);
+  if (rc) return rc;
+  long long o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  const long long nprod = (long long)batch * p.P;
+  if (use_tensor_mul(p.mf, p.mg) && !use_tcj(p.mf, p.mg, nprod)) tc_plan_info(p.mf, p.mg, nprod, o);
+  else if (use_tensor_mul(p.mf, p.mg)) o[0] = 2;  // chunked single-tile kernel
+  for (int i = 0; i < 8; i++) out8[i] = o[i];
+  return KMX_OK;
+}
 
 int kmx_mul_engine(int variant, int len_f, int len_g, int coeff_bits, unsigned flags) {
   KsPlan p;

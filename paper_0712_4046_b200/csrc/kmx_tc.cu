@@ -825,4 +825,56 @@ cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, cons
 }
 }  // namespace
 
+
+namespace {
+template <int H>
+void tc_count(int ma, int mb, const TcPlan& p, long long out[8]) {
+  const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
+  const TcDims d = tc_dims<H>(mA, mB);
+  long long mmas = 0, build_steps = 0;
+  for (int r0 = 0; r0 < d.ntiles; r0 += p.TPC) {
+    int lo = d.S, hi = 0;
+    for (int t = r0; t < (r0 + p.TPC < d.ntiles ? r0 + p.TPC : d.ntiles); t++) {
+      int slo, shi;
+      tc_tile_steps<H>(d, t, slo, shi);
+      if (shi > slo) {
+        mmas += shi - slo;
+        lo = slo < lo ? slo : lo;
+        hi = shi > hi ? shi : hi;
+      }
+    }
+    if (hi > lo) build_steps += hi - lo;
+  }
+  out[0] = 1; out[1] = H; out[2] = p.NW; out[3] = p.KC; out[4] = p.TPC;
+  out[5] = mmas;
+  // shared-memory bytes per product: each MMA reads its A tile (128 x 32 B)
+  // and B tile (16H x 32 B); the builders write each staged B step once
+  out[6] = mmas * (4096LL + 512LL * H) + build_steps * 512LL * H;
+  out[7] = 128LL * 16 * H * 32 * mmas;  // issued byte MACs
+}
+}  // namespace
+
+// The tiled tensor-core plan a launch of nprod products runs with (the
+// autotuned one when cached, else the model's) and its work counts:
+// out = {1, H, NW, KC, TPC, MMAs per product, smem operand bytes per product,
+// issued byte MACs per product}.  false if the shape is not tensor-core.
+bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]) {
+  TcPlan p;
+  if (!tc_plan(ma, mb, nprod, 0, p)) return false;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_tune.find(TuneKey{ma, mb, nprod});
+    if (it != g_tune.end()) p = it->second;
+  }
+  switch (p.H) {
+    case 1: tc_count<1>(ma, mb, p, out); break;
+    case 2: tc_count<2>(ma, mb, p, out); break;
+    case 3: tc_count<3>(ma, mb, p, out); break;
+    case 4: tc_count<4>(ma, mb, p, out); break;
+    case 6: tc_count<6>(ma, mb, p, out); break;
+    default: tc_count<8>(ma, mb, p, out); break;
+  }
+  return true;
+}
+
 }  // namespace kmx
