@@ -33,6 +33,17 @@ struct SmemDigitSink {    // the reconstruction's padded shared-memory copy (k_f
   }
 };
 
+// Word w of the W-bit digit starting at bit lb >= 0 of a chunk buffer of
+// FIN_HALO + FW_CH words (bits at or above W masked off).
+__device__ __forceinline__ u32 dig_word(const u32* buf, int lb, int w, int W) {
+  const int bit = lb + 32 * w, q = bit >> 5;
+  const u32 lo = buf[q], hi = q + 1 < FIN_HALO + FW_CH ? buf[q + 1] : 0u;
+  u32 x = __funnelshift_r(lo, hi, bit & 31);
+  const int rem = W - 32 * w;
+  if (rem < 32) x &= (1u << rem) - 1u;
+  return x;
+}
+
 // One output stream (index si of pair `pair`) by one warp; buf: FIN_HALO +
 // FW_CH words of this warp's shared memory (16-byte aligned).  Digit-buffer
 // streams (mode 1) go to the sink.
@@ -169,13 +180,41 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
     __syncwarp();
     // digits whose top bit falls inside this chunk
     const long long clo = 32LL * q00, chi = 32LL * (q00 + FW_CH);
-    const long long t = clo - off + 1;
+    // stream bit positions stay below 2^31 (products of < 2^26 limbs), so
+    // 32-bit divisions
+    const int t = (int)(clo - off + 1);
     long long jl = t <= 0 ? 0 : (t + W - 1) / W - 1;
     if (jl < 0) jl = 0;
-    const long long u = chi - off;
+    const int u = (int)(chi - off);
     long long jh = u <= 0 ? 0 : u / W;
     if (jh > S.cnt) jh = S.cnt;
     const long long base = off - 32LL * (q00 - FIN_HALO);
+    if (W <= 32 * FIN_HALO) {
+      // lean extraction: every digit handled here starts inside the halo or
+      // the chunk (bit >= 0), so chunk-local 32-bit positions, one funnel
+      // shift per word and no range tests
+      const int ib = (int)(base + jl * W);
+      for (int jj = lane; jj < (int)(jh - jl); jj += 32) {
+        const int j = (int)jl + jj;
+        const int lb = ib + jj * W;
+        if (S.mode == 0) {
+          const long long kpos = S.pos0 + (long long)j * S.pstride;
+          u32* dst = hpair + kpos * a.out_words;
+          if (a.bias.enabled) {
+            unsigned __int128 hp = 0;
+            for (int w = 0; w < Wd && w < 4; w++) hp |= (unsigned __int128)dig_word(buf, lb, w, W) << (32 * w);
+            store_coeff128(dst, a.out_words, hp, kpos, a.bias, pair);
+          } else {
+            for (int w = 0; w < a.out_words; w++) dst[w] = w < Wd ? dig_word(buf, lb, w, W) : 0u;
+          }
+        } else {
+          const int idx = S.reversed ? (S.cnt - 1 - j) : j;
+          u32* dp = dbase + sink.off(idx, 0);
+#pragma unroll 2
+          for (int w = 0; w < a.dwords; w++) dp[w] = w < Wd ? dig_word(buf, lb, w, W) : 0u;
+        }
+      }
+    } else
     for (long long j = jl + lane; j < jh; j += 32) {
       const long long lb = base + j * W;
       if (S.mode == 0) {

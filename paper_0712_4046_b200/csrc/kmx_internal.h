@@ -33,6 +33,7 @@ struct PackArgs {
   int bias;                   // signed inputs: add 2^(b-1) (bias lift)
   uint32_t* err;
   int stage;                  // set by launch_pack: coefficients staged in shared memory
+  int fast1;                  // set by launch_pack: loop-free bitstream windows allowed (KMX_PACK_FAST)
 };
 
 // -------------------------------------------------------------- multiply
@@ -131,6 +132,7 @@ struct ReconArgs {
   uint32_t* diag;             // optional counter of sequential fallbacks
   int rw_slice;               // k_recon_warp: shared-memory words per warp
   int bias_smem;              // k_recon_par: stage the signed path's prefix sums in shared memory
+  int spec;                   // k_recon_par: speculative stores from this scan round on (0: never)
 };
 
 // ---------------------------------------------------------- signed (bias)

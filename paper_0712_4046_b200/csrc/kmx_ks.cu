@@ -849,7 +849,7 @@ __device__ __forceinline__ void recon_fallback(const ReconArgs& a, const ReconSt
 template <int NW>
 __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconStream& S, int pair, const u32* F,
                                                const u32* R, int lgV, int V, const BiasFix& bfx, u32* smw, int* smi,
-                                               uint8_t* dend, int* fallback) {
+                                               uint8_t* dend, int* fallback, int spec) {
   u32* H = a.h + (long long)pair * a.h_pair_stride;
   const int W = a.W, dw = a.dwords, ow = a.out_words, count = S.count;
   const int nsteps = count - 1;
@@ -885,7 +885,7 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
   if (tid == 0) *fallback = 0;
   bool bad = false;
   ReconState<NW> st, st0;
-  bool converged = false;
+  bool converged = false, stored = false, bad_it = false;
   for (int it = 0; it < RECON_MAXIT && !converged; it++) {
     const int p = s0 & 1;
     mw_add_small(st.lo_cur, p ? cs1 : cs0, p ? E1 : E0);
@@ -901,7 +901,17 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
     st0 = st;
     int n0 = 0, n1 = 0;
     bool b1 = false;
-    recon_walk<NW, false>(st, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, b1, bfx, pair);
+    // From round `spec` on (0: never) the walk stores speculatively: the round
+    // that converges started from the exact state, so its stores are the
+    // output and the separate output walk disappears (earlier rounds' stores
+    // are overwritten by the same thread, or by the fallback after a barrier).
+    // c2 streams typically converge in round 2 (guess, correction, check).
+    stored = spec > 0 && it >= spec;
+    if (stored)
+      recon_walk<NW, true>(st, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, b1, bfx, pair);
+    else
+      recon_walk<NW, false>(st, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, n0, n1, b1, bfx, pair);
+    bad_it = b1;
     block_exscan_i2(n0, n1, smi);
     dend[tid] = (uint8_t)st.fc;
     __syncthreads();
@@ -911,7 +921,9 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
     E0 = n0; E1 = n1; dstart = dnew;
   }
   TRACE(4);
-  if (converged) {  // output walk from the verified start state
+  if (converged && stored) {
+    bad |= bad_it;
+  } else if (converged) {  // output walk from the verified start state
     ReconState<NW> sw = st0;
     int q0 = 0, q1 = 0;
     recon_walk<NW, true>(sw, s0, s1, F, R, dw, lgV, H, S.pos0, S.pstride, ow, W, topmask, mask, q0, q1, bad, bfx, pair);
@@ -929,9 +941,11 @@ __device__ __forceinline__ void recon_par_body(const ReconArgs& a, const ReconSt
   if (bad && (!*fallback || tid == 0)) raise_err(a.err, ERR_RECON);
 }
 
-template <int NW>
-__global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
-  __shared__ u32 smw[2 * 17 * 32];
+// MINB > 1: a register-capped instance for CTAs of at most 128 threads, so
+// MINB CTAs fit per SM (the NW <= 2 streams of c2-sized products).
+template <int NW, int MINB = 1>
+__global__ void __launch_bounds__(MINB > 1 ? 128 : RECON_PAR_MAXT, MINB) k_recon_par(ReconArgs a) {
+  __shared__ u32 smw[2 * NW * (RECON_PAR_MAXT / 32)];  // block_exscan_mw2: 2 NW words per warp
   __shared__ int smi[64];
   __shared__ uint8_t dend[RECON_PAR_MAXT];
   __shared__ int fallback;
@@ -955,10 +969,10 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_recon_par(ReconArgs a) {
     cp_async_commit();
     cp_async_wait<0>();
     __syncthreads();
-    recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback);
+    recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback, a.spec);
     TRACE(6);
   } else {
-    recon_par_body<NW>(a, S, pair, F, R, -1, V, BiasFix{}, smw, smi, dend, &fallback);
+    recon_par_body<NW>(a, S, pair, F, R, -1, V, BiasFix{}, smw, smi, dend, &fallback, a.spec);
     if (a.bias.enabled) {  // signed inputs: correct this stream's coefficients in place
       __syncthreads();
       bias_pass(a.bias, pair, a.h + (long long)pair * a.h_pair_stride, a.out_words, S.pos0, S.pstride, S.count,
@@ -1003,7 +1017,32 @@ __global__ void __launch_bounds__(RECON_PAR_MAXT) k_finrec(FinishArgs fa, ReconA
   cp_async_commit();
   cp_async_wait<0>();
   __syncthreads();
-  recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback);
+  recon_par_body<NW>(a, S, pair, rst, rst + slot, lgV, V, bfx, smw, smi, dend, &fallback, a.spec);
+}
+
+// Exact dynamic shared memory (words) of k_recon_par / k_finrec with T threads:
+// the two padded digit slots of stage_stream and the padded prefix sums of
+// stage_prefix (+1 alignment word), maximised over the launch's streams.
+static size_t recon_stage_words(const ReconArgs& a, int T, bool bias_smem) {
+  size_t best = 0;
+  for (int i = 0; i < a.ns; i++) {
+    const int count = a.s[i].count, nsteps = count - 1;
+    int lgV = 0;
+    while ((T << lgV) < nsteps) lgV++;
+    size_t w = 2 * ((size_t)(count + 1) * a.dwords + (size_t)((count + 1) >> lgV) + 1);
+    if (a.bias.enabled && bias_smem) {
+      const int lgp = lgV + (a.s[i].pstride > 1 ? 1 : 0);
+      const long long ne = (long long)a.bias.lf + a.bias.lg + 2;
+      w += 1 + 2 * (size_t)((ne - 1) + ((ne - 1) >> lgp) + 1);
+    }
+    if (w > best) best = w;
+  }
+  return best + 4;
+}
+
+static int recon_spec() {
+  static const int v = getenv("KMX_RECON_SPEC") ? atoi(getenv("KMX_RECON_SPEC")) : 2;
+  return v;
 }
 
 template <int NW>
@@ -1017,9 +1056,9 @@ static cudaError_t launch_finrec_t(const FinishArgs& fa, const ReconArgs& a, int
   ReconArgs b = a;
   static const int bias_smem = getenv("KMX_RECON_BIAS_SMEM") ? atoi(getenv("KMX_RECON_BIAS_SMEM")) : 1;
   b.bias_smem = bias_smem;
+  b.spec = recon_spec();
   b.stage = 1;
-  size_t smem = (size_t)(2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4) * sizeof(u32);
-  if (a.bias.enabled && bias_smem) smem += (size_t)(4 * (a.bias.lf + a.bias.lg + 2) + 4) * sizeof(u32);
+  const size_t smem = recon_stage_words(a, T, bias_smem) * sizeof(u32);
   if (smem > 160 * 1024) return cudaSuccess;  // not used: too long to stage
   if (smem > 32 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_finrec<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -1221,13 +1260,26 @@ static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStre
   if (T < 32) T = 32;
   if (T > RECON_PAR_MAXT) T = RECON_PAR_MAXT;
   ReconArgs b = a;
-  size_t smem = (size_t)(2 * ((maxcount + 1) * (a.dwords + 1) + 2) + 4) * sizeof(u32);
   // signed path: prefix sums staged in shared memory (default; c2 ks4 recon 68 us)
   // or read from L2 (KMX_RECON_BIAS_SMEM=0: 78 us, the occupancy gain does not pay)
   static const int bias_smem = getenv("KMX_RECON_BIAS_SMEM") ? atoi(getenv("KMX_RECON_BIAS_SMEM")) : 1;
   b.bias_smem = bias_smem;
-  if (a.bias.enabled && bias_smem) smem += (size_t)(4 * (a.bias.lf + a.bias.lg + 2) + 4) * sizeof(u32);
+  b.spec = recon_spec();
+  const size_t smem = recon_stage_words(a, T, bias_smem) * sizeof(u32);
   b.stage = smem <= 160 * 1024;
+  // register-capped instance (KMX_RECON_MINB=0 disables)
+  static const int minb = getenv("KMX_RECON_MINB") ? atoi(getenv("KMX_RECON_MINB")) : 5;
+  if constexpr (NW <= 2) {
+    if (minb > 1 && T <= 128) {
+      auto kern = minb >= 6 ? k_recon_par<NW, 6> : k_recon_par<NW, 5>;
+      if (b.stage && smem > 32 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+      }
+      kern<<<a.batch * a.ns, T, b.stage ? smem : 0, st>>>(b);
+      return cudaGetLastError();
+    }
+  }
   if (b.stage && smem > 32 * 1024) {  // dynamic + ~5 KB static must fit the opt-in limit
     cudaError_t e = cudaFuncSetAttribute(k_recon_par<NW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;

@@ -47,6 +47,8 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   int lmax = 0;
   for (int i = 0; i < a.nops; i++) lmax = a.op[i].len > lmax ? a.op[i].len : lmax;
   PackArgs b = a;
+  static const int fast = getenv("KMX_PACK_FAST") ? atoi(getenv("KMX_PACK_FAST")) : 1;
+  b.fast1 = fast;
   const int nw = (lmax + PK_PAD) * a.in_words;
   b.stage = nw <= PK_STAGE_WORDS;
   const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;

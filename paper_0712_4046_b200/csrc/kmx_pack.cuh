@@ -90,6 +90,20 @@ struct StreamCur {
     t += 32;
     while (t >= S) { t -= S; m++; }
   }
+  // one-word coefficients (b <= 32) at spacing S >= 32: at most the tail of
+  // coefficient m and the head of coefficient m+1 meet a 32-bit window, so
+  // no loops (staged vectors are zero-padded past L)
+  __device__ __forceinline__ void next1(int S) {
+    t += 32;
+    if (t >= S) { t -= S; m++; }
+  }
+  template <class Ctx>
+  __device__ __forceinline__ u32 bits1(const Ctx& C, int par, int S) const {
+    u32 v = (m >= 0 && t < C.b) ? (C.sc[2 * m + par] >> t) : 0u;
+    const int sh = S - t;
+    if (sh < 32) v |= C.sc[2 * (m + 1) + par] << sh;
+    return v;
+  }
   // the 32 bits of this stream in the current digit window
   template <class Ctx>
   __device__ __forceinline__ u32 bits(const Ctx& C, int par, int S) const {
@@ -235,7 +249,22 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
 
   int my_top = 0;
   u32 my_topv = 0u;
-  if (!neg && C.N >= C.b) {
+  const bool fast1 = STAGED && A.fast1 && C.iw == 1 && S >= 32 && C.b <= 32;
+  if (!neg && C.N >= C.b && fast1) {
+    for (int q0 = tid * PK_V; q0 < m; q0 += T * PK_V) {
+      StreamCur ce, co;
+      ce.init(q0, 0, S);
+      co.init(q0, C.N, S);
+#pragma unroll 1
+      for (int v = 0; v < PK_V && q0 + v < m; v++) {
+        const u32 d = ce.bits1(C, 0, S) | co.bits1(C, 1, S);
+        ce.next1(S);
+        co.next1(S);
+        out[q0 + v] = d;
+        if (d) { my_top = q0 + v + 1; my_topv = d; }
+      }
+    }
+  } else if (!neg && C.N >= C.b) {
     // disjoint bit fields (pack.py:66-67): V = E | O, no carries at all --
     // a pure gather, every thread independent
     for (int q0 = tid * PK_V; q0 < m; q0 += T * PK_V) {
@@ -268,12 +297,21 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
     for (int v = 0; v < PK_V; v++) {
       const int q = q0 + v;
       u32 e = 0u, ov = 0u;
-      if (q < m) {
-        e = ce.bits(C, 0, S);
-        ov = co.bits(C, 1, S);
+      if (fast1) {
+        if (q < m) {
+          e = ce.bits1(C, 0, S);
+          ov = co.bits1(C, 1, S);
+        }
+        ce.next1(S);
+        co.next1(S);
+      } else {
+        if (q < m) {
+          e = ce.bits(C, 0, S);
+          ov = co.bits(C, 1, S);
+        }
+        ce.next(S);
+        co.next(S);
       }
-      ce.next(S);
-      co.next(S);
       const i64 x = (!neg ? (i64)e + ov : (order > 0 ? (i64)e - ov : (i64)ov - e)) + c;
       d[v] = (u32)x;
       c = (int)(x >> 32);
@@ -428,6 +466,7 @@ __device__ __forceinline__ void pack_pair(const PackArgs& A, int pair, int o0, i
   const int negative = (order < 0) != flip ? 1 : 0;
   int top0 = 0, top1 = 0;
   u32 topv0 = 0u, topv1 = 0u;
+  const bool fast1 = A.fast1 && C.iw == 1 && S >= 32 && C.b <= 32;
   for (int c0 = 0; c0 < m; c0 += T * PK_V) {
     const int q0 = c0 + tid * PK_V;
     StreamCur ce, co;
@@ -436,15 +475,7 @@ __device__ __forceinline__ void pack_pair(const PackArgs& A, int pair, int o0, i
     u32 d0[PK_V], d1[PK_V];
     int k0 = 0, k1 = 0;
     u32 f0 = 0xffffffffu, a0 = 0u, f1 = 0xffffffffu, a1 = 0u;
-#pragma unroll
-    for (int v = 0; v < PK_V; v++) {
-      u32 e = 0u, ov = 0u;
-      if (q0 + v < m) {
-        e = ce.bits(C, 0, S);
-        ov = co.bits(C, 1, S);
-      }
-      ce.next(S);
-      co.next(S);
+    auto digit = [&](int v, u32 e, u32 ov) {
       const i64 x0 = (i64)e + ov + k0;
       const i64 x1 = (order > 0 ? (i64)e - ov : (i64)ov - e) + k1;
       d0[v] = (u32)x0;
@@ -453,6 +484,31 @@ __device__ __forceinline__ void pack_pair(const PackArgs& A, int pair, int o0, i
       k1 = (int)(x1 >> 32);
       f0 &= d0[v]; a0 |= d0[v];
       f1 &= d1[v]; a1 |= d1[v];
+    };
+    if (fast1) {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++) {
+        u32 e = 0u, ov = 0u;
+        if (q0 + v < m) {
+          e = ce.bits1(C, 0, S);
+          ov = co.bits1(C, 1, S);
+        }
+        ce.next1(S);
+        co.next1(S);
+        digit(v, e, ov);
+      }
+    } else {
+#pragma unroll
+      for (int v = 0; v < PK_V; v++) {
+        u32 e = 0u, ov = 0u;
+        if (q0 + v < m) {
+          e = ce.bits(C, 0, S);
+          ov = co.bits(C, 1, S);
+        }
+        ce.next(S);
+        co.next(S);
+        digit(v, e, ov);
+      }
     }
     // thread carry maps (c0 - all0, c0, c0 + allF), one block scan per stream
     const u32 M0 = (u32)(k0 - (a0 == 0u ? 1 : 0) + 1) | ((u32)(k0 + 1) << 2) |

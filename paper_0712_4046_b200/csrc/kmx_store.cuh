@@ -13,12 +13,13 @@ __device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int1
   u64 lo = (u64)hp, hi = (u64)(hp >> 64);
   if (bf.enabled) {
     const unsigned long long* PF = bf.pf + pair * bf.pair_stride;
-    const long long lf = bf.lf, lg = bf.lg;
-    const long long i0 = k - lg + 1 > 0 ? k - lg + 1 : 0, i1 = k < lf - 1 ? k : lf - 1;
-    const long long j0 = k - lf + 1 > 0 ? k - lf + 1 : 0, j1 = k < lg - 1 ? k : lg - 1;
+    // coefficient indices < 2^31: 32-bit index arithmetic
+    const int kk = (int)k, lf = bf.lf, lg = bf.lg, lgp = bf.lgpad;
+    const int i0 = max(kk - lg + 1, 0), i1 = min(kk, lf - 1);
+    const int j0 = max(kk - lf + 1, 0), j1 = min(kk, lg - 1);
     // staged copies are padded: entry i at i + (i >> lgpad) (PG follows PF)
-    auto pe = [&](long long i) -> u64 { return PF[bf.lgpad >= 0 ? i + (i >> bf.lgpad) : i]; };
-    const long long g0 = lf + 1;
+    auto pe = [&](int i) -> u64 { return PF[lgp >= 0 ? i + (i >> lgp) : i]; };
+    const int g0 = lf + 1;
     const u64 S = (pe(i1 + 1) - pe(i0)) + (pe(g0 + j1 + 1) - pe(g0 + j0));
     const u64 cnt = (u64)(i1 - i0 + 1);
     const int sh1 = bf.b - 1, sh2 = 2 * bf.b - 2;       // 0..31, 0..62

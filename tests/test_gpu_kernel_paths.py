@@ -25,6 +25,9 @@ SETTINGS = [
     {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands)
     {"KMX_TC": "1", "KMX_TCJ": "1", "KMX_PACK_PAIR": "2"},  # chunked single-tile tensor-core kernel; paired packs at every batch size
     {"KMX_RECON_BIAS_SMEM": "0", "KMX_RECON_WARP": "1"},  # signed prefix sums from L2; warp-per-stream recon
+    {"KMX_RECON_SPEC": "1", "KMX_RECON_MINB": "0"},  # recon: speculative stores from round 1; uncapped registers
+    {"KMX_RECON_SPEC": "0", "KMX_PACK_FAST": "0"},  # recon: separate output walk; looped pack windows only
+    {"KMX_RECON_MINB": "6", "KMX_RECON_V": "4"},  # recon: 6-CTA register cap; 4 steps per thread
 ]
 
 
