@@ -194,6 +194,8 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
       // the chunk (bit >= 0), so chunk-local 32-bit positions, one funnel
       // shift per word and no range tests
       const int ib = (int)(base + jl * W);
+      const bool two = S.mode == 1 && a.dwords == 2 && Wd == 2;
+      const u32 m1 = W >= 64 ? 0xffffffffu : ((1u << (W - 32)) - 1u);
       for (int jj = lane; jj < (int)(jh - jl); jj += 32) {
         const int j = (int)jl + jj;
         const int lb = ib + jj * W;
@@ -210,8 +212,20 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
         } else {
           const int idx = S.reversed ? (S.cnt - 1 - j) : j;
           u32* dp = dbase + sink.off(idx, 0);
+          if (two) {  // 33..64-bit digits: three words, two funnel shifts
+            const int q = lb >> 5, sb = lb & 31;
+            const u32 w0 = buf[q], w1 = buf[q + 1], w2 = q + 2 < FIN_HALO + FW_CH ? buf[q + 2] : 0u;
+            const u32 x0 = __funnelshift_r(w0, w1, sb), x1 = __funnelshift_r(w1, w2, sb) & m1;
+            if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) {
+              *reinterpret_cast<uint2*>(dp) = make_uint2(x0, x1);
+            } else {
+              dp[0] = x0;
+              dp[1] = x1;
+            }
+          } else {
 #pragma unroll 2
-          for (int w = 0; w < a.dwords; w++) dp[w] = w < Wd ? dig_word(buf, lb, w, W) : 0u;
+            for (int w = 0; w < a.dwords; w++) dp[w] = w < Wd ? dig_word(buf, lb, w, W) : 0u;
+          }
         }
       }
     } else

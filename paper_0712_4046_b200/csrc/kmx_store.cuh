@@ -17,8 +17,15 @@ __device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int1
     const int kk = (int)k, lf = bf.lf, lg = bf.lg, lgp = bf.lgpad;
     const int i0 = max(kk - lg + 1, 0), i1 = min(kk, lf - 1);
     const int j0 = max(kk - lf + 1, 0), j1 = min(kk, lg - 1);
-    // staged copies are padded: entry i at i + (i >> lgpad) (PG follows PF)
-    auto pe = [&](int i) -> u64 { return PF[lgp >= 0 ? i + (i >> lgp) : i]; };
+    // staged copies (lgpad >= 0) live in shared memory, padded: entry i at
+    // i + (i >> lgpad) (PG follows PF); read them with ld.shared
+    const u32 sbase = lgp >= 0 ? (u32)__cvta_generic_to_shared(PF) : 0u;
+    auto pe = [&](int i) -> u64 {
+      if (lgp < 0) return PF[i];
+      u64 v;
+      asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sbase + 8u * (u32)(i + (i >> lgp))));
+      return v;
+    };
     const int g0 = lf + 1;
     const u64 S = (pe(i1 + 1) - pe(i0)) + (pe(g0 + j1 + 1) - pe(g0 + j0));
     const u64 cnt = (u64)(i1 - i0 + 1);
