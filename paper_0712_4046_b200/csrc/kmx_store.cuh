@@ -21,7 +21,7 @@ __device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int1
     // i + (i >> lgpad) (PG follows PF); read them with ld.shared
     const u32 sbase = lgp >= 0 ? (u32)__cvta_generic_to_shared(PF) : 0u;
     auto pe = [&](int i) -> u64 {
-      if (lgp < 0) return PF[i];
+      if (lgp < 0) return __ldg(PF + i);  // read-only for the kernel: loads may move above the stores
       u64 v;
       asm volatile("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(sbase + 8u * (u32)(i + (i >> lgp))));
       return v;
