@@ -289,6 +289,32 @@ __global__ void __launch_bounds__(32 * FW_WARPS) k_finchunk(FinishArgs a, long l
   u32* hpair = a.h + (long long)pair * a.h_pair_stride;
   u32* dbase = F.S.mode == 1 ? sink.base(F.S, pair) : nullptr;
   const int W = F.W, Wd = F.Wd;
+  if (W <= 32 * FIN_HALO) {
+    // lean extraction (as finish_warp_stream): chunk-local 32-bit positions,
+    // one funnel shift per word; digits start inside the chunk and end in
+    // the upper halo at the latest
+    const int ib = (int)(base + jl * W);
+    for (int jj = lane; jj < (int)(jh - jl); jj += 32) {
+      const int j = (int)jl + jj;
+      const int lb = ib + jj * W;
+      if (F.S.mode == 0) {
+        const long long kpos = F.S.pos0 + (long long)j * F.S.pstride;
+        u32* dst = hpair + kpos * a.out_words;
+        if (a.bias.enabled) {
+          unsigned __int128 hp = 0;
+          for (int w = 0; w < Wd && w < 4; w++) hp |= (unsigned __int128)dig_word(buf, lb, w, W) << (32 * w);
+          store_coeff128(dst, a.out_words, hp, kpos, a.bias, pair);
+        } else {
+          for (int w = 0; w < a.out_words; w++) dst[w] = w < Wd ? dig_word(buf, lb, w, W) : 0u;
+        }
+      } else {
+        const int idx = F.S.reversed ? (F.S.cnt - 1 - j) : j;
+        u32* dp = dbase + sink.off(idx, 0);
+        for (int w = 0; w < a.dwords; w++) dp[w] = w < Wd ? dig_word(buf, lb, w, W) : 0u;
+      }
+    }
+    return;
+  }
   for (long long j = jl + lane; j < jh; j += 32) {
     const long long lb = base + j * W;
     if (F.S.mode == 0) {
