@@ -90,18 +90,30 @@ struct StreamCur {
     t += 32;
     while (t >= S) { t -= S; m++; }
   }
-  // one-word coefficients (b <= 32) at spacing S >= 32: at most the tail of
-  // coefficient m and the head of coefficient m+1 meet a 32-bit window, so
-  // no loops (staged vectors are zero-padded past L)
+  // spacing S >= 32 (and S >= b, as always): at most the tail of coefficient
+  // m and the head of coefficient m+1 meet a 32-bit window, so no loops
+  // (staged vectors are zero-padded past L; bits at or above b are zero)
   __device__ __forceinline__ void next1(int S) {
     t += 32;
     if (t >= S) { t -= S; m++; }
   }
   template <class Ctx>
-  __device__ __forceinline__ u32 bits1(const Ctx& C, int par, int S) const {
+  __device__ __forceinline__ u32 bits1(const Ctx& C, int par, int S) const {  // one-word coefficients
     u32 v = (m >= 0 && t < C.b) ? (C.sc[2 * m + par] >> t) : 0u;
     const int sh = S - t;
     if (sh < 32) v |= C.sc[2 * (m + 1) + par] << sh;
+    return v;
+  }
+  template <class Ctx>
+  __device__ __forceinline__ u32 bitsw(const Ctx& C, int par, int S) const {  // multi-word coefficients
+    u32 v = 0u;
+    if (m >= 0 && t < C.b) {
+      const int wq = t >> 5;
+      const u32* p = C.sc + (2 * m + par) * C.iw + wq;
+      v = __funnelshift_r(p[0], wq + 1 < C.iw ? p[1] : 0u, t & 31);
+    }
+    const int sh = S - t;
+    if (sh < 32) v |= C.sc[(2 * (m + 1) + par) * C.iw] << sh;
     return v;
   }
   // the 32 bits of this stream in the current digit window
@@ -249,15 +261,19 @@ __device__ __forceinline__ void pack_op(const PackArgs& A, int pair, int o, u32*
 
   int my_top = 0;
   u32 my_topv = 0u;
-  const bool fast1 = STAGED && A.fast1 && C.iw == 1 && S >= 32 && C.b <= 32;
-  if (!neg && C.N >= C.b && fast1) {
+  // loop-free windows: every width in the carry-free disjoint path; one-word
+  // coefficients only in the carry path (multi-word there measured slower:
+  // c1 ks3/ks4 pack 19 -> 21 us)
+  const bool fastw = STAGED && A.fast1 && S >= 32 && C.b <= S;
+  const bool fast1 = fastw && C.iw == 1;
+  if (!neg && C.N >= C.b && fastw) {
     for (int q0 = tid * PK_V; q0 < m; q0 += T * PK_V) {
       StreamCur ce, co;
       ce.init(q0, 0, S);
       co.init(q0, C.N, S);
 #pragma unroll 1
       for (int v = 0; v < PK_V && q0 + v < m; v++) {
-        const u32 d = ce.bits1(C, 0, S) | co.bits1(C, 1, S);
+        const u32 d = fast1 ? (ce.bits1(C, 0, S) | co.bits1(C, 1, S)) : (ce.bitsw(C, 0, S) | co.bitsw(C, 1, S));
         ce.next1(S);
         co.next1(S);
         out[q0 + v] = d;
@@ -466,7 +482,10 @@ __device__ __forceinline__ void pack_pair(const PackArgs& A, int pair, int o0, i
   const int negative = (order < 0) != flip ? 1 : 0;
   int top0 = 0, top1 = 0;
   u32 topv0 = 0u, topv1 = 0u;
-  const bool fast1 = A.fast1 && C.iw == 1 && S >= 32 && C.b <= 32;
+  // loop-free windows for one-word coefficients only: with multi-word
+  // coefficients (c1, b = 64) the extra loop variant costs this kernel more
+  // than it saves (c1 ks3/ks4 pack 19 -> 21 us); pack_op takes them
+  const bool fast1 = A.fast1 && S >= 32 && C.b <= S && C.iw == 1;
   for (int c0 = 0; c0 < m; c0 += T * PK_V) {
     const int q0 = c0 + tid * PK_V;
     StreamCur ce, co;
