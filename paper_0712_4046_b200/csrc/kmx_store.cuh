@@ -38,6 +38,16 @@ __device__ __forceinline__ void store_coeff128(u32* dst, int ow, unsigned __int1
     hi = h1 + c_hi + (lo < l1 ? 1ull : 0ull);
   }
   const u32 ext = (hi >> 63) ? 0xffffffffu : 0u;
+  if (ow == 3) {  // 12-byte records (c2): one 8-byte and one 4-byte store
+    if ((reinterpret_cast<uintptr_t>(dst) & 7) == 0) {
+      *reinterpret_cast<uint2*>(dst) = make_uint2((u32)lo, (u32)(lo >> 32));
+      dst[2] = (u32)hi;
+    } else {
+      dst[0] = (u32)lo;
+      *reinterpret_cast<uint2*>(dst + 1) = make_uint2((u32)(lo >> 32), (u32)hi);
+    }
+    return;
+  }
   dst[0] = (u32)lo;
   if (ow > 1) dst[1] = (u32)(lo >> 32);
   if (ow > 2) dst[2] = (u32)hi;
