@@ -2,28 +2,38 @@
 """Benchmark of the multipoint Kronecker-substitution hot path on B200.
 
 Metric (BASELINE.json): polynomial products per second per KS variant, with
-the multiply kernel's fraction of its measured peak: the dense tcgen05 u8 MMA
-rate when it runs on the tensor cores (kmx_tc.cu), the IMAD.WIDE.U32 rate
-when it runs on the integer pipe (kmx_mul.cu).
-Default workload = BASELINE config 2 (configs[1]): Z[x], signed int32
-coefficients, batch 1024 pairs, n = 1024.  A step = one pass of the hot path
-(pack -> multiply -> finish [-> reconstruct] -> bias) over the whole batch.
+the multiply kernel's fraction of its measured peak (dense tcgen05 u8 MMA rate
+on the tensor cores, IMAD.WIDE.U32 rate on the integer pipe) and the HBM
+fractions of the pack / finish / reconstruction kernels.
+
+Headline workload = BASELINE config 2 (configs[1]): Z[x], signed int32
+coefficients, batch 1024 pairs, n = 1024, variant ks4.  A step = one pass of
+the hot path (pack -> multiply -> finish [-> reconstruct]) over the whole
+batch.  The default single-GPU run also measures every other BASELINE config
+under the same clock and prints them inside the same JSON line:
+``per_config`` (c1, c3, c4: all four variants, kernel split, rooflines, e2e,
+parity) and ``c5`` (the 30-point crossover sweep, all four variants, parity
+per point).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config c1|c2|c3|c4]
-                  [--variant 1..4] [--impl ours|reference]
+                  [--variant 1..4] [--impl ours|reference] [--quick]
 
-One JSON line on rank 0.  N > 1 runs under torchrun: every rank multiplies
-its own batch (independent pairs, no collective on the data path: weak
-scaling); the step time is the max over ranks.  ``--impl reference`` times the
-reference algorithm's CPU implementation (the oracle port of kronmul, since
-the reference is pure Python and /root/reference is absent on the GPU box)
-on all host cores of rank 0.
+One JSON line on rank 0.  ``--gpus N`` (N > 1) without a torchrun
+environment relaunches itself under torch.distributed.run with N ranks; every
+rank multiplies its own batch (independent pairs, no collective on the data
+path: weak scaling) and the step time is the max over ranks.
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port of kronmul, within 0-10% of the reference's own time,
+profiles/r02/port_vs_reference.json) on all host cores of rank 0.
 """
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
+import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -35,6 +45,7 @@ sys.path.insert(0, ROOT)
 METRIC = "poly products/sec per KS variant; fraction of the tensor (or IMAD) peak and HBM roofline"
 VNAME = {1: "ks1", 2: "ks2", 3: "ks3", 4: "ks4"}
 VDESC = {1: "standard 2^N", 2: "reciprocal 2^N,2^-N", 3: "negated +-2^N", 4: "four-point +-2^N,+-2^-N"}
+PCOUNT = {1: 1, 2: 2, 3: 2, 4: 4}
 CONFIGS = {
     "c1": dict(kind="ks", batch=64, n=256, b=64, signed=False, seed=1,
                desc="c1: Z[x] u64 coefficients, batch 64, n=256"),
@@ -45,7 +56,15 @@ CONFIGS = {
     "c4": dict(kind="ks", batch=32, n=4096, b=128, signed=False, seed=4,
                desc="c4: Z[x] u128 coefficients, batch 32, n=4096"),
 }
+C5_NS = (16, 64, 256, 1024, 4096, 8192)
+C5_BITS = (8, 32, 64, 128, 256)
 L2_FLUSH_BYTES = 256 << 20
+
+
+def c5_config(n, b, scale=1):
+    B = int(math.ceil(1e6 / (2 * n - 1))) * scale
+    return dict(kind="ks", batch=B, n=n, b=b, signed=False, seed=5000 + 17 * n + b,
+                desc=f"c5: Z[x] u{b}, batch {B}, n={n}")
 
 
 # ------------------------------------------------------------------ inputs
@@ -86,44 +105,63 @@ def to_ints(arr, signed):
     return out
 
 
+# ------------------------------------------------------------ work / bytes
+def ks_geometry(cfg, variant):
+    """Derived sizes of one pair (kmx_ks_params, ksint.py:82-98): the variant
+    actually run (KS4 -> KS1 fallback), P, operand limbs, digit streams."""
+    from paper_0712_4046_b200 import _lib
+    p = (ctypes.c_int64 * 8)()
+    flags = _lib.KMX_SIGNED if cfg["signed"] else 0
+    n, b = cfg["n"], cfg["b"]
+    _lib.check(_lib.lib().kmx_ks_params(variant, n, n, b, flags, p))
+    e, N1, N2, N4, safe, k = (int(p[i]) for i in range(6))
+    v = variant
+    if v == 4 and (not safe or k == 1):
+        v = 1
+    ne, no = (k + 1) // 2, k // 2
+    if v == 2:  # fwd/rev, k+1 digits of N2 bits
+        streams = [(k + 1, N2)] * 2
+    elif v == 4:  # fwd/rev even and odd, n_even+1 / n_odd+1 digits of 2 N4 bits
+        streams = [(ne + 1, 2 * N4), (no + 1, 2 * N4)] * 2
+    else:
+        streams = []
+    ow = _lib.lib().kmx_ks_out_words(n, n, b, flags)
+    return dict(variant=v, P=PCOUNT[v], mf=int(p[6]), mg=int(p[7]), streams=streams, out_words=ow,
+                in_words=1 if cfg["signed"] else (b + 31) // 32, k=k)
+
+
 def algorithmic_products(cfg, variant):
     """Schoolbook 32x32 limb products per pair: sum over the
-    sub-products of m_f * m_g, m = ceil((N (L-1) + b + 2) / 32) limbs."""
-    import ctypes
-    from paper_0712_4046_b200 import _lib
+    sub-products of m_f * m_g, m = ceil((N (L-1) + b + 2) / 32) limbs; for the
+    bivariate config the coefficient MACs of the univariate products."""
     if cfg["kind"] == "bks":
         lx, ly = cfg["lx"], cfg["ly"]
         Lu = {1: (2 * lx - 1) * (ly - 1) + lx, 2: lx * ly, 3: lx * ly, 4: (lx + 1) // 2 * (ly - 1) + lx}[variant]
-        P = {1: 1, 2: 2, 3: 2, 4: 4}[variant]
-        return P * Lu * Lu
-    p = (ctypes.c_int64 * 8)()
-    flags = _lib.KMX_SIGNED if cfg["signed"] else 0
-    _lib.check(_lib.lib().kmx_ks_params(variant, cfg["n"], cfg["n"], cfg["b"], flags, p))
-    eff_variant = variant
-    if variant == 4 and (not p[4] or p[5] == 1):
-        eff_variant = 1
-    P = {1: 1, 2: 2, 3: 2, 4: 4}[eff_variant]
-    return P * int(p[6]) * int(p[7])
+        return PCOUNT[variant] * Lu * Lu
+    g = ks_geometry(cfg, variant)
+    return g["P"] * g["mf"] * g["mg"]
 
 
-def pack_unpack_bytes(cfg, variant):
-    """Algorithmic HBM bytes of one step outside the multiply: inputs + packed
-    operands (pack), products + outputs (finish), digit streams (recon)."""
-    import ctypes
-    from paper_0712_4046_b200 import _lib
+def hbm_bytes(cfg, variant):
+    """Algorithmic HBM bytes per step of the kernels around the multiply:
+    pack reads the inputs once and writes the packed operands; finish reads
+    the products and writes the coefficients (ks1/ks3) or the digit streams
+    (ks2/ks4); reconstruction reads the digit streams and writes the
+    coefficients."""
     if cfg["kind"] == "bks":
         return None
-    p = (ctypes.c_int64 * 8)()
-    flags = _lib.KMX_SIGNED if cfg["signed"] else 0
-    _lib.check(_lib.lib().kmx_ks_params(variant, cfg["n"], cfg["n"], cfg["b"], flags, p))
-    P = {1: 1, 2: 2, 3: 2, 4: 4}[variant]
+    g = ks_geometry(cfg, variant)
     B, n = cfg["batch"], cfg["n"]
-    iw = 1 if cfg["signed"] else (cfg["b"] + 31) // 32
-    ow = _lib.lib().kmx_ks_out_words(n, n, cfg["b"], flags)
-    mf, mg = int(p[6]), int(p[7])
-    pack = B * (2 * n * iw * 4 * P + P * (mf + mg) * 4)
-    fin = B * (P * (mf + mg) * 4 + (2 * n - 1) * ow * 4)
-    return {"pack_bytes": pack, "finish_bytes": fin}
+    inputs = 2 * n * g["in_words"] * 4
+    operands = g["P"] * (g["mf"] + g["mg"]) * 4
+    coeffs = g["k"] * g["out_words"] * 4
+    digits = sum(cnt * ((w + 31) // 32) * 4 for cnt, w in g["streams"])
+    out = {"pack": B * (inputs + operands),
+           "finish": B * (operands + (digits if g["streams"] else coeffs))}
+    if g["streams"]:
+        out["recon"] = B * (digits + coeffs)
+        out["fused"] = B * (operands + coeffs)  # k_finrec: the digit streams stay on chip
+    return out
 
 
 # -------------------------------------------------------------- multi-rank
@@ -145,6 +183,21 @@ def max_over_ranks(x, dist=None, device=None):
 def job_products(batch_per_rank, world):
     """Weak scaling: every rank multiplies its own batch of independent pairs."""
     return batch_per_rank * world
+
+
+def free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_under_torchrun(n):
+    """``--gpus N`` outside torchrun: run N ranks (one per GPU) under
+    torch.distributed.run on this node; rank 0 prints the line."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__),
+           *sys.argv[1:]]
+    return subprocess.call(cmd)
 
 
 # ------------------------------------------------------------------ clocks
@@ -194,197 +247,361 @@ class ClockMonitor:
 
 
 # ---------------------------------------------------------- GPU measurement
-def run_ours(args, cfg, rank, world, local_rank):
-    import numpy as np
-    import torch
+class Gpu:
+    """Per-process measurement context: device, L2 flush buffer, live peaks."""
 
-    import paper_0712_4046_b200 as kmx
-    from paper_0712_4046_b200 import _lib
+    def __init__(self, local_rank, dist=None):
+        import torch
 
-    dev = torch.device("cuda", local_rank)
-    torch.cuda.set_device(dev)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        import paper_0712_4046_b200 as kmx
+        from paper_0712_4046_b200 import _lib
+        self.torch, self.kmx, self._lib = torch, kmx, _lib
+        self.dev = torch.device("cuda", local_rank)
+        torch.cuda.set_device(self.dev)
+        self.dist = dist
+        self.L = _lib.lib()
+        self.flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=self.dev)
+        self.stream = torch.cuda.current_stream(self.dev)
+        self.imad = kmx.imad_peak(4096)  # live IMAD.WIDE.U32 microbenchmark (limb products/s)
+        self.tensor = kmx.tc_peak(2000)  # live dense tcgen05 u8 MMA microbenchmark (MAC/s)
+        try:
+            self.hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
+            self.hbm_src = "MEASURED_PEAKS.json hbm_gbs"
+        except Exception:
+            self.hbm, self.hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
+    def barrier(self):
+        if self.dist is not None:
+            self.dist.barrier()
+        self.torch.cuda.synchronize()
 
-    def mor(x):
-        return max_over_ranks(x, dist, dev)
+    def mor(self, x):
+        return max_over_ranks(x, self.dist, self.dev)
 
-    fh, gh = make_inputs(cfg, rank)
-    signed = cfg.get("signed", False)
-    B = cfg["batch"]
-    flush_buf = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.int32, device=dev)
-    stream = torch.cuda.current_stream(dev)
-    L = _lib.lib()
-    peak = kmx.imad_peak(4096)  # live IMAD.WIDE.U32 microbenchmark, same process and clocks
-    tpeak = kmx.tc_peak(2000)   # live dense tcgen05 u8 MMA microbenchmark (MAC/s)
+    def traffic(self, cfg_name, variant, key):
+        """Per-launch DRAM bytes of a kernel from the committed ncu capture
+        (profiles/ncu_traffic.json, captured at the commit it names)."""
+        try:
+            d = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+            return d["configs"][cfg_name][VNAME[variant]][key]
+        except Exception:
+            return None
 
-    variants = [args.variant] + [v for v in (1, 2, 3, 4) if v != args.variant] if args.all_variants else [args.variant]
-    per_variant = {}
-    clocks = None
-    headline = None
-    for vi, v in enumerate(variants):
-        if cfg["kind"] == "bks":
-            op = kmx.BksBatch(v, B, cfg["lx"], cfg["ly"], cfg["b"], device=dev)
-            fd = torch.from_numpy(fh).to(dev)
-            gd = torch.from_numpy(gh).to(dev)
-            out = torch.empty((B, 2 * cfg["lx"] - 1, 2 * cfg["ly"] - 1), dtype=torch.int64, device=dev)
-        else:
-            op = kmx.KsBatch(v, B, cfg["n"], cfg["n"], cfg["b"], signed=signed, device=dev)
-            fd = torch.from_numpy(fh.view(np.int32)).to(dev)
-            gd = torch.from_numpy(gh.view(np.int32)).to(dev)
-            out = op.empty_out()
-        for _ in range(args.warmup):
-            op(fd, gd, out)
+
+def _op_for(g, cfg, v):
+    torch, kmx = g.torch, g.kmx
+    if cfg["kind"] == "bks":
+        op = kmx.BksBatch(v, cfg["batch"], cfg["lx"], cfg["ly"], cfg["b"], device=g.dev)
+        out = torch.empty((cfg["batch"], 2 * cfg["lx"] - 1, 2 * cfg["ly"] - 1), dtype=torch.int64, device=g.dev)
+    else:
+        op = kmx.KsBatch(v, cfg["batch"], cfg["n"], cfg["n"], cfg["b"], signed=cfg.get("signed", False),
+                         device=g.dev)
+        out = op.empty_out()
+    return op, out
+
+
+KS_SLOTS = ["pack", "mul", "finish", "recon", "bias"]
+BKS_SLOTS = ["beval", "conv", "brecover"]
+
+
+def kernel_split(g, op, fd, gd, out, steps):
+    """Per-kernel durations: CUDA events recorded on the launch stream around
+    each launch (kmx_prof_*), eager calls with the L2 flushed before each."""
+    prof = (ctypes.c_float * 6)()
+    kern = [0.0] * 6
+    g.L.kmx_prof_enable(1)
+    op(fd, gd, out)  # untimed: the unsplit shape's first call (plan autotuning)
+    g.L.kmx_prof_read(prof, 6)
+    for _ in range(steps):
+        g.flush.fill_(1)
+        op(fd, gd, out)
+        g.L.kmx_prof_read(prof, 6)
+        for i in range(6):
+            kern[i] += prof[i]
+    g.L.kmx_prof_enable(0)
+    return [k / steps for k in kern]
+
+
+def measure_variant(g, cfg, cfg_name, v, fd, gd, steps, warmup, graphs=True, monitor=None):
+    """Device-timed products/s of one variant (CUDA-graph replay, L2 flushed
+    between timed steps, CUDA events on the launch stream, max over ranks),
+    plus the per-kernel split and the rooflines.  Returns (record, output)."""
+    torch = g.torch
+    op, out = _op_for(g, cfg, v)
+    for _ in range(warmup):
+        op(fd, gd, out)
+    op.status()
+    graph = None
+    if graphs:
+        graph, out = op.capture(fd, gd, out)
+        graph.replay()
         op.status()
-        graph = None
-        if args.graphs:  # CUDA graph of the whole step (no per-kernel launch gaps)
-            graph, out = op.capture(fd, gd, out)
-            graph.replay()
-            op.status()
-        L.kmx_prof_enable(1)
-        import ctypes
-        prof = (ctypes.c_float * 6)()
-        kern = [0.0] * 6
-        mon = None
-        if vi == 0 and rank == 0:
-            mon = ClockMonitor(local_rank)
-            mon.start()
-        barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        total_ms = 0.0
-        launches = 0
-        for _ in range(args.steps):
-            flush_buf.fill_(1)  # L2 flush between timed steps (untimed)
-            e0.record(stream)
-            if graph is not None:
-                graph.replay()
-            else:
-                op(fd, gd, out)
-            e1.record(stream)
-            e1.synchronize()
-            total_ms += e0.elapsed_time(e1)
-            launches += L.kmx_last_launch_count()
-            if graph is None:
-                L.kmx_prof_read(prof, 6)
-                for i in range(6):
-                    kern[i] += prof[i]
-        barrier()
-        L.kmx_prof_enable(0)
-        if mon is not None:
-            clocks = mon.stop()
-        op.status()
+    launches = g.L.kmx_last_launch_count()
+    if monitor is not None:
+        monitor.start()
+    g.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    total_ms = 0.0
+    for _ in range(steps):
+        g.flush.fill_(1)  # L2 flush between timed steps (untimed)
+        e0.record(g.stream)
         if graph is not None:
-            # per-kernel durations: CUDA events around each launch (kmx_prof),
-            # eager launches right after the graph-timed region
-            L.kmx_prof_enable(1)
-            op(fd, gd, out)  # untimed: the unsplit shape's first call (plan autotuning)
-            L.kmx_prof_read(prof, 6)
-            for _ in range(args.steps):
-                flush_buf.fill_(1)
-                op(fd, gd, out)
-                L.kmx_prof_read(prof, 6)
-                for i in range(6):
-                    kern[i] += prof[i]
-            L.kmx_prof_enable(0)
-        total_ms = mor(total_ms)
-        ms = total_ms / args.steps
-        rec = {"products_per_s": job_products(B, world) / (ms * 1e-3), "ms_per_step": ms, "launches_per_step": launches / args.steps}
-        if cfg["kind"] == "bks":
-            names = ["beval", "conv", "brecover"]
-            rec["kernel_ms"] = {nm: kern[i] / args.steps for i, nm in enumerate(names) if kern[i] > 0}
-            conv_ms = kern[1] / args.steps
-            if conv_ms > 0:  # one IMAD.WIDE (int32 x int32 -> int64) per coefficient MAC
-                rec["conv_macs_per_s"] = algorithmic_products(cfg, v) * B / (conv_ms * 1e-3)
-                rec["conv_frac_of_imad_peak"] = rec["conv_macs_per_s"] / peak
-        if cfg["kind"] == "ks":
-            names = ["pack", "mul", "finish", "recon", "bias"]
-            rec["kernel_ms"] = {nm: kern[i] / args.steps for i, nm in enumerate(names) if kern[i] > 0}
-            if "recon" in rec["kernel_ms"] and "finish" not in rec["kernel_ms"]:  # K3 + K4 fused (k_finrec)
-                rec["kernel_ms"]["finish+recon (fused)"] = rec["kernel_ms"].pop("recon")
-            prods = algorithmic_products(cfg, v) * B
-            mul_ms = kern[1] / args.steps
-            rec["mul_limb_products_per_s"] = prods / (mul_ms * 1e-3) if mul_ms > 0 else None
-            rec["mul_frac_of_imad_peak"] = rec["mul_limb_products_per_s"] / peak if mul_ms > 0 else None
-            rec["mul_engine"] = kmx.mul_engine(v, cfg["n"], cfg["n"], cfg["b"], signed=signed)
-            plan = (ctypes.c_int64 * 8)()
-            if L.kmx_mul_plan(v, B, cfg["n"], cfg["n"], cfg["b"], _lib.KMX_SIGNED if signed else 0, plan) == 0:
-                rec["mul_plan"] = {"engine": ["imad", "tensor tiled", "tensor chunked"][int(plan[0])],
-                                   "H": int(plan[1]), "NW": int(plan[2]), "KC": int(plan[3]), "TPC": int(plan[4]),
-                                   "mmas_per_product": int(plan[5]), "smem_bytes_per_product": int(plan[6]),
-                                   "issued_byte_macs_per_product": int(plan[7])}
-            if rec["mul_engine"] == "tensor" and mul_ms > 0:
-                # algorithmic byte MACs of the u8 convolution: 16 per 32x32 limb product
-                rec["mul_frac_of_tensor_peak"] = 16.0 * rec["mul_limb_products_per_s"] / tpeak
-        per_variant[VNAME[v]] = rec
-        if vi == 0:
-            headline = (v, rec, op, fd, gd, out, launches)
-        del op
-    v, rec, op, fd, gd, out, launches = headline
-    peaks = {"imad": peak, "tensor": tpeak}
+            graph.replay()
+        else:
+            op(fd, gd, out)
+        e1.record(g.stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    g.barrier()
+    clocks = monitor.stop() if monitor is not None else None
+    op.status()
+    kern = kernel_split(g, op, fd, gd, out, steps)
+    op.status()
+    world = 1 if g.dist is None else g.dist.get_world_size()
+    ms = g.mor(total_ms) / steps
+    B = cfg["batch"]
+    rec = {"products_per_s": job_products(B, world) / (ms * 1e-3), "ms_per_step": ms,
+           "gpu_launches_per_step": launches}
+    if cfg["kind"] == "bks":
+        rec["kernel_ms"] = {nm: kern[i] for i, nm in enumerate(BKS_SLOTS) if kern[i] > 0}
+        conv_ms = kern[1]
+        macs = algorithmic_products(cfg, v) * B
+        ach = macs / (conv_ms * 1e-3) if conv_ms > 0 else None
+        rec["roofline"] = {"bound": "imad", "kernel": "k_conv (int32 x int32 -> int64 IMAD.WIDE convolution)",
+                           "achieved": ach / 1e9 if ach else None, "peak": g.imad / 1e9, "unit": "G MAC/s",
+                           "frac": ach / g.imad if ach else None,
+                           "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
+                           "algorithmic_work": f"{macs} coefficient MACs per launch "
+                                               f"({algorithmic_products(cfg, v)} per pair x {B})",
+                           "traffic": g.traffic(cfg_name, v, "conv_dram_bytes")}
+    else:
+        km = {nm: kern[i] for i, nm in enumerate(KS_SLOTS) if kern[i] > 0}
+        if "recon" in km and "finish" not in km:  # K3 + K4 fused (k_finrec)
+            km["finish+recon (fused)"] = km.pop("recon")
+        rec["kernel_ms"] = km
+        rec["roofline"] = mul_roofline(g, cfg, cfg_name, v, km.get("mul"), clocks)
+        rec["roofline_hbm"] = hbm_roofline(g, cfg, v, km)
+    if clocks is not None:
+        rec["clocks"] = clocks
+    return rec, out, op
 
-    # ---- end to end through the public host API (pinned host buffers)
-    e2e = None
+
+def mul_roofline(g, cfg, cfg_name, v, mul_ms, clocks):
+    """K2's roofline: the tcgen05 byte convolution against the live dense u8
+    MMA peak, or the integer-pipe schoolbook against the live IMAD peak."""
+    from paper_0712_4046_b200 import _lib
+    if not mul_ms:
+        return None
+    B = cfg["batch"]
+    prods = algorithmic_products(cfg, v) * B
+    lps = prods / (mul_ms * 1e-3)
+    flags = _lib.KMX_SIGNED if cfg["signed"] else 0
+    plan = (ctypes.c_int64 * 8)()
+    eng = g.kmx.mul_engine(v, cfg["n"], cfg["n"], cfg["b"], signed=cfg["signed"])
+    karatsuba = None
+    info = {}
+    if g.L.kmx_mul_plan(v, B, cfg["n"], cfg["n"], cfg["b"], flags, plan) == 0:
+        info = {"engine": ["imad", "tensor tiled", "tensor chunked", "karatsuba"][min(3, int(plan[0]))],
+                "H": int(plan[1]), "NW": int(plan[2]), "KC": int(plan[3]), "TPC": int(plan[4]),
+                "mmas_per_product": int(plan[5]), "smem_bytes_per_product": int(plan[6]),
+                "issued_byte_macs_per_product": int(plan[7])}
+    if hasattr(g.L, "kmx_mul_karatsuba_levels"):
+        karatsuba = int(g.L.kmx_mul_karatsuba_levels(v, B, cfg["n"], cfg["n"], cfg["b"], flags))
+    work = (f"{prods} 32x32->64 limb products per launch ({algorithmic_products(cfg, v)} per pair x {B}; "
+            f"schoolbook count, the work the reference's classical multiply does)")
+    if eng == "tensor":
+        tops = 2.0 * 16.0 * lps / 1e12
+        tpk = 2.0 * g.tensor / 1e12
+        r = {"bound": "tensor", "kernel": "k_tcmul (tcgen05.mma kind::i8 byte convolution, TMEM s32)",
+             "achieved": tops, "peak": tpk, "unit": "TOPS (int8, 2 ops per MAC)", "frac": tops / tpk,
+             "peak_source": "kmx_tc_peak() live: dense tcgen05 u8 MMA M=128 N=256 K=32 from smem, all SMs",
+             "algorithmic_work": f"{16 * prods} byte MACs per launch (16 per 32x32 limb product); " + work,
+             "traffic": g.traffic(cfg_name, v, "tcmul_dram_bytes"),
+             "same_kernel_in_imad_units": {"achieved": lps / 1e9, "unit": "G limb-products/s",
+                                           "frac_of_imad_peak": lps / g.imad}}
+        if info.get("engine") == "tensor tiled" and info.get("smem_bytes_per_product"):
+            nprod = B * PCOUNT[ks_geometry(cfg, v)["variant"]]
+            clk = (clocks or {}).get("sm_mhz") or 1965.0
+            smem_peak = 148 * 128 * clk * 1e6 / 1e9
+            smem_ach = info["smem_bytes_per_product"] * nprod / (mul_ms * 1e-3) / 1e9
+            r["smem_operand_bound"] = {
+                "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s", "frac": smem_ach / smem_peak,
+                "bytes_per_launch": info["smem_bytes_per_product"] * nprod,
+                "plan": {k: info[k] for k in ("H", "NW", "KC", "TPC", "mmas_per_product")},
+                "algorithmic_fraction_of_issued_macs": (16.0 * prods / nprod / info["issued_byte_macs_per_product"]
+                                                        if info["issued_byte_macs_per_product"] else None),
+                "note": "peak = 148 SMs x 128 B/clk shared-memory bandwidth at the observed SM clock"}
+    else:
+        r = {"bound": "imad", "kernel": "k_mul (IMAD.WIDE.U32 schoolbook)",
+             "achieved": lps / 1e9, "peak": g.imad / 1e9, "unit": "G limb-products/s", "frac": lps / g.imad,
+             "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
+             "algorithmic_work": work, "traffic": g.traffic(cfg_name, v, "mul_dram_bytes")}
+    r["mul_plan"] = info
+    if karatsuba:
+        r["karatsuba_levels"] = karatsuba
+    return r
+
+
+def hbm_roofline(g, cfg, v, km):
+    """Algorithmic bytes / CUDA-event duration of pack, finish and
+    reconstruction against the measured HBM bandwidth."""
+    by = hbm_bytes(cfg, v)
+    out = {"bound": "hbm", "unit": "GB/s", "peak": g.hbm, "peak_source": g.hbm_src,
+           "bytes_per_step": by}
+
+    def ent(name, nbytes, ms, kernel):
+        if not ms or not nbytes:
+            return None
+        a = nbytes / (ms * 1e-3) / 1e9
+        return {"achieved": a, "frac": a / g.hbm, "bytes": nbytes, "ms": ms, "kernel": kernel}
+
+    out["pack"] = ent("pack", by["pack"], km.get("pack"), "k_pack_pair / k_pack")
+    if "finish+recon (fused)" in km:
+        out["finish+recon"] = ent("finish+recon", by["fused"], km["finish+recon (fused)"], "k_finrec")
+    else:
+        out["finish"] = ent("finish", by["finish"], km.get("finish"), "k_finish_w / k_finish / k_finchunk")
+        if "recon" in by:
+            out["recon"] = ent("recon", by["recon"], km.get("recon"), "k_recon_par")
+    return out
+
+
+def measure_e2e(g, cfg, v, fh, gh, steps, warmup, dev_out):
+    """End to end through the public host API (pinned host buffers; H2D copy
+    of the inputs, the kernels and the D2H copy of the result inside the
+    timed call), and a full-batch comparison with the device-path output."""
+    import numpy as np
+    torch, kmx = g.torch, g.kmx
     if cfg["kind"] == "ks":
-        ow = L.kmx_ks_out_words(cfg["n"], cfg["n"], cfg["b"], _lib.KMX_SIGNED if signed else 0)
+        signed = cfg["signed"]
+        ow = dev_out.shape[2]
         fp = torch.from_numpy(fh.view(np.int32)).pin_memory().numpy().view(np.uint32)
         gp = torch.from_numpy(gh.view(np.int32)).pin_memory().numpy().view(np.uint32)
-        hp = torch.empty((B, 2 * cfg["n"] - 1, ow), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
+        hp = torch.empty((cfg["batch"], 2 * cfg["n"] - 1, ow), dtype=torch.int32).pin_memory().numpy().view(np.uint32)
         call = lambda: kmx.ks_mul_host(v, fp, gp, cfg["b"], signed=signed, out=hp)  # noqa: E731
-        h2d = fp.nbytes + gp.nbytes
-        d2h = hp.nbytes
+        api = "paper_0712_4046_b200.ks_mul_host -> kmx_ks_mul_host"
     else:
         fp = torch.from_numpy(fh).pin_memory().numpy()
         gp = torch.from_numpy(gh).pin_memory().numpy()
-        hp = torch.empty((B, 2 * cfg["lx"] - 1, 2 * cfg["ly"] - 1), dtype=torch.int64).pin_memory().numpy()
+        hp = torch.empty((cfg["batch"], 2 * cfg["lx"] - 1, 2 * cfg["ly"] - 1), dtype=torch.int64).pin_memory().numpy()
         call = lambda: kmx.bks_mul_host(v, fp, gp, cfg["b"], out=hp)  # noqa: E731
-        h2d = fp.nbytes + gp.nbytes
-        d2h = hp.nbytes
-    for _ in range(max(1, args.warmup)):
+        api = "paper_0712_4046_b200.bks_mul_host -> kmx_bks_mul_host"
+    for _ in range(max(1, warmup)):
         call()
-    barrier()
+    g.barrier()
     tot = 0.0
-    for _ in range(args.steps):
-        flush_buf.fill_(1)
+    for _ in range(steps):
+        g.flush.fill_(1)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         call()
         tot += time.perf_counter() - t0
-    barrier()
-    tot = mor(tot)
-    e2e = {"value": job_products(B, world) / (tot / args.steps), "unit": "poly products/s",
-           "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
-           "ms_per_step": 1e3 * tot / args.steps, "api": "paper_0712_4046_b200.ks_mul_host -> kmx_ks_mul_host"
-           if cfg["kind"] == "ks" else "paper_0712_4046_b200.bks_mul_host -> kmx_bks_mul_host"}
+    g.barrier()
+    tot = g.mor(tot)
+    world = 1 if g.dist is None else g.dist.get_world_size()
+    same = bool(np.array_equal(hp.view(np.uint8), dev_out.cpu().numpy().view(np.uint8)))
+    return {"value": job_products(cfg["batch"], world) / (tot / steps), "unit": "poly products/s",
+            "h2d_bytes_per_step": int(fp.nbytes + gp.nbytes), "d2h_bytes_per_step": int(hp.nbytes),
+            "ms_per_step": 1e3 * tot / steps, "api": api, "equals_device_output": same}
 
-    # correctness spot check of the timed output against the oracle (pair 0)
-    check = None
-    if rank == 0:
-        from oracle import ks_oracle as O
-        from paper_0712_4046_b200.words import words_to_ints
-        if cfg["kind"] == "ks":
-            fi = to_ints(fh[:1], signed)[0]
-            gi = to_ints(gh[:1], signed)[0]
-            want = (O.ks_mul_signed(1, fi, gi, cfg["b"], mode="native") if signed
-                    else O.ks_mul(1, fi, gi, cfg["b"], mode="native"))
-            got = words_to_ints(out[0].cpu().numpy().view(np.uint32), signed=signed)
-            check = got == want
-        else:
-            want = O.bks(v, fh[0].tolist(), gh[0].tolist())
-            check = out[0].cpu().tolist() == want
 
-    result = dict(rec=rec, per_variant=per_variant, e2e=e2e, peak=peak, tpeak=tpeak, clocks=clocks, variant=v,
-                  launches=launches, check=check)
-    if dist is not None:
-        dist.destroy_process_group()
-    return result
+def oracle_pairs(cfg, B):
+    """Pairs checked against the oracle: the first and last of every part a
+    batch split (2 or 4 parts) or the host path's chunking can produce, i.e.
+    0, B/4, B/2, 3B/4 and their predecessors, and B-1."""
+    cand = {0, B - 1}
+    for q in (4, 2):
+        for i in range(1, q):
+            s = (B * i) // q
+            cand.update({s, s - 1})
+    return sorted(p for p in cand if 0 <= p < B)
+
+
+def check_pairs(cfg, v, fh, gh, out, pairs):
+    import numpy as np
+    from oracle import ks_oracle as O
+    from paper_0712_4046_b200.words import words_to_ints
+    host = out.cpu().numpy()
+    ok = True
+    for p in pairs:
+        if cfg["kind"] == "bks":
+            ok = ok and host[p].tolist() == O.bks(v, fh[p].tolist(), gh[p].tolist())
+            continue
+        signed = cfg["signed"]
+        fi = to_ints(fh[p:p + 1], signed)[0]
+        gi = to_ints(gh[p:p + 1], signed)[0]
+        want = (O.ks_mul_signed(1, fi, gi, cfg["b"], mode="native") if signed
+                else O.ks_mul(1, fi, gi, cfg["b"], mode="native"))
+        ok = ok and words_to_ints(host[p].view(np.uint32), signed=signed) == want
+    return bool(ok)
+
+
+def measure_config(g, cfg_name, cfg, variants, steps, warmup, graphs=True, e2e=True, monitor_first=False,
+                   rank=0, oracle=True, pairs=None):
+    """Every variant of one config; parity: all variants bit-identical on
+    the whole batch, and the oracle on pairs from every split part."""
+    torch = g.torch
+    import numpy as np
+    fh, gh = make_inputs(cfg, rank)
+    if cfg["kind"] == "bks":
+        fd, gd = torch.from_numpy(fh).to(g.dev), torch.from_numpy(gh).to(g.dev)
+    else:
+        fd = torch.from_numpy(fh.view(np.int32)).to(g.dev)
+        gd = torch.from_numpy(gh.view(np.int32)).to(g.dev)
+    recs, outs = {}, {}
+    for i, v in enumerate(variants):
+        mon = ClockMonitor(g.dev.index) if (monitor_first and i == 0 and rank == 0) else None
+        rec, out, op = measure_variant(g, cfg, cfg_name, v, fd, gd, steps, warmup, graphs, mon)
+        if e2e:
+            rec["e2e"] = measure_e2e(g, cfg, v, fh, gh, max(3, steps // 2), 1, out)
+        recs[VNAME[v]] = rec
+        outs[v] = out.clone()
+        del op
+    res = {"workload": cfg["desc"], "batch": cfg["batch"], "variants": recs}
+    base = recs.get("ks1")
+    if base:
+        res["speed_ratios_vs_ks1"] = {k: r["products_per_s"] / base["products_per_s"] for k, r in recs.items()}
+    ref = outs[variants[0]]
+    par = {"variants_bit_identical_full_batch": all(torch.equal(ref, o) for o in outs.values())}
+    if oracle and rank == 0:
+        pairs = pairs if pairs is not None else oracle_pairs(cfg, cfg["batch"])
+        par["oracle_pairs"] = pairs
+        par["oracle_ok"] = check_pairs(cfg, variants[0], fh, gh, ref, pairs)
+    if e2e:
+        par["e2e_equals_device_all_variants"] = all(r["e2e"]["equals_device_output"] for r in recs.values())
+    res["parity"] = par
+    return res
+
+
+def c5_summary(g, steps, warmup, scale=1, ns=C5_NS, bits=C5_BITS, detail=False):
+    """BASELINE config 5: the crossover sweep, all four variants per point;
+    parity per point: the four variants bit-identical on the whole batch and
+    the oracle on the first and last pair."""
+    points = []
+    t0 = time.time()
+    for n in ns:
+        for b in bits:
+            cfg = c5_config(n, b, scale)
+            res = measure_config(g, "c5", cfg, [4, 1, 2, 3], steps, warmup, e2e=False,
+                                 pairs=[0, cfg["batch"] - 1])
+            pt = {"n": n, "bits": b, "batch": cfg["batch"]}
+            for k in ("ks1", "ks2", "ks3", "ks4"):
+                pt[k] = res["variants"][k]["products_per_s"]
+            pt["fastest"] = max(res["variants"], key=lambda k: res["variants"][k]["products_per_s"])
+            pt["parity_ok"] = bool(res["parity"]["variants_bit_identical_full_batch"] and res["parity"]["oracle_ok"])
+            if detail:
+                pt["detail"] = res["variants"]
+            else:
+                pt["mul_frac"] = {k: (r["roofline"] or {}).get("frac") for k, r in res["variants"].items()}
+                pt["mul_engine"] = {k: (r["roofline"] or {}).get("bound") for k, r in res["variants"].items()}
+                pt["hbm_frac"] = {k: {s: (r["roofline_hbm"].get(s) or {}).get("frac")
+                                      for s in ("pack", "finish", "recon", "finish+recon") if r["roofline_hbm"].get(s)}
+                                  for k, r in res["variants"].items()}
+            points.append(pt)
+    return {"config": "BASELINE configs[4]: n x bits crossover sweep over Z[x], unsigned uniform from seed, "
+                      "B = ceil(1e6/(2n-1)) pairs per point",
+            "scale": scale, "steps": steps, "points": points, "wall_s": time.time() - t0,
+            "all_parity_ok": all(p["parity_ok"] for p in points)}
 
 
 # ------------------------------------------------------------ CPU baseline
@@ -400,13 +617,15 @@ def _cpu_task(args):
 
 def cpu_tasks(cfg, variant, count):
     fh, gh = make_inputs(cfg, 0)
-    count = min(count, cfg["batch"])
+    count = max(1, min(count, cfg["batch"]))
     if cfg["kind"] == "bks":
-        return [("bks", variant, fh[i].tolist(), gh[i].tolist(), cfg["b"], False) for i in range(count)]
-    signed = cfg["signed"]
-    fi = to_ints(fh[:count], signed)
-    gi = to_ints(gh[:count], signed)
-    return [("ks", variant, fi[i], gi[i], cfg["b"], signed) for i in range(count)]
+        tasks = [("bks", variant, fh[i].tolist(), gh[i].tolist(), cfg["b"], False) for i in range(count)]
+    else:
+        signed = cfg["signed"]
+        fi = to_ints(fh[:count], signed)
+        gi = to_ints(gh[:count], signed)
+        tasks = [("ks", variant, fi[i], gi[i], cfg["b"], signed) for i in range(count)]
+    return tasks
 
 
 def host_cores():
@@ -414,34 +633,6 @@ def host_cores():
         return len(os.sched_getaffinity(0))
     except Exception:
         return os.cpu_count() or 1
-
-
-def cpu_baseline(cfg, variant, budget_s=12.0):
-    """Oracle port of the reference algorithm (Python ints, restated
-    Karatsuba as in bignat.py:344-371) over all host cores on a bounded
-    sample of pairs of the same workload."""
-    import multiprocessing as mp
-    cores = host_cores()
-    t0 = time.perf_counter()
-    _cpu_task(cpu_tasks(cfg, variant, 1)[0])
-    t_pair = max(1e-4, time.perf_counter() - t0)
-    n = int(max(cores, min(cfg["batch"] * 4, budget_s * cores / t_pair)))
-    if cfg["kind"] == "bks":
-        n = cores  # one pair per core (seconds each through the pure-Python UniMul)
-    tasks = cpu_tasks(cfg, variant, n)
-    while len(tasks) < n:
-        tasks += tasks[:n - len(tasks)]
-    with mp.get_context("fork").Pool(cores) as pool:
-        pool.map(_cpu_task, tasks[:cores])  # warm the workers
-        t0 = time.perf_counter()
-        pool.map(_cpu_task, tasks, chunksize=1)
-        dt = time.perf_counter() - t0
-    return {"value": len(tasks) / dt, "unit": "poly products/s", "cores": cores, "kind": "port",
-            "sample": f"{len(tasks)} pairs of {cfg['desc']} through oracle/ks_oracle.py "
-                      f"({VNAME[variant]}, restated reference Karatsuba on Python ints"
-                      f"{', bias-lifted signed inputs' if cfg.get('signed') else ''}), "
-                      f"multiprocessing over {cores} cores, {dt:.1f} s",
-            "cpu_model": cpu_model()}
 
 
 def cpu_model():
@@ -452,6 +643,63 @@ def cpu_model():
     except Exception:
         pass
     return None
+
+
+def cpu_rate_1core(cfg, v, budget_s):
+    """Serial, in this process: pairs/s of the oracle port on one core."""
+    tasks = cpu_tasks(cfg, v, 64)
+    _cpu_task(tasks[0])
+    n, t0 = 0, time.perf_counter()
+    while True:
+        _cpu_task(tasks[n % len(tasks)])
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt >= budget_s or n >= 4 * cfg["batch"]:
+            return n / dt, n, dt
+
+
+def cpu_rate_all(cfg, v, cores, budget_s, pool):
+    t0 = time.perf_counter()
+    _cpu_task(cpu_tasks(cfg, v, 1)[0])
+    t_pair = max(1e-4, time.perf_counter() - t0)
+    n = int(max(cores, min(cfg["batch"] * 4, budget_s * cores / t_pair)))
+    if cfg["kind"] == "bks":
+        n = cores  # one pair per core (seconds each through the pure-Python UniMul)
+    tasks = cpu_tasks(cfg, v, n)
+    while len(tasks) < n:
+        tasks += tasks[:n - len(tasks)]
+    pool.map(_cpu_task, tasks[:cores])  # warm the workers
+    t0 = time.perf_counter()
+    pool.map(_cpu_task, tasks, chunksize=1)
+    dt = time.perf_counter() - t0
+    return len(tasks) / dt, len(tasks), dt
+
+
+def cpu_baseline(cfg, variants, headline, budget_all=4.0, budget_1=2.0, one_core=True):
+    """The oracle port of the reference algorithm (Python ints, restated
+    reference Karatsuba, bignat.py:344-371) on the host cores, on a bounded
+    sample of pairs of the same workload: all cores (multiprocessing over
+    pairs, as the reference's README recommends) and one core, per variant."""
+    import multiprocessing as mp
+    cores = host_cores()
+    per = {}
+    with mp.get_context("fork").Pool(cores) as pool:
+        for v in variants:
+            r_all, n_all, dt_all = cpu_rate_all(cfg, v, cores, budget_all, pool)
+            e = {"all_cores": r_all, "all_cores_sample": f"{n_all} pairs in {dt_all:.1f} s"}
+            if one_core and cfg["kind"] == "ks":
+                r1, n1, dt1 = cpu_rate_1core(cfg, v, budget_1)
+                e["one_core"] = r1
+                e["one_core_sample"] = f"{n1} pairs in {dt1:.1f} s"
+            per[VNAME[v]] = e
+    h = per[VNAME[headline]]
+    return {"value": h["all_cores"], "unit": "poly products/s", "cores": cores, "kind": "port",
+            "one_core_value": h.get("one_core"),
+            "sample": f"{h['all_cores_sample']} of {cfg['desc']} through oracle/ks_oracle.py "
+                      f"({VNAME[headline]}, restated reference Karatsuba on Python ints"
+                      f"{', bias-lifted signed inputs' if cfg.get('signed') else ''}), "
+                      f"multiprocessing over {cores} cores",
+            "per_variant": per, "cpu_model": cpu_model()}
 
 
 def run_reference(args, cfg):
@@ -482,7 +730,9 @@ def run_reference(args, cfg):
                          "sample": f"{per_step} pairs per step of {cfg['desc']} ({VNAME[v]}) through "
                                    f"oracle/ks_oracle.py over {cores} cores (the reference is pure "
                                    f"Python; its restatement runs here because /root/reference is "
-                                   f"absent on the GPU box)", "cpu_model": cpu_model()},
+                                   f"absent on the GPU box; measured within 0-10% of the reference's "
+                                   f"own per-pair time, profiles/r02/port_vs_reference.json)",
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "poly products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
@@ -499,15 +749,6 @@ def config_json(cfg, v):
     return c
 
 
-def load_traffic(config_name, variant, key="mul_dram_bytes"):
-    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    try:
-        d = json.load(open(path))
-        return d[config_name][VNAME[variant]][key]
-    except Exception:
-        return None
-
-
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -516,25 +757,53 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--variant", type=int, default=4, choices=[1, 2, 3, 4])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--quick", action="store_true",
+                    help="headline config and variant only (no per_config / c5 / CPU baseline)")
     ap.add_argument("--no-all-variants", dest="all_variants", action="store_false")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false")
+    ap.add_argument("--no-c5", dest="c5", action="store_false")
     ap.add_argument("--no-graphs", dest="graphs", action="store_false",
                     help="launch kernels eagerly instead of replaying a captured CUDA graph")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
+    if args.quick:
+        args.all_variants = args.cpu_baseline = args.per_config = args.c5 = False
     cfg = CONFIGS[args.config]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(relaunch_under_torchrun(args.gpus))
     rank, world, local_rank = rank_env()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
 
     if args.impl == "reference":
         if rank == 0:
             print(json.dumps(run_reference(args, cfg)), flush=True)
         return
 
-    r = run_ours(args, cfg, rank, world, local_rank)
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    g = Gpu(local_rank, dist)
+    v = args.variant
+    variants = [v] + [x for x in (1, 2, 3, 4) if x != v] if args.all_variants else [v]
+    head = measure_config(g, args.config, cfg, variants, args.steps, args.warmup, args.graphs,
+                          e2e=True, monitor_first=True, rank=rank)
+    rec = head["variants"][VNAME[v]]
+    per_config, c5 = {}, None
+    if world == 1 and args.per_config:
+        for name in ("c1", "c2", "c3", "c4"):
+            if name != args.config:
+                per_config[name] = measure_config(g, name, CONFIGS[name], [1, 2, 3, 4], args.steps,
+                                                  args.warmup, args.graphs, e2e=True)
+    if world == 1 and args.c5:
+        c5 = c5_summary(g, max(3, args.steps // 4), 3)
+    if dist is not None:
+        dist.destroy_process_group()
     if rank != 0:
         return
-    v = r["variant"]
-    rec = r["rec"]
     line = {
         "metric": METRIC, "value": rec["products_per_s"], "unit": "poly products/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": rec["ms_per_step"],
@@ -542,89 +811,40 @@ def main():
         "data": "synthetic (seeded numpy PCG64, BASELINE shapes)", "config": config_json(cfg, v),
         "parallelism": f"replicas x{world} (independent pairs, no collective)",
         "cuda_graph": bool(args.graphs),
+        "roofline": rec["roofline"],
     }
-    if cfg["kind"] == "ks":
-        mul_ms = rec["kernel_ms"].get("mul")
-        prods = algorithmic_products(cfg, v) * cfg["batch"]
-        ach = prods / (mul_ms * 1e-3) / 1e9
-        imad_view = {"bound": "imad", "kernel": "k_mul (IMAD.WIDE.U32 schoolbook)",
-                     "achieved": ach, "peak": r["peak"] / 1e9, "unit": "G limb-products/s",
-                     "frac": ach * 1e9 / r["peak"],
-                     "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
-                     "algorithmic_work": f"{prods} 32x32->64 limb products per launch "
-                                         f"({algorithmic_products(cfg, v)} per pair x {cfg['batch']})"}
-        if rec.get("mul_engine") == "tensor":
-            tops = 2.0 * 16.0 * prods / (mul_ms * 1e-3) / 1e12
-            tpk = 2.0 * r["tpeak"] / 1e12
-            line["roofline"] = {
-                "bound": "tensor", "kernel": "k_tcmul (tcgen05.mma kind::i8 byte convolution, TMEM s32)",
-                "achieved": tops, "peak": tpk, "unit": "TOPS (int8, 2 ops per MAC)", "frac": tops / tpk,
-                "peak_source": "kmx_tc_peak() live: dense tcgen05 u8 MMA M=128 N=256 K=32 from smem, all SMs",
-                "algorithmic_work": f"{16 * prods} byte MACs per launch (16 per 32x32 limb product; "
-                                    f"{algorithmic_products(cfg, v)} limb products per pair x {cfg['batch']})",
-                "traffic": load_traffic(args.config, v, "tcmul_dram_bytes"),
-                "same_kernel_in_imad_units": {"achieved": ach, "unit": "G limb-products/s",
-                                              "frac_of_imad_peak": ach * 1e9 / r["peak"]}}
-            mp_ = rec.get("mul_plan")
-            if mp_ and mp_["engine"] == "tensor tiled" and mp_["smem_bytes_per_product"]:
-                # what bounds it: the SS-mode MMAs read A (128 x 32 B) and B (16H x 32 B)
-                # from shared memory per MMA; peak = 128 B/clk/SM at the observed SM clock
-                P_ = {1: 1, 2: 2, 3: 2, 4: 4}[v]
-                nprod = cfg["batch"] * P_
-                clk = (r["clocks"] or {}).get("sm_mhz") or 1965.0
-                smem_peak = 148 * 128 * clk * 1e6 / 1e9
-                smem_ach = mp_["smem_bytes_per_product"] * nprod / (mul_ms * 1e-3) / 1e9
-                line["roofline"]["smem_operand_bound"] = {
-                    "achieved": smem_ach, "peak": smem_peak, "unit": "GB/s", "frac": smem_ach / smem_peak,
-                    "bytes_per_launch": mp_["smem_bytes_per_product"] * nprod,
-                    "plan": {k: mp_[k] for k in ("H", "NW", "KC", "TPC", "mmas_per_product")},
-                    "algorithmic_fraction_of_issued_macs": 16.0 * algorithmic_products(cfg, v) / P_ /
-                    mp_["issued_byte_macs_per_product"] if mp_["issued_byte_macs_per_product"] else None,
-                    "note": "peak = 148 SMs x 128 B/clk shared-memory bandwidth at the observed SM clock"}
-        else:
-            imad_view["traffic"] = load_traffic(args.config, v)
-            line["roofline"] = imad_view
-        pu = pack_unpack_bytes(cfg, v)
-        try:
-            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-            hbm = peaks["hbm_gbs"]
-            src = "MEASURED_PEAKS.json hbm_gbs"
-        except Exception:
-            hbm, src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
-        km = rec["kernel_ms"]
-        fin_ms = km.get("finish", km.get("finish+recon (fused)"))
-        line["roofline_hbm"] = {"bound": "hbm", "unit": "GB/s", "peak": hbm, "peak_source": src,
-                                "finish": {"achieved": pu["finish_bytes"] / (fin_ms * 1e-3) / 1e9,
-                                           "frac": pu["finish_bytes"] / (fin_ms * 1e-3) / 1e9 / hbm,
-                                           "kernel": "k_finrec (finish + reconstruct fused)"
-                                           if "finish" not in km else "k_finish_w / k_finish"}}
-        if "pack" in km:
-            line["roofline_hbm"]["pack"] = {"achieved": pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9,
-                                            "frac": pu["pack_bytes"] / (km["pack"] * 1e-3) / 1e9 / hbm}
-        else:
-            line["roofline_hbm"]["pack"] = "fused into the tensor-core multiply (operands packed in shared memory)"
-    else:
-        macs = algorithmic_products(cfg, v) * cfg["batch"]
-        cms = rec["kernel_ms"].get("conv")
-        ach = macs / (cms * 1e-3) / 1e9 if cms else None
-        line["roofline"] = {"bound": "imad", "kernel": "k_conv (int32 x int32 -> int64 IMAD.WIDE convolution)",
-                            "achieved": ach, "peak": r["peak"] / 1e9, "unit": "G MAC/s",
-                            "frac": ach * 1e9 / r["peak"] if ach else None,
-                            "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
-                            "algorithmic_work": f"{macs} coefficient MACs per launch "
-                                                f"({algorithmic_products(cfg, v)} per pair x {cfg['batch']})",
-                            "traffic": load_traffic(args.config, v, "conv_dram_bytes")}
-    pv = r["per_variant"]
-    line["per_variant"] = pv
-    if all(VNAME[x] in pv for x in (1, 2, 3, 4)):
-        base = pv["ks1"]["products_per_s"]
-        line["speed_ratios_vs_ks1"] = {k: pv[k]["products_per_s"] / base for k in ("ks1", "ks2", "ks3", "ks4")}
-    line["e2e"] = r["e2e"]
-    line["gpu_launches"] = int(r["launches"])
-    line["clocks"] = r["clocks"]
-    line["oracle_spot_check_pair0"] = r["check"]
+    if "roofline_hbm" in rec:
+        line["roofline_hbm"] = rec["roofline_hbm"]
+    line["kernel_ms"] = rec["kernel_ms"]
+    line["per_variant"] = head["variants"]
+    if "speed_ratios_vs_ks1" in head:
+        line["speed_ratios_vs_ks1"] = head["speed_ratios_vs_ks1"]
+    line["parity"] = head["parity"]
+    line["e2e"] = rec["e2e"]
+    line["gpu_launches"] = int(rec["gpu_launches_per_step"]) * args.steps
+    line["gpu_launches_per_step"] = int(rec["gpu_launches_per_step"])
+    line["clocks"] = rec.get("clocks")
+    line["peaks"] = {"imad_limb_products_per_s": g.imad, "tensor_u8_macs_per_s": g.tensor, "hbm_gbs": g.hbm}
+    if per_config:
+        line["per_config"] = per_config
+    if c5 is not None:
+        line["c5"] = c5
     if world == 1 and args.cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg, v)
+        cb = cpu_baseline(cfg, variants, v)
+        for k, e in cb["per_variant"].items():
+            gpu = head["variants"][k]
+            e["gpu_over_all_cores"] = gpu["products_per_s"] / e["all_cores"]
+            e["e2e_over_all_cores"] = gpu["e2e"]["value"] / e["all_cores"]
+            if e.get("one_core"):
+                e["gpu_over_one_core"] = gpu["products_per_s"] / e["one_core"]
+        line["cpu_baseline"] = cb
+        if per_config:
+            for name, pc in per_config.items():
+                c = CONFIGS[name]
+                pcb = cpu_baseline(c, [1, 2, 3, 4], 4, budget_all=2.0, one_core=False)
+                for k, e in pcb["per_variant"].items():
+                    e["gpu_over_all_cores"] = pc["variants"][k]["products_per_s"] / e["all_cores"]
+                pc["cpu_baseline"] = {"cores": pcb["cores"], "kind": "port", "per_variant": pcb["per_variant"]}
     print(json.dumps(line), flush=True)
 
 

@@ -62,6 +62,7 @@ extern "C" {
 #define KMX_SIGNED 1u          /* two's-complement input coefficients        */
 #define KMX_NO_VALIDATE 2u     /* skip the 0 <= c < 2^b range check           */
 #define KMX_NO_SPLIT 4u        /* kmx_ks_mul: do not split the batch over two streams */
+#define KMX_NO_TUNE 8u         /* kmx_ks_mul: no first-call timing runs (model-chosen plan, default schedule) */
 
 /* Derived parameters (ksint.py:82-98).  out[0..7] = e, N1, N2, N4,
  * four_point_safe, out_len, limbs of the packed f operand, limbs of the
@@ -77,7 +78,15 @@ int kmx_ks_out_words(int len_f, int len_g, int coeff_bits, unsigned flags);
 size_t kmx_ks_workspace_bytes(int variant, int batch, int len_f, int len_g, int coeff_bits,
                               unsigned flags);
 
-/* Batched KS product on the device (asynchronous on `stream`). */
+/* Batched KS product on the device (asynchronous on `stream`).
+ *
+ * First call per (device, shape, batch) with batch >= 64, outside a CUDA
+ * graph capture and without KMX_NO_TUNE: the call measures its batch-split
+ * schedule and tensor-core tiling by running the product several times on
+ * `stream` and BLOCKS the host until those timing runs finish (each run
+ * writes the same bit-exact h).  The choice is cached per device; later calls
+ * (and graph captures) are asynchronous.  Pass KMX_NO_TUNE (or set
+ * KMX_TC_AUTOTUNE=0 and KMX_SPLIT) for a strictly asynchronous first call. */
 int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits,
                const uint32_t* f, const uint32_t* g, int in_words,
                uint32_t* h, int out_words,
@@ -102,6 +111,21 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
                     const uint32_t* f, const uint32_t* g, int in_words,
                     uint32_t* h, int out_words, unsigned flags,
                     uint64_t* limb_products64 /* nullable: MulStats count */);
+
+/* K1 alone: kronmul.pack.pack (kind 0), pack_negated (1), pack_reversed (2),
+ * pack_negated_reversed (3) (pack.py:79-110) of `batch` coefficient vectors
+ * [batch][len][in_words] at width_bits (2*width_bits >= coeff_bits, else
+ * KMX_EINVAL as pack.py:55-59).  out: [batch][out_limbs] |value| little-endian
+ * limbs, out_limbs >= kmx_pack_limbs(); meta (required on the device entry,
+ * nullable on the host entry):
+ * [batch][2] = {sign (1: negative), bit length of |value|}.  Coefficients
+ * outside [0, 2^coeff_bits) latch KMX_EINVAL (read with kmx_ws_status);
+ * the device workspace is >= 256 bytes. */
+int kmx_pack_limbs(int len, int width_bits, int coeff_bits);
+int kmx_pack(int kind, int batch, int len, int width_bits, int coeff_bits, const uint32_t* coeffs, int in_words,
+             uint32_t* out, int out_limbs, uint32_t* meta, void* workspace, size_t ws_bytes, void* stream);
+int kmx_pack_host(int kind, int batch, int len, int width_bits, int coeff_bits, const uint32_t* coeffs,
+                  int in_words, uint32_t* out, int out_limbs, uint32_t* meta);
 
 /* Overlap reconstruction of `batch` independent digit-stream pairs on the
  * device: fwd, rev are [batch][count+1][dwords] (rev listed most significant

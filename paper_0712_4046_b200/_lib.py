@@ -22,6 +22,7 @@ KMX_ENOMEM = -5
 KMX_SIGNED = 1
 KMX_NO_VALIDATE = 2
 KMX_NO_SPLIT = 4
+KMX_NO_TUNE = 8
 
 
 class ReconstructionError(ArithmeticError):
@@ -54,6 +55,9 @@ _SIGS = {
     "kmx_ws_status": (_i, [_vp, _vp]),
     "kmx_ws_limb_products": (_i, [_vp, _i, _i, _i, _i, _i, _u, _u64p, _vp]),
     "kmx_ks_mul_host": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i, _u, _u64p]),
+    "kmx_pack_limbs": (_i, [_i, _i, _i]),
+    "kmx_pack": (_i, [_i, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp, _vp, _sz, _vp]),
+    "kmx_pack_host": (_i, [_i, _i, _i, _i, _i, _vp, _i, _vp, _i, _vp]),
     "kmx_reconstruct": (_i, [_i, _i, _i, _vp, _vp, _i, _vp, _i, _vp, _sz, _vp, _vp]),
     "kmx_reconstruct_workspace_bytes": (_sz, [_i, _i, _i]),
     "kmx_reconstruct_host": (_i, [_i, _i, _i, _vp, _vp, _i, _vp, _i, _vp]),

@@ -31,11 +31,11 @@ class KsBatch:
     """Plan + workspace for repeated batched KS products of one shape."""
 
     def __init__(self, variant: int, batch: int, len_f: int, len_g: int, coeff_bits: int,
-                 signed: bool = False, device=None):
+                 signed: bool = False, device=None, tune: bool = True):
         torch = _torch()
         self.variant, self.batch, self.len_f, self.len_g = variant, batch, len_f, len_g
         self.coeff_bits = coeff_bits
-        self.flags = KMX_SIGNED if signed else 0
+        self.flags = (KMX_SIGNED if signed else 0) | (0 if tune else _lib.KMX_NO_TUNE)
         self.in_words = 1 if signed else (coeff_bits + 31) // 32
         self.out_len = len_f + len_g - 1
         ow = lib().kmx_ks_out_words(len_f, len_g, coeff_bits, self.flags)
@@ -105,13 +105,14 @@ class KsBatch:
 
 
 def ks_mul_host(variant: int, f: np.ndarray, g: np.ndarray, coeff_bits: int, signed: bool = False,
-                out: np.ndarray | None = None) -> np.ndarray:
+                out: np.ndarray | None = None, tune: bool = True) -> np.ndarray:
     """Host-buffer batched KS product: f [batch, len_f, in_words] uint32/int32,
-    g [batch, len_g, in_words] -> [batch, len_f+len_g-1, out_words] uint32."""
+    g [batch, len_g, in_words] -> [batch, len_f+len_g-1, out_words] uint32.
+    ``tune=False`` skips the first-call plan measurement (KMX_NO_TUNE)."""
     assert f.ndim == 3 and g.ndim == 3 and f.shape[0] == g.shape[0] and f.shape[2] == g.shape[2]
     batch, lf, iw = f.shape
     lg = g.shape[1]
-    flags = KMX_SIGNED if signed else 0
+    flags = (KMX_SIGNED if signed else 0) | (0 if tune else _lib.KMX_NO_TUNE)
     ow = lib().kmx_ks_out_words(lf, lg, coeff_bits, flags)
     if ow < 0:
         check(ow, "ks_mul_host")

@@ -28,6 +28,11 @@ using namespace kmx;
 namespace {
 
 int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
+int cur_dev() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 
 // K2 engine choice.  Default: the tcgen05 byte convolution wherever its shape
 // gate admits the operands and the shorter one has more than 144 limbs; below
@@ -48,7 +53,7 @@ namespace {
 // the tiled kernel's CTAs (< 4 per SM): one CTA per product with a K span
 // shortened by J is lower-latency there (c1 ks2/ks3 +9-11%, ks4 +8%), while
 // the tiled kernel keeps the edge on full batches (c2 ks4 K2 0.121 vs 0.129 ms)
-// and on long products (profiles/r01_tcj_sweep_*.json, c5 sweep).
+// and on long products (profiles/r01/tcj_sweep_*.json, c5 sweep).
 // KMX_TCJ=1 / 0 forces it on / off wherever its shape gate admits the product.
 bool use_tcj(int ma, int mb, long long nprod) {
   const char* v = getenv("KMX_TCJ");
@@ -340,6 +345,8 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   if (after_pack && cudaEventRecord(after_pack, st) != cudaSuccess) return KMX_ECUDA;
 
   MulArgs ma;
+  memset(&ma, 0, sizeof ma);
+  ma.flags_no_tune = (p.flags & KMX_NO_TUNE) != 0;
   ma.A = opf; ma.a_stride = p.mfs; ma.ma = p.mf;
   ma.B = opg; ma.b_stride = p.mgs; ma.mb = p.mg;
   ma.P = prod; ma.p_stride = p.ps; ma.spill = spill;
@@ -544,9 +551,10 @@ Sched default_sched(int batch, unsigned flags) {
 struct SchedKey {
   int variant, batch, lf, lg, b, iw;
   unsigned flags;
+  int dev;
   bool operator<(const SchedKey& o) const {
-    const int x[6] = {variant, batch, lf, lg, b, iw}, y[6] = {o.variant, o.batch, o.lf, o.lg, o.b, o.iw};
-    for (int i = 0; i < 6; i++)
+    const int x[7] = {variant, batch, lf, lg, b, iw, dev}, y[7] = {o.variant, o.batch, o.lf, o.lg, o.b, o.iw, o.dev};
+    for (int i = 0; i < 7; i++)
       if (x[i] != y[i]) return x[i] < y[i];
     return flags < o.flags;
   }
@@ -664,8 +672,8 @@ int kmx_ks_mul(int variant, int batch, int len_f, int len_g, int coeff_bits, con
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, in_words, flags);
   if (rc) return rc;
   cudaStream_t st = (cudaStream_t)stream;
-  const SchedKey key{variant, batch, len_f, len_g, coeff_bits, p.in_words, flags};
-  const bool tune = !g_prof.on && !(flags & KMX_NO_SPLIT) && split_force() < 0 && batch >= 64;
+  const SchedKey key{variant, batch, len_f, len_g, coeff_bits, p.in_words, flags, cur_dev()};
+  const bool tune = !g_prof.on && !(flags & (KMX_NO_SPLIT | KMX_NO_TUNE)) && split_force() < 0 && batch >= 64;
   Sched sc0;
   if (!tune || tuned_sched(key, &sc0)) {
     if (!tune) sc0 = current_sched(key);
@@ -773,7 +781,7 @@ int kmx_ws_limb_products(void* workspace, int variant, int batch, int len_f, int
   KsPlan p;
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);
   if (rc) return rc;
-  const Sched used = current_sched(SchedKey{variant, batch, len_f, len_g, coeff_bits, p.in_words, flags});
+  const Sched used = current_sched(SchedKey{variant, batch, len_f, len_g, coeff_bits, p.in_words, flags, cur_dev()});
   if (used.ways > 1) {  // the parts' workspaces after a 256-byte header
     const int k = used.ways;
     KsPlan parts[SPLIT_MAX];
@@ -842,7 +850,8 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
   if (cudaMemcpyAsync(h, c->buf[1], hb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
   rc = kmx_ws_status(c->buf[2], c->st);
   if (rc == KMX_OK && limb_products64)
-    rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, coeff_bits, flags, limb_products64, c->st);
+    rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, coeff_bits, flags | KMX_NO_SPLIT,
+                              limb_products64, c->st);
   return rc;
 }
 
@@ -918,8 +927,71 @@ int kmx_mod_mul_host(int variant, int batch, int len_f, int len_g, uint64_t modu
   if (cudaMemcpyAsync(h, c->buf[1], hb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
   rc = kmx_ws_status(c->buf[2], c->st);
   if (rc == KMX_OK && limb_products64)  // the KS workspace leads the mod workspace
-    rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, p.b, 0, limb_products64, c->st);
+    rc = kmx_ws_limb_products(c->buf[2], variant, batch, len_f, len_g, p.b, KMX_NO_SPLIT, limb_products64, c->st);
   return rc;
+}
+
+// ------------------------------------------------------------------ K1 alone
+// kronmul.pack.pack / pack_reversed / pack_negated / pack_negated_reversed
+// (pack.py:79-110) for a batch of coefficient vectors at one width: K1 by
+// itself, writing |value| as out_limbs little-endian limbs and [sign, bitlen]
+// per vector.
+int kmx_pack_limbs(int len, int width_bits, int coeff_bits) {
+  if (len < 1 || width_bits < 1 || coeff_bits < 1) return KMX_EINVAL;
+  const long long bits = (long long)width_bits * (len - 1) + coeff_bits + 2;
+  if ((bits + 31) / 32 > (1LL << 28)) return KMX_EINVAL;
+  return (int)((bits + 31) / 32);
+}
+
+int kmx_pack(int kind, int batch, int len, int width_bits, int coeff_bits, const uint32_t* coeffs, int in_words,
+             uint32_t* out, int out_limbs, uint32_t* meta, void* workspace, size_t ws_bytes, void* stream) {
+  if (kind < 0 || kind > 3 || batch < 0 || in_words < (coeff_bits + 31) / 32) return KMX_EINVAL;
+  const int m = kmx_pack_limbs(len, width_bits, coeff_bits);
+  if (m < 0) return m;
+  if (2LL * width_bits < coeff_bits) return KMX_EINVAL;  // pack.py:55-59
+  if (out_limbs < m || ws_bytes < 256 || !workspace) return KMX_EINVAL;
+  g_launches = 0;
+  if (batch == 0) return KMX_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  uint32_t* err = (uint32_t*)workspace;
+  if (cudaMemsetAsync(err, 0, 4, st) != cudaSuccess) return KMX_ECUDA;
+  // limbs past m are not written by K1: clear the caller's padding
+  if (out_limbs > m &&
+      cudaMemset2DAsync(out + m, (size_t)out_limbs * 4, 0, (size_t)(out_limbs - m) * 4, batch, st) != cudaSuccess)
+    return KMX_ECUDA;
+  PackArgs pa;
+  memset(&pa, 0, sizeof pa);
+  pa.nops = 1; pa.N = width_bits; pa.b = coeff_bits; pa.in_words = in_words; pa.err = err;
+  PackOp& o = pa.op[0];
+  o.coeffs = coeffs; o.coeff_pair_stride = (long long)len * in_words; o.len = len; o.kind = kind;
+  o.out = out; o.out_pair_stride = out_limbs; o.meta = meta; o.meta_pair_stride = 2; o.m = m; o.validate = 1;
+  if (launch_pack(pa, batch, st) != cudaSuccess) return KMX_ECUDA;
+  g_launches = 1;
+  return KMX_OK;
+}
+
+int kmx_pack_host(int kind, int batch, int len, int width_bits, int coeff_bits, const uint32_t* coeffs, int in_words,
+                  uint32_t* out, int out_limbs, uint32_t* meta) {
+  const int m = kmx_pack_limbs(len, width_bits, coeff_bits);
+  if (m < 0) return m;
+  if (batch <= 0) return batch < 0 ? KMX_EINVAL : KMX_OK;
+  int rc;
+  HostCtx* c = host_ctx(&rc);
+  if (!c) return rc;
+  std::lock_guard<std::mutex> lk(c->mu);
+  if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
+  const size_t cb = (size_t)batch * len * in_words * 4, ob = (size_t)batch * out_limbs * 4, mb = (size_t)batch * 8;
+  if ((rc = ensure(*c, 0, cb))) return rc;
+  if ((rc = ensure(*c, 1, align256(ob) + mb))) return rc;
+  if ((rc = ensure(*c, 2, 256))) return rc;
+  uint32_t* dm = (uint32_t*)((char*)c->buf[1] + align256(ob));
+  if (cudaMemcpyAsync(c->buf[0], coeffs, cb, cudaMemcpyHostToDevice, c->st) != cudaSuccess) return KMX_ECUDA;
+  rc = kmx_pack(kind, batch, len, width_bits, coeff_bits, (const uint32_t*)c->buf[0], in_words, (uint32_t*)c->buf[1],
+                out_limbs, dm, c->buf[2], c->cap[2], c->st);
+  if (rc) return rc;
+  if (cudaMemcpyAsync(out, c->buf[1], ob, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
+  if (meta && cudaMemcpyAsync(meta, dm, mb, cudaMemcpyDeviceToHost, c->st) != cudaSuccess) return KMX_ECUDA;
+  return kmx_ws_status(c->buf[2], c->st);
 }
 
 size_t kmx_reconstruct_workspace_bytes(int batch, int count, int dwords) {

@@ -28,8 +28,11 @@ __device__ __forceinline__ void point_flags(int variant, int pt, int& rev, int& 
 }
 
 // evals: [batch][P][2][Lu] int32 (f then g)
-__global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, const int32_t* g, int32_t* ev) {
+__global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, const int32_t* g, int32_t* ev,
+                                               uint32_t* err) {
   const int lx = p.lx, ly = p.ly, Lu = p.Lu, sp = p.spacing;
+  const long long lim = 1LL << p.cbits;  // the declared bound the int64 budget was derived from
+  bool bad = false;
   const long long total = (long long)p.batch * p.P * 2 * Lu;
   for (long long id = (long long)blockIdx.x * blockDim.x + threadIdx.x; id < total;
        id += (long long)gridDim.x * blockDim.x) {
@@ -50,10 +53,12 @@ __global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, co
       const int k = rev ? (ly - 1 - q) : q;
       const int i = t - q * sp;
       const long long v = c[(long long)i * ly + k];
+      bad |= v >= lim || v <= -lim;
       acc += (alt && (k & 1)) ? -v : v;
     }
     ev[id] = (int32_t)acc;
   }
+  if (bad) raise_err(err, ERR_INVAL);
 }
 
 // ------------------------------------------------------------ k_brecover
@@ -147,7 +152,7 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   int grid = (int)std::min<long long>((ne + 255) / 256, 148LL * 32);
   if (grid < 1) grid = 1;
   prof_mark(0, true, st);
-  k_beval<<<grid, 256, 0, st>>>(p, f, g, evals);
+  k_beval<<<grid, 256, 0, st>>>(p, f, g, evals, err);
   prof_mark(0, false, st);
   (*nlaunch)++;
   cudaError_t e = cudaGetLastError();
@@ -185,6 +190,7 @@ int bks_plan(BivarPlan& p, int variant, int batch, int lx, int ly, int coeff_bit
     return KMX_EINVAL;
   p.variant = variant; p.lx = lx; p.ly = ly; p.batch = batch;
   p.n4 = (lx + 1) / 2;
+  p.cbits = coeff_bits;
   switch (variant) {
     case 1: p.P = 1; p.spacing = 2 * lx - 1; p.Lu = (2 * lx - 1) * (ly - 1) + lx; break;
     case 2: p.P = 2; p.spacing = lx; p.Lu = lx * ly; break;

@@ -47,6 +47,7 @@ struct MulArgs {
   unsigned long long* spill;                      // [z][nbands][2]
   int nprod, nbands, G, TI;
   int* counter;                                   // work-unit counter, zeroed before launch
+  int flags_no_tune;                              // KMX_NO_TUNE: the cost model's tiling, no timing runs
 };
 struct ConvArgs {
   const int32_t* A; long long a_stride;
@@ -182,6 +183,7 @@ struct BivarPlan {
   int Lu;         // univariate operand length
   int spacing;    // chunk spacing in the evaluation
   int n4;         // four-point half length
+  int cbits;      // declared bound |c| < 2^cbits, checked on the device (ERR_INVAL)
 };
 cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h,
                          int32_t* evals, int64_t* prods, uint32_t* err, cudaStream_t st,

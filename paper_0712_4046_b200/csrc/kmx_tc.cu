@@ -718,12 +718,18 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
 }
 
 struct TuneKey {
-  int ma, mb;
+  int dev, ma, mb;
   long long nprod;
   bool operator<(const TuneKey& o) const {
+    if (dev != o.dev) return dev < o.dev;
     return ma != o.ma ? ma < o.ma : (mb != o.mb ? mb < o.mb : nprod < o.nprod);
   }
 };
+int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 std::mutex g_tune_mu;
 std::map<TuneKey, TcPlan> g_tune;
 
@@ -739,10 +745,18 @@ bool tc_tuned_plan(const MulArgs& a, cudaStream_t st, TcPlan& p, bool* launched)
   static const int on = env_int_tc("KMX_TC_AUTOTUNE", 1) && !getenv("KMX_TC_H") && !getenv("KMX_TC_KC") &&
                         !getenv("KMX_TC_NW") && !getenv("KMX_TC_NB") && !getenv("KMX_TC_TPC");
   if (!on) return false;
-  const TuneKey key{a.ma, a.mb, a.nprod};
-  std::lock_guard<std::mutex> lk(g_tune_mu);
-  auto it = g_tune.find(key);
-  if (it != g_tune.end()) { p = it->second; return true; }
+  if (a.flags_no_tune) return false;
+  // small launches (e.g. single drop-in products) keep the model's plan: the
+  // timing runs would cost more than any plan difference
+  if ((double)a.nprod * a.ma * a.mb < (double)(1 << 24)) return false;
+  const TuneKey key{current_device(), a.ma, a.mb, a.nprod};
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    auto it = g_tune.find(key);
+    if (it != g_tune.end()) { p = it->second; return true; }
+  }
+  // the lock is not held while timing: another thread tuning the same key
+  // concurrently does redundant work but stores an equally valid plan
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return false;
   std::vector<TcPlan> cands = tc_candidates(a.ma, a.mb, a.nprod);
@@ -765,7 +779,10 @@ bool tc_tuned_plan(const MulArgs& a, cudaStream_t st, TcPlan& p, bool* launched)
   cudaEventDestroy(e1);
   if (best < 0) return false;
   p = cands[best];
-  g_tune[key] = p;
+  {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tune[key] = p;
+  }
   if (env_int_tc("KMX_TC_VERBOSE", 0))
     fprintf(stderr, "kmx_tc autotune: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d (%.4f ms of %zu candidates)\n", a.ma,
             a.mb, a.nprod, p.H, p.NW, p.KC, best_ms, cands.size());
@@ -863,7 +880,7 @@ bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]) {
   if (!tc_plan(ma, mb, nprod, 0, p)) return false;
   {
     std::lock_guard<std::mutex> lk(g_tune_mu);
-    auto it = g_tune.find(TuneKey{ma, mb, nprod});
+    auto it = g_tune.find(TuneKey{current_device(), ma, mb, nprod});
     if (it != g_tune.end()) p = it->second;
   }
   switch (p.H) {

@@ -4,7 +4,7 @@ Mirrors pkg/src/kronmul/ksint.py: same names, signatures, return types and
 exceptions; every product runs through libkmx.so (pack -> multiply ->
 finish -> reconstruct kernels on sm_100a).  There is no CPU fallback.
 
-  derive_params          ksint.py:82-98 (host scalars, via kmx_ks_params)
+  derive_params          ksint.py:82-98 (host scalars)
   ks1_mul .. ks4_mul     ksint.py:219-348   (kmx_ks_mul_host)
   reconstruct_overlapped ksint.py:182-195   (kmx_reconstruct_host)
 """
@@ -25,15 +25,16 @@ __all__ = ["KsParams", "OverlapDigits", "ReconstructionError", "derive_params", 
 
 def derive_params(len_f: int, len_g: int, coeff_bits: int) -> KsParams:
     """Chunk widths for inputs of the given lengths and bit bound
-    (ksint.py:82-98)."""
+    (ksint.py:82-98).  Host scalars, so computed here for any size; the
+    kernels take the same widths from kmx_ks_params (tests/test_abi.py
+    checks that the two agree)."""
     if len_f < 1 or len_g < 1:
         raise ValueError("polynomial lengths must be >= 1")
     if coeff_bits < 1:
         raise ValueError("coefficient bit bound must be >= 1")
-    out = (ctypes.c_int64 * 8)()
-    check(lib().kmx_ks_params(1, len_f, len_g, coeff_bits, 0, out), "derive_params")
-    e, n1, n2, n4 = int(out[0]), int(out[1]), int(out[2]), int(out[3])
-    return KsParams(len_f, len_g, coeff_bits, e, n1, n2, n4)
+    e = _e(len_f, len_g)
+    full = 2 * coeff_bits + e
+    return KsParams(len_f, len_g, coeff_bits, e, full, coeff_bits + (e + 1) // 2, (full + 3) // 4)
 
 
 def _ks(variant: int, f: CoeffVec, g: CoeffVec, stats: MulStats | None) -> CoeffVec:

@@ -9,7 +9,7 @@ finish [-> reconstruct] -> K9 modular reduction); there is no CPU fallback.
 ``DEFAULT_THRESHOLDS`` keep the reference's bands (48 / 512, modpoly.py:74-75)
 so AUTO resolves to the same variant as the reference does.  Results never
 depend on the variant.  ``GPU_THRESHOLDS`` are the bands calibrated on B200
-from the config-5 crossover sweep (profiles/r01_c5_sweep.json,
+from the config-5 crossover sweep (profiles/r01/c5_sweep_final6.json,
 tools/calibrate_auto.py).
 
 ``ModMulBatch`` / ``mod_mul_host`` are the batched device / host-buffer forms.
@@ -80,7 +80,7 @@ class AutoThresholds:
 
 DEFAULT_THRESHOLDS = AutoThresholds()
 # B200 bands from the config-5 sweep (tools/calibrate_auto.py over
-# profiles/r01_c5_sweep_final2.json, coefficient widths 8..64 bits): the band
+# profiles/r01/c5_sweep_final6.json, coefficient widths 8..64 bits): the band
 # edges that minimise the time lost against the per-point fastest variant
 # (2.1% mean loss).
 GPU_THRESHOLDS = AutoThresholds(ks1_max_length=64, ks3_max_length=1024)

@@ -3,12 +3,12 @@
 
 The reference's AUTO (modpoly.py:79-92) is a length-only band lookup: ks1 up
 to ks1_max_length, ks3 up to ks3_max_length, ks4 beyond.  This reads
-profiles/r01_c5_sweep.json and, over coefficient widths up to --max-bits
+profiles/r01/c5_sweep_final6.json and, over coefficient widths up to --max-bits
 (word-sized moduli: the (Z/nZ)[x] front end has b <= 64), picks the band
 edges that minimise the total time lost against the per-point fastest
 variant, searching edges over the swept lengths.
 
-  python tools/calibrate_auto.py [--sweep profiles/r01_c5_sweep.json] [--max-bits 64]
+  python tools/calibrate_auto.py [--sweep profiles/r01/c5_sweep_final6.json] [--max-bits 64]
 """
 import argparse
 import json
