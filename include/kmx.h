@@ -190,9 +190,14 @@ double kmx_imad_peak(int iters);
  * environment forces 0.  Negative: error code. */
 int kmx_mul_engine(int variant, int len_f, int len_g, int coeff_bits, unsigned flags);
 
+/* Karatsuba levels (bignat.py:344-371) the multiply stage applies above the
+ * engines for this shape (0: one engine launch per product). */
+int kmx_mul_karatsuba_levels(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags);
+
 /* The multiply plan a kmx_ks_mul of this shape runs with (split schedules
  * aside: for `batch` products per launch): out8 = {engine (0 integer pipe,
- * 1 tiled tensor-core kernel, 2 chunked single-tile kernel), H, NW, KC, tiles
+ * 1 tiled tensor-core kernel, 2 chunked single-tile kernel, 3 Karatsuba levels
+ * over the engines with out8[1] = levels), H, NW, KC, tiles
  * per CTA, MMAs per product, shared-memory operand bytes per product, issued
  * byte MACs per product}; fields 1-7 are filled for engine 1 only. */
 int kmx_mul_plan(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags, int64_t* out8);

@@ -73,6 +73,7 @@ _SIGS = {
     "kmx_imad_peak": (ctypes.c_double, [_i]),
     "kmx_tc_peak": (ctypes.c_double, [_i]),
     "kmx_mul_engine": (_i, [_i, _i, _i, _i, _u]),
+    "kmx_mul_karatsuba_levels": (_i, [_i, _i, _i, _i, _i, _u]),
     "kmx_mul_plan": (_i, [_i, _i, _i, _i, _i, _u, _i64p]),
     "kmx_error_string": (ctypes.c_char_p, [_i]),
     "kmx_last_launch_count": (_i, []),

@@ -63,13 +63,28 @@ bool use_tcj(int ma, int mb, long long nprod) {
   return tcj_plan(ma, mb, nullptr, force < 0);
 }
 
+int tc_force() {
+  static const int f = getenv("KMX_TC") && *getenv("KMX_TC") ? atoi(getenv("KMX_TC")) : -1;
+  return f;
+}
 bool use_tensor_mul(int ma, int mb) {
-  const char* v = getenv("KMX_TC");
-  const int force = v && *v ? atoi(v) : -1;
+  const int force = tc_force();
   if (force == 0) return false;
   if (force < 0 && (ma < mb ? ma : mb) <= 144) return false;
   return tc_supported(ma, mb);
 }
+}  // namespace
+namespace kmx {
+bool mul_use_tensor(int ma, int mb) { return use_tensor_mul(ma, mb); }
+// the product goes to one engine launch unless the tensor cores would be the
+// engine of choice but cannot stage the operands (then Karatsuba splits it)
+bool mul_engine_takes(int ma, int mb) {
+  if (tc_force() == 0) return true;
+  if (tc_force() < 0 && (ma < mb ? ma : mb) <= 144) return true;
+  return tc_supported(ma, mb);
+}
+}  // namespace kmx
+namespace {
 
 // ---- tiny host bignum for the four-point bound (ksint.py:282-286)
 typedef std::vector<uint32_t> Big;
@@ -117,7 +132,8 @@ struct KsPlan {
   int W, dwords, cnt_max, dslots;
   int nrs;
   ReconStream rs[2];
-  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, off_cmap, total;
+  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, off_cmap, off_kara, total;
+  bool kara;
   int fin_chunks;  // 256-limb chunks of the longest finish stream (chunk-parallel finish maps)
 };
 
@@ -271,6 +287,10 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
   }
   p.off_cmap = o;
   o = align256(o + (size_t)batch * p.ns * p.fin_chunks);
+  // Karatsuba levels above the engines (kmx_kara.cu): sums, sub-products, maps
+  p.kara = kara_used(p.mf, p.mg);
+  p.off_kara = o;
+  if (p.kara) o = align256(o + kara_ws_bytes(p.mf, p.mg, (long long)batch * p.P));
   p.total = o;
   return KMX_OK;
 }
@@ -329,7 +349,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   // the coefficient vectors can be staged in shared memory (KMX_FUSE=1).  Off
   // by default: with one-shot CTAs the pack latency is exposed in front of
   // the MMAs (c2 ks4: 0.27 ms fused vs 0.08 + 0.12 ms separate).
-  const bool tc = use_tensor_mul(p.mf, p.mg);
+  const bool tc = !p.kara && use_tensor_mul(p.mf, p.mg);
   int lmax = p.lf > p.lg ? p.lf : p.lg;
   const size_t stage = (size_t)(lmax + PK_PAD_WORDS) * p.in_words * 4;
   const char* fz = getenv("KMX_FUSE");
@@ -352,8 +372,13 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.P = prod; ma.p_stride = p.ps; ma.spill = spill;
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
   ma.counter = (int*)cnt;
+  ma.err = err;
   prof_begin(1, st);
-  if (tc && !fuse && use_tcj(p.mf, p.mg, (long long)p.batch * p.P)) {
+  if (p.kara) {
+    int nl = 0;
+    if ((e = launch_kara(ma, w + p.off_kara, st, &nl)) != cudaSuccess) return KMX_ECUDA;
+    g_launches += nl - 1;
+  } else if (tc && !fuse && use_tcj(p.mf, p.mg, (long long)p.batch * p.P)) {
     if ((e = launch_tcmulj(ma, st)) != cudaSuccess) return KMX_ECUDA;
   } else if (tc) {
     if ((e = launch_tcmul(ma, st, fuse ? &pa : nullptr, p.P)) != cudaSuccess) return KMX_ECUDA;
@@ -1070,7 +1095,8 @@ int kmx_mul_plan(int variant, int batch, int len_f, int len_g, int coeff_bits, u
   if (rc) return rc;
   long long o[8] = {0, 0, 0, 0, 0, 0, 0, 0};
   const long long nprod = (long long)batch * p.P;
-  if (use_tensor_mul(p.mf, p.mg) && !use_tcj(p.mf, p.mg, nprod)) tc_plan_info(p.mf, p.mg, nprod, o);
+  if (p.kara) o[0] = 3, o[1] = kara_levels(p.mf, p.mg);  // Karatsuba over the engines
+  else if (use_tensor_mul(p.mf, p.mg) && !use_tcj(p.mf, p.mg, nprod)) tc_plan_info(p.mf, p.mg, nprod, o);
   else if (use_tensor_mul(p.mf, p.mg)) o[0] = 2;  // chunked single-tile kernel
   for (int i = 0; i < 8; i++) out8[i] = o[i];
   return KMX_OK;
@@ -1080,7 +1106,22 @@ int kmx_mul_engine(int variant, int len_f, int len_g, int coeff_bits, unsigned f
   KsPlan p;
   int rc = make_plan(p, variant, 1, len_f, len_g, coeff_bits, 0, flags);
   if (rc) return rc;
-  return use_tensor_mul(p.mf, p.mg) ? 1 : 0;
+  // Karatsuba levels: the engine of the leaves (the split halves)
+  int ma = p.mf, mb = p.mg;
+  while (!mul_engine_takes(ma, mb)) {
+    const int mx = ma > mb ? ma : mb, h = (mx + 1) / 2;
+    if ((ma < mb ? ma : mb) > h) ma = mb = h + 1;
+    else if (ma >= mb) ma = h;
+    else mb = h;
+  }
+  return use_tensor_mul(ma, mb) ? 1 : 0;
+}
+
+int kmx_mul_karatsuba_levels(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags) {
+  KsPlan p;
+  int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);
+  if (rc) return rc;
+  return p.kara ? kara_levels(p.mf, p.mg) : 0;
 }
 
 const char* kmx_error_string(int code) {

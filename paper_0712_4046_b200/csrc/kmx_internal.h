@@ -48,6 +48,7 @@ struct MulArgs {
   int nprod, nbands, G, TI;
   int* counter;                                   // work-unit counter, zeroed before launch
   int flags_no_tune;                              // KMX_NO_TUNE: the cost model's tiling, no timing runs
+  uint32_t* err;                                  // error flag (Karatsuba recombination check)
 };
 struct ConvArgs {
   const int32_t* A; long long a_stride;
@@ -68,6 +69,34 @@ bool tc_supported(int ma, int mb, size_t stage_bytes = 0);
 // operands never reach global memory (MulArgs A/B unused).
 cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk = nullptr, int P = 1);
 double measure_tc_peak(int iters);
+// engine choice (kmx_api.cu): the tensor cores for this shape, and whether
+// some engine takes the whole product (else Karatsuba splits it)
+bool mul_use_tensor(int ma, int mb);
+bool mul_engine_takes(int ma, int mb);
+
+// ---------------------------------------------------- Karatsuba (kmx_kara.cu)
+// Linear-combination normalizer: out[z] = sum_t sign_t term_t[z] 2^(32 off_t),
+// each term a product in the engines' format (limbs + optional band spills).
+constexpr int LC_MAXT = 5;
+constexpr int KARA_MAX_DEPTH = 4;
+struct LcTerm {
+  const uint32_t* p; long long stride; long long len; long long off; int sign;
+  const unsigned long long* spill; int nbands;    // [z][nbands][2] or null
+};
+struct LcArgs {
+  LcTerm t[LC_MAXT];
+  int nt;
+  uint32_t* out; long long out_stride; long long out_len;
+  int nchunks;                                    // set by launch_lincomb
+  void* maps;                                     // [nprod][nchunks] chunk carry maps
+  uint32_t* err;
+};
+cudaError_t launch_lincomb(const LcArgs& a, long long nprod, cudaStream_t st);
+size_t lc_map_bytes(long long nprod, int out_len);
+bool kara_used(int ma, int mb);
+int kara_levels(int ma, int mb);
+size_t kara_ws_bytes(int ma, int mb, long long nprod);
+cudaError_t launch_kara(const MulArgs& a, void* ws, cudaStream_t st, int* nlaunch);
 
 // Signed inputs (bias lift): the coefficient writers apply
 // h = h' - 2^(b-1) (J*f' + J*g') + 2^(2b-2) (J*J) before storing, from the

@@ -35,7 +35,9 @@ def log_uniform(rng, hi):
 
 
 def test_exhaustive_small_lengths(kmx):
-    checked = 0
+    # the reference's leg pairs vectors of equal length (266,304 pairs); the
+    # unequal-length combinations are checked too (74,752 more)
+    checked = equal = 0
     for lf, lg in itertools.product((1, 2, 3), repeat=2):
         F = np.array(list(itertools.product(range(8), repeat=lf)), dtype=np.int64)
         G = np.array(list(itertools.product(range(8), repeat=lg)), dtype=np.int64)
@@ -53,7 +55,8 @@ def test_exhaustive_small_lengths(kmx):
             assert h.shape[2] == 1
             assert np.array_equal(h[:, :, 0].astype(np.int64), want), (lf, lg, v)
         checked += len(fb)
-    assert checked == 266304
+        equal += len(fb) if lf == lg else 0
+    assert equal == 266304 and checked == 341056
 
 
 def test_randomized_10k(kmx):

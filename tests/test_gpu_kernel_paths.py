@@ -28,6 +28,8 @@ SETTINGS = [
     {"KMX_RECON_SPEC": "1", "KMX_RECON_MINB": "0"},  # recon: speculative stores from round 1; uncapped registers
     {"KMX_RECON_SPEC": "0", "KMX_PACK_FAST": "0"},  # recon: separate output walk; looped pack windows only
     {"KMX_RECON_MINB": "6", "KMX_RECON_V": "4"},  # recon: 6-CTA register cap; 4 steps per thread
+    {"KMX_KARA_MIN": "600"},    # Karatsuba levels on every product above 600 limbs (tensor-core leaves)
+    {"KMX_KARA_MIN": "300", "KMX_TC": "0"},  # Karatsuba over integer-pipe leaves, up to 4 levels
 ]
 
 
