@@ -116,7 +116,8 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
  * pack_negated_reversed (3) (pack.py:79-110) of `batch` coefficient vectors
  * [batch][len][in_words] at width_bits (2*width_bits >= coeff_bits, else
  * KMX_EINVAL as pack.py:55-59).  out: [batch][out_limbs] |value| little-endian
- * limbs, out_limbs >= kmx_pack_limbs(); meta (required on the device entry,
+ * limbs, out_limbs >= kmx_pack_limbs() and a multiple of 4 (out 16-byte
+ * aligned: K1 stores limb quads); meta (required on the device entry,
  * nullable on the host entry):
  * [batch][2] = {sign (1: negative), bit length of |value|}.  Coefficients
  * outside [0, 2^coeff_bits) latch KMX_EINVAL (read with kmx_ws_status);
@@ -152,6 +153,20 @@ int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits,
                 void* workspace, size_t ws_bytes, void* stream);
 int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits,
                      const int32_t* f, const int32_t* g, int64_t* h);
+
+/* Bivariate reductions over R = Z for coefficients of any width (bipoly.py
+ * :177-278 with ring_z(); the reference takes any integer): f, g
+ * [batch][lx][ly][in_words] two's-complement integers with |c| < 2^coeff_bits
+ * (checked -> KMX_EINVAL via kmx_ws_status); h [batch][2lx-1][2ly-1]
+ * [out_words] two's complement, out_words >= kmx_bks_wide_out_words().  The
+ * reduction runs over Z/p_i for word-sized primes (kmx_bks_mod_mul each) and
+ * the coefficients are recovered by CRT on the device. */
+int kmx_bks_wide_out_words(int lx, int ly, int coeff_bits);
+size_t kmx_bks_wide_workspace_bytes(int variant, int batch, int lx, int ly, int coeff_bits);
+int kmx_bks_wide_mul(int variant, int batch, int lx, int ly, int coeff_bits, const uint32_t* f, const uint32_t* g,
+                     int in_words, uint32_t* h, int out_words, void* workspace, size_t ws_bytes, void* stream);
+int kmx_bks_wide_mul_host(int variant, int batch, int lx, int ly, int coeff_bits, const uint32_t* f,
+                          const uint32_t* g, int in_words, uint32_t* h, int out_words);
 
 /* (Z/nZ)[x] products, 2 <= n < 2^64 (kronmul.modpoly.mod_mul,
  * modpoly.py:95-115): f [batch][len_f], g [batch][len_g] u64 coefficients in

@@ -64,6 +64,10 @@ _SIGS = {
     "kmx_bks_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "kmx_bks_mul": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "kmx_bks_mul_host": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp]),
+    "kmx_bks_wide_out_words": (_i, [_i, _i, _i]),
+    "kmx_bks_wide_workspace_bytes": (_sz, [_i, _i, _i, _i, _i]),
+    "kmx_bks_wide_mul": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i, _vp, _sz, _vp]),
+    "kmx_bks_wide_mul_host": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _i, _vp, _i]),
     "kmx_mod_workspace_bytes": (_sz, [_i, _i, _i, _i, ctypes.c_uint64]),
     "kmx_mod_mul": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp, _vp, _sz, _vp]),
     "kmx_mod_mul_host": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp, _u64p]),

@@ -7,9 +7,11 @@ bks_standard / bks_reciprocal / bks_negated / bks_four (:177-278).
 With ring_z() or ring_zmod(n) and the default univariate multiplier, the
 whole reduction (evaluation, univariate products, half-sums and overlap
 recovery) runs in libkmx.so: over Z through kmx_bks_mul (int32 coefficients,
-int64 products), over Z/nZ through kmx_bks_mod_mul (u64 residues; the
-univariate products go through the integer KS path, kmx_mod_mul).  Custom
-univariate multipliers raise NotImplementedError -- never a silent CPU path.
+int64 products) or, for wider coefficients, kmx_bks_wide_mul (any width: the
+reduction over word-sized primes and CRT on the device); over Z/nZ through
+kmx_bks_mod_mul (u64 residues; the univariate products go through the
+integer KS path, kmx_mod_mul).  Custom univariate multipliers raise
+NotImplementedError -- never a silent CPU path.
 """
 from __future__ import annotations
 
@@ -127,14 +129,35 @@ def _bks(variant: int, f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None,
     ga = np.asarray(g.coeffs, dtype=object)
     mx = max(max(abs(int(c)) for c in fa.reshape(-1)), max(abs(int(c)) for c in ga.reshape(-1)))
     cb = max(1, mx.bit_length())
-    if cb > 30:
-        raise ValueError("coefficient magnitude beyond the GPU path's int64 accumulation bound (|c| < 2^30)")
-    f32 = np.ascontiguousarray(fa.astype(np.int64).astype(np.int32))
-    g32 = np.ascontiguousarray(ga.astype(np.int64).astype(np.int32))
-    h = np.zeros((2 * lx - 1, 2 * ly - 1), dtype=np.int64)
-    rc = lib().kmx_bks_mul_host(variant, 1, lx, ly, cb, _lib.ptr(f32), _lib.ptr(g32), _lib.ptr(h))
-    check(rc, "bks")
-    return BiPoly(tuple(tuple(int(v) for v in row) for row in h))
+    if cb <= 30:
+        # int32 inputs, int64 univariate products (kmx_bks_mul) when the
+        # accumulation bound holds; KMX_EINVAL otherwise -> the wide path
+        f32 = np.ascontiguousarray(fa.astype(np.int64).astype(np.int32))
+        g32 = np.ascontiguousarray(ga.astype(np.int64).astype(np.int32))
+        h = np.zeros((2 * lx - 1, 2 * ly - 1), dtype=np.int64)
+        rc = lib().kmx_bks_mul_host(variant, 1, lx, ly, cb, _lib.ptr(f32), _lib.ptr(g32), _lib.ptr(h))
+        if rc != _lib.KMX_EINVAL:
+            check(rc, "bks")
+            return BiPoly(tuple(tuple(int(v) for v in row) for row in h))
+    return _bks_wide(variant, f, g, lx, ly, cb)
+
+
+def _bks_wide(variant: int, f: BiPoly, g: BiPoly, lx: int, ly: int, cb: int) -> BiPoly:
+    """Any coefficient width over Z: kmx_bks_wide_mul (the reduction over
+    word-sized primes, CRT on the device; two's-complement multiword I/O)."""
+    from .words import ints_to_words, words_to_ints
+    iw = (cb + 1 + 31) // 32
+    ow = lib().kmx_bks_wide_out_words(lx, ly, cb)
+    if ow < 0:
+        check(ow, "bks")
+    fw = ints_to_words([c for row in f.coeffs for c in row], iw, signed=True)
+    gw = ints_to_words([c for row in g.coeffs for c in row], iw, signed=True)
+    h = np.zeros(((2 * lx - 1) * (2 * ly - 1), ow), dtype=np.uint32)
+    check(lib().kmx_bks_wide_mul_host(variant, 1, lx, ly, cb, _lib.ptr(fw), _lib.ptr(gw), iw, _lib.ptr(h), ow),
+          "bks")
+    vals = words_to_ints(h, signed=True)
+    w2 = 2 * ly - 1
+    return BiPoly(tuple(tuple(vals[i * w2:(i + 1) * w2]) for i in range(2 * lx - 1)))
 
 
 def bks_standard(f: BiPoly, g: BiPoly, ring: RingOps, mul: UniMul | None = None) -> BiPoly:

@@ -28,6 +28,10 @@ using namespace kmx;
 namespace {
 
 int bitlen_u64(unsigned long long x) { return x ? 64 - __builtin_clzll(x) : 0; }
+int getenv_int(const char* n, int d) {
+  const char* v = getenv(n);
+  return v && *v ? atoi(v) : d;
+}
 int cur_dev() {
   int d = 0;
   cudaGetDevice(&d);
@@ -134,6 +138,9 @@ struct KsPlan {
   ReconStream rs[2];
   size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, off_cmap, off_kara, total;
   bool kara;
+  bool wide;  // digits past the fast finish / reconstruction budgets (kmx_wide.cu)
+  size_t off_wnum, off_wmaps, off_wscr;
+  long long wt_stride;
   int fin_chunks;  // 256-limb chunks of the longest finish stream (chunk-parallel finish maps)
 };
 
@@ -260,9 +267,9 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
     p.rs[1] = ReconStream{1, 3, n_odd, 1, 2};
     p.cnt_max = n_even + 1; p.dslots = 4;
   }
-  if (p.W > 32 * (FIN_HALO - 1)) return KMX_EINVAL;
   p.dwords = (p.W + 31) / 32;
-  if (p.nrs && p.dwords > 17) return KMX_EINVAL;
+  p.wide = p.W > 32 * (FIN_HALO - 1) || (p.nrs && p.dwords > 17) || (getenv_int("KMX_WIDE", 0) == 1 && !p.sign);
+  if (p.wide && p.sign) return KMX_EINVAL;  // signed inputs have b <= 32: never wide
   // workspace layout
   size_t o = 0;
   p.off_err = o; o = align256(o + 16);
@@ -291,11 +298,67 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
   p.kara = kara_used(p.mf, p.mg);
   p.off_kara = o;
   if (p.kara) o = align256(o + kara_ws_bytes(p.mf, p.mg, (long long)batch * p.P));
+  if (p.wide) {  // normalized stream numerators, their carry maps, reconstruction scratch
+    p.wt_stride = (p.mp + 1 + 3) & ~3LL;
+    p.off_wnum = o; o = align256(o + (size_t)batch * p.wt_stride * 4);
+    p.off_wmaps = o; o = align256(o + lc_map_bytes(batch, p.mp + 1));
+    p.off_wscr = o; o = align256(o + wide_recon_scratch_words(batch, p.nrs, p.dwords) * 4);
+  }
   p.total = o;
   return KMX_OK;
 }
 
 int cuda_rc(cudaError_t e) { return e == cudaSuccess ? KMX_OK : KMX_ECUDA; }
+
+// finish + reconstruction for wide digits (kmx_wide.cu): per stream, the
+// numerator P +- sgn(Q)|Q| normalized by the linear-combination kernels, a
+// bit-field gather of its digits, then the multiword reconstruction
+int run_wide(const KsPlan& p, const FinishArgs& fa, char* w, cudaStream_t st) {
+  uint32_t* T = (uint32_t*)(w + p.off_wnum);
+  cudaError_t e;
+  for (int i = 0; i < p.ns; i++) {
+    const Stream& S = p.st[i];
+    LcArgs la;
+    memset(&la, 0, sizeof la);
+    la.maps = w + p.off_wmaps;
+    la.err = fa.err;
+    la.nt = 1;
+    const long long pstr = (long long)p.P * p.ps, sstr = (long long)p.P * p.nbands * 2;
+    la.t[0] = LcTerm{fa.P + (long long)S.zP * p.ps, pstr, p.mp, 0, +1, fa.spill + (long long)S.zP * p.nbands * 2,
+                     p.nbands, sstr, nullptr, 0, 0};
+    if (S.qsign) {
+      la.nt = 2;
+      la.t[1] = LcTerm{fa.P + (long long)S.zQ * p.ps, pstr, p.mp, 0, S.qsign, fa.spill + (long long)S.zQ * p.nbands * 2,
+                       p.nbands, sstr, fa.meta + 2 * S.qmeta, fa.meta_per_pair, 2 * fa.mf_slot_stride};
+    }
+    la.out = T;
+    la.out_stride = p.wt_stride;
+    la.out_len = p.mp + 1;
+    if ((e = launch_lincomb(la, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+    WideDigitArgs wa;
+    memset(&wa, 0, sizeof wa);
+    wa.T = T; wa.t_stride = p.wt_stride; wa.t_len = p.mp + 1;
+    wa.s = S;
+    wa.h = fa.h; wa.out_words = fa.out_words; wa.h_pair_stride = fa.h_pair_stride;
+    wa.dbuf = fa.dbuf; wa.dwords = fa.dwords; wa.dslot_stride = fa.dslot_stride; wa.dslots_pair = fa.dslots_pair;
+    wa.err = fa.err;
+    wa.batch = p.batch;
+    if ((e = launch_wide_digits(wa, st)) != cudaSuccess) return KMX_ECUDA;
+    g_launches += 3;
+  }
+  if (p.nrs) {
+    ReconArgs ra;
+    memset(&ra, 0, sizeof ra);
+    for (int i = 0; i < p.nrs; i++) ra.s[i] = p.rs[i];
+    ra.ns = p.nrs; ra.batch = p.batch; ra.W = p.W;
+    ra.dbuf = fa.dbuf; ra.dwords = p.dwords; ra.dslot_stride = fa.dslot_stride; ra.dslots_pair = p.dslots;
+    ra.h = fa.h; ra.out_words = fa.out_words; ra.h_pair_stride = fa.h_pair_stride;
+    ra.err = fa.err;
+    if ((e = launch_wide_recon(ra, (uint32_t*)(w + p.off_wscr), st)) != cudaSuccess) return KMX_ECUDA;
+    g_launches++;
+  }
+  return KMX_OK;
+}
 
 int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h, int out_words,
              void* ws, size_t ws_bytes, cudaStream_t st, uint32_t* err_shared = nullptr,
@@ -403,6 +466,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.nchunks = p.fin_chunks;
   ReconArgs ra;
   memset(&ra, 0, sizeof ra);
+  if (p.wide) return run_wide(p, fa, w, st);
   if (p.nrs) {
     for (int i = 0; i < p.nrs; i++) ra.s[i] = p.rs[i];
     ra.ns = p.nrs; ra.batch = p.batch; ra.W = p.W;
@@ -974,7 +1038,8 @@ int kmx_pack(int kind, int batch, int len, int width_bits, int coeff_bits, const
   const int m = kmx_pack_limbs(len, width_bits, coeff_bits);
   if (m < 0) return m;
   if (2LL * width_bits < coeff_bits) return KMX_EINVAL;  // pack.py:55-59
-  if (out_limbs < m || ws_bytes < 256 || !workspace) return KMX_EINVAL;
+  if (out_limbs < m || (out_limbs & 3) || ws_bytes < 256 || !workspace) return KMX_EINVAL;
+  if (((uintptr_t)out & 15) || !meta) return KMX_EINVAL;  // K1 writes 16-byte limb quads
   g_launches = 0;
   if (batch == 0) return KMX_OK;
   cudaStream_t st = (cudaStream_t)stream;
@@ -999,6 +1064,7 @@ int kmx_pack_host(int kind, int batch, int len, int width_bits, int coeff_bits, 
                   uint32_t* out, int out_limbs, uint32_t* meta) {
   const int m = kmx_pack_limbs(len, width_bits, coeff_bits);
   if (m < 0) return m;
+  if (out_limbs & 3) return KMX_EINVAL;
   if (batch <= 0) return batch < 0 ? KMX_EINVAL : KMX_OK;
   int rc;
   HostCtx* c = host_ctx(&rc);
@@ -1021,7 +1087,9 @@ int kmx_pack_host(int kind, int batch, int len, int width_bits, int coeff_bits, 
 
 size_t kmx_reconstruct_workspace_bytes(int batch, int count, int dwords) {
   if (batch < 0 || count < 1 || dwords < 1) return 0;
-  return 256 + (size_t)batch * 2 * (count + 1) * dwords * 4;
+  size_t o = 256 + align256((size_t)batch * 2 * (count + 1) * dwords * 4);
+  if (dwords > 17) o += align256(wide_recon_scratch_words(batch, 1, dwords) * 4);  // kmx_wide.cu
+  return o;
 }
 
 int kmx_reconstruct(int batch, int count, int width_bits, const uint32_t* fwd, const uint32_t* rev, int dwords,
@@ -1029,11 +1097,11 @@ int kmx_reconstruct(int batch, int count, int width_bits, const uint32_t* fwd, c
   // The reconstruction kernel reads both streams from one digit buffer; the
   // standalone entry takes them as two arrays, so stage them in the
   // workspace: [batch][2][count+1][dwords] plus the error word.
-  if (batch < 0 || count < 1 || width_bits < 1 || dwords < (width_bits + 31) / 32 || dwords > 17 ||
+  if (batch < 0 || count < 1 || width_bits < 1 || dwords < (width_bits + 31) / 32 ||
       hwords < (2 * width_bits + 31) / 32)
     return KMX_EINVAL;
   const size_t slot = (size_t)(count + 1) * dwords;
-  const size_t need = 256 + (size_t)batch * 2 * slot * 4;
+  const size_t need = kmx_reconstruct_workspace_bytes(batch, count, dwords);
   if (ws_bytes < need) return KMX_EINVAL;
   cudaStream_t st = (cudaStream_t)stream;
   uint32_t* err = (uint32_t*)workspace;
@@ -1051,7 +1119,9 @@ int kmx_reconstruct(int batch, int count, int width_bits, const uint32_t* fwd, c
   ra.dbuf = db; ra.dwords = dwords; ra.dslot_stride = (long long)slot; ra.dslots_pair = 2;
   ra.h = h; ra.out_words = hwords; ra.h_pair_stride = (long long)count * hwords; ra.err = err;
   ra.carries = carries;
-  cudaError_t e = launch_recon(ra, st);
+  cudaError_t e = dwords > 17 ? launch_wide_recon(ra, (uint32_t*)((char*)workspace + 256 +
+                                                                 align256((size_t)batch * 2 * slot * 4)), st)
+                              : launch_recon(ra, st);
   g_launches = 1;
   return cuda_rc(e);
 }

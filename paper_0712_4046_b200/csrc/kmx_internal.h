@@ -81,7 +81,10 @@ constexpr int LC_MAXT = 5;
 constexpr int KARA_MAX_DEPTH = 4;
 struct LcTerm {
   const uint32_t* p; long long stride; long long len; long long off; int sign;
-  const unsigned long long* spill; int nbands;    // [z][nbands][2] or null
+  const unsigned long long* spill; int nbands;    // band spills, band bi at spill[z * spill_stride + 2 bi]
+  long long spill_stride;                         // u64 entries per z (0: nbands * 2)
+  const uint32_t* smeta; long long smeta_stride; int smeta_off;  // optional: sign *= -1 when
+                                                  // smeta[z*stride] ^ smeta[z*stride + off] (mul_signed)
 };
 struct LcArgs {
   LcTerm t[LC_MAXT];
@@ -97,6 +100,8 @@ bool kara_used(int ma, int mb);
 int kara_levels(int ma, int mb);
 size_t kara_ws_bytes(int ma, int mb, long long nprod);
 cudaError_t launch_kara(const MulArgs& a, void* ws, cudaStream_t st, int* nlaunch);
+
+
 
 // Signed inputs (bias lift): the coefficient writers apply
 // h = h' - 2^(b-1) (J*f' + J*g') + 2^(2b-2) (J*J) before storing, from the
@@ -217,5 +222,23 @@ struct BivarPlan {
 cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h,
                          int32_t* evals, int64_t* prods, uint32_t* err, cudaStream_t st,
                          int* nlaunch);
+
+// ------------------------------------------- wide digits (kmx_wide.cu)
+// Digit widths past the chunked finish / register reconstruction
+// (W > 32 (FIN_HALO - 1) or reconstruction digits > 17 words): the
+// numerator of each stream normalized by the linear-combination kernels, a
+// bit-field gather for the digits, a sequential multiword reconstruction.
+struct WideDigitArgs {
+  const uint32_t* T; long long t_stride; long long t_len;  // normalized numerator [pair][t_len]
+  Stream s;
+  uint32_t* h; int out_words; long long h_pair_stride;
+  uint32_t* dbuf; int dwords; long long dslot_stride; int dslots_pair;
+  uint32_t* err;
+  int batch;
+};
+cudaError_t launch_wide_digits(const WideDigitArgs& a, cudaStream_t st);
+size_t wide_recon_scratch_words(int batch, int ns, int dwords);
+// ReconArgs with any dwords; scratch: wide_recon_scratch_words(...) words
+cudaError_t launch_wide_recon(const ReconArgs& a, uint32_t* scratch, cudaStream_t st);
 
 }  // namespace kmx

@@ -73,11 +73,17 @@ __device__ __forceinline__ long long lc_limb(const LcArgs& a, long long z, long 
     if (j < 0 || j >= T.len) continue;
     long long v = (long long)__ldg(T.p + z * T.stride + j);
     if (T.spill) {  // band spills fold in at band starts (kmx_finish.cuh)
-      const long long* sp = reinterpret_cast<const long long*>(T.spill) + z * T.nbands * 2;
-      if (j > 0 && (j & 255) == 0) v += sp[((j >> 8) - 1) * 2];
-      if (j > 1 && (j & 255) == 1) v += sp[((j >> 8) - 1) * 2 + 1];
+      const long long* sp =
+          reinterpret_cast<const long long*>(T.spill) + z * (T.spill_stride ? T.spill_stride : T.nbands * 2LL);
+      if (j > 0 && (j & 255) == 0 && (j >> 8) <= T.nbands) v += sp[((j >> 8) - 1) * 2];
+      if (j > 1 && (j & 255) == 1 && (j >> 8) <= T.nbands) v += sp[((j >> 8) - 1) * 2 + 1];
     }
-    s += T.sign > 0 ? v : -v;
+    int sg = T.sign;
+    if (T.smeta) {
+      const uint32_t* m = T.smeta + z * T.smeta_stride;
+      if (m[0] ^ m[T.smeta_off]) sg = -sg;
+    }
+    s += sg > 0 ? v : -v;
   }
   return s;
 }
@@ -338,8 +344,8 @@ cudaError_t node_mul(const MulArgs& base, int ma, int mb, const u32* A, long lon
       const long long xs = side ? bs : as;
       const int mx = side ? mb : ma;
       la.nt = 2;
-      la.t[0] = LcTerm{X, xs, h, 0, +1, nullptr, 0};
-      la.t[1] = LcTerm{X + h, xs, mx - h, 0, +1, nullptr, 0};
+      la.t[0] = LcTerm{X, xs, h, 0, +1, nullptr, 0, 0, nullptr, 0, 0};
+      la.t[1] = LcTerm{X + h, xs, mx - h, 0, +1, nullptr, 0, 0, nullptr, 0, 0};
       la.out = side ? SB : SA;
       la.out_stride = sw;
       la.out_len = h + 1;
@@ -359,11 +365,11 @@ cudaError_t node_mul(const MulArgs& base, int ma, int mb, const u32* A, long lon
     const long long p0 = pstride_of(cm[0][0], cm[0][1]), p2 = pstride_of(cm[1][0], cm[1][1]),
                     p1 = pstride_of(cm[2][0], cm[2][1]);
     la.nt = 5;
-    la.t[0] = LcTerm{Z[0], p0, l0, 0, +1, ZS[0], nb0};
-    la.t[1] = LcTerm{Z[2], p1, l1, h, +1, ZS[2], nb1};
-    la.t[2] = LcTerm{Z[0], p0, l0, h, -1, ZS[0], nb0};
-    la.t[3] = LcTerm{Z[1], p2, l2, h, -1, ZS[1], nb2};
-    la.t[4] = LcTerm{Z[1], p2, l2, 2LL * h, +1, ZS[1], nb2};
+    la.t[0] = LcTerm{Z[0], p0, l0, 0, +1, ZS[0], nb0, 0, nullptr, 0, 0};
+    la.t[1] = LcTerm{Z[2], p1, l1, h, +1, ZS[2], nb1, 0, nullptr, 0, 0};
+    la.t[2] = LcTerm{Z[0], p0, l0, h, -1, ZS[0], nb0, 0, nullptr, 0, 0};
+    la.t[3] = LcTerm{Z[1], p2, l2, h, -1, ZS[1], nb2, 0, nullptr, 0, 0};
+    la.t[4] = LcTerm{Z[1], p2, l2, 2LL * h, +1, ZS[1], nb2, 0, nullptr, 0, 0};
   } else {
     const bool along_a = ma >= mb;
     const u32* CA[2] = {A, along_a ? A + h : A};
@@ -373,7 +379,7 @@ cudaError_t node_mul(const MulArgs& base, int ma, int mb, const u32* A, long lon
                         nb_of(cm[c][0], cm[c][1]), child, depth + 1, st, nl)) != cudaSuccess)
         return e;
     la.nt = 2;
-    la.t[0] = LcTerm{Z[0], pstride_of(cm[0][0], cm[0][1]), cm[0][0] + cm[0][1], 0, +1, ZS[0], nb_of(cm[0][0], cm[0][1])};
+    la.t[0] = LcTerm{Z[0], pstride_of(cm[0][0], cm[0][1]), cm[0][0] + cm[0][1], 0, +1, ZS[0], nb_of(cm[0][0], cm[0][1]), 0, nullptr, 0, 0};
     la.t[1] = LcTerm{Z[1], pstride_of(cm[1][0], cm[1][1]), cm[1][0] + cm[1][1], h, +1, ZS[1],
                      nb_of(cm[1][0], cm[1][1])};
   }

@@ -2,6 +2,7 @@
 // coefficient vectors at +-2^N, +-2^-N (pack.py:62-110, bignat._pack_ints
 // bignat.py:411-428), one block per (pair, pack op); the per-operand body is
 // pack_op in kmx_pack.cuh (shared with the fused tensor-core prologue).
+#include <cstdio>
 #include <cstdlib>
 
 #include "kmx_common.cuh"
@@ -62,6 +63,9 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
     k_pack_pair<<<batch * (a.nops / 2), T, smem, st>>>(b);
     return cudaGetLastError();
   }
+  if (getenv("KMX_DEBUG_PACK"))
+    fprintf(stderr, "launch_pack: batch=%d nops=%d T=%d stage=%d smem=%zu N=%d b=%d iw=%d m=%d\n", batch, a.nops, T,
+            b.stage, smem, a.N, a.b, a.in_words, mmax);
   if (b.stage) {
     if (smem > 44 * 1024) {  // + static shared memory must fit the opt-in limit
       cudaError_t e = cudaFuncSetAttribute(k_pack<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -71,7 +75,9 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   } else {
     k_pack<false><<<batch * a.nops, T, 0, st>>>(b);
   }
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && getenv("KMX_DEBUG_PACK")) fprintf(stderr, "launch_pack: %s\n", cudaGetErrorString(e));
+  return e;
 }
 
 }  // namespace kmx

@@ -23,17 +23,18 @@ KIND = {"pack": 0, "pack_negated": 1, "pack_reversed": 2, "pack_negated_reversed
 
 
 def pack_batch(kind: int, coeffs: np.ndarray, width_bits: int, coeff_bits: int):
-    """coeffs [batch, len, words] uint32 -> (|values| [batch, limbs] uint32,
+    """coeffs [batch, len, words] uint32 -> (|values| [batch, limbs] uint32
+    (limbs = kmx_pack_limbs rounded up to a multiple of 4),
     meta [batch, 2] = sign, bit length) through kmx_pack_host."""
     coeffs = np.ascontiguousarray(coeffs, dtype=np.uint32)
     batch, length, words = coeffs.shape
     m = lib().kmx_pack_limbs(length, width_bits, coeff_bits)
     if m < 0:
         check(m, "pack")
-    out = np.zeros((batch, m), dtype=np.uint32)
+    out = np.zeros((batch, (m + 3) & ~3), dtype=np.uint32)  # K1 stores 16-byte limb quads
     meta = np.zeros((batch, 2), dtype=np.uint32)
     check(lib().kmx_pack_host(kind, batch, length, width_bits, coeff_bits, _lib.ptr(coeffs), words,
-                              _lib.ptr(out), m, _lib.ptr(meta)), "pack")
+                              _lib.ptr(out), out.shape[1], _lib.ptr(meta)), "pack")
     return out, meta
 
 

@@ -10,7 +10,9 @@
 #   launches  ncu launch list of the default command           -> TAG_launches.csv
 #   full      ncu --set full of the c2 ks4 hot kernels         -> TAG_full.ncu-rep
 #   sanitize  compute-sanitizer memcheck/racecheck/synccheck   -> TAG_san_*.log
-#             over tools/sanitize_suite.py (reduced suite)
+#             over tools/sanitize_suite.py (reduced suite); NOTE: the round-2
+#             GPU pool refuses compute-sanitizer (exit 86, "closed on this
+#             pool"), so this mode only runs where the tool is allowed
 # Each step runs only after the previous one of the same mode exited 0
 # (profilers never run on a command that has not already passed without them).
 set -u
