@@ -148,6 +148,11 @@ int kmx_reconstruct_host(int batch, int count, int width_bits, const uint32_t* f
  * int64.  coeff_bits bounds |c| < 2^coeff_bits (<= 30) and must keep every
  * univariate product coefficient inside int64 (checked -> KMX_EINVAL). */
 size_t kmx_bks_workspace_bytes(int variant, int batch, int lx, int ly);
+/* Workspace for this coefficient bound: large enough for the univariate
+ * products to run on the integer KS path (tensor cores) where that is the
+ * engine; kmx_bks_workspace_bytes() sizes the k_conv engine, which
+ * kmx_bks_mul falls back to when the workspace is smaller. */
+size_t kmx_bks_workspace_bytes_cb(int variant, int batch, int lx, int ly, int coeff_bits);
 int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits,
                 const int32_t* f, const int32_t* g, int64_t* h,
                 void* workspace, size_t ws_bytes, void* stream);

@@ -132,7 +132,7 @@ class BksBatch:
     def __init__(self, variant: int, batch: int, lx: int, ly: int, coeff_bits: int, device=None):
         torch = _torch()
         self.variant, self.batch, self.lx, self.ly, self.coeff_bits = variant, batch, lx, ly, coeff_bits
-        self.ws_bytes = lib().kmx_bks_workspace_bytes(variant, batch, lx, ly)
+        self.ws_bytes = lib().kmx_bks_workspace_bytes_cb(variant, batch, lx, ly, coeff_bits)
         if self.ws_bytes == 0:
             raise ValueError("invalid bivariate problem shape")
         self.device = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())

@@ -175,7 +175,14 @@ namespace kmx {
 void prof_mark(int slot, bool begin, cudaStream_t st) {
   if (begin) prof_begin(slot, st); else prof_end(slot, st);
 }
+bool prof_suspend() {
+  const bool was = g_prof.on;
+  g_prof.on = false;
+  return was;
+}
+void prof_resume(bool was) { g_prof.on = was; }
 void prof_reset() { for (int i = 0; i < 6; i++) g_prof.used[i] = false; }
+void prof_keep(int slot) { g_prof.used[slot] = true; }
 }  // namespace kmx
 
 namespace {

@@ -8,6 +8,7 @@
 //              int32 -> int64 column sums, one IMAD.WIDE per product term
 //   k_brecover half-sums, exact halving and the chunk overlap recovery
 //              (_overlap_recover bipoly.py:151-174; _split_chunks :146-148)
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -27,7 +28,8 @@ __device__ __forceinline__ void point_flags(int variant, int pt, int& rev, int& 
   else if (variant == 4) { alt = pt & 1; rev = (pt >> 1) & 1; }
 }
 
-// evals: [batch][P][2][Lu] int32 (f then g)
+// evals: [2][batch * P][Lu] int32 (all f evaluations, then all g evaluations:
+// each side is a contiguous [products][Lu] operand array for the KS path)
 __global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, const int32_t* g, int32_t* ev,
                                                uint32_t* err) {
   const int lx = p.lx, ly = p.ly, Lu = p.Lu, sp = p.spacing;
@@ -38,7 +40,8 @@ __global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, co
        id += (long long)gridDim.x * blockDim.x) {
     const int t = (int)(id % Lu);
     long long r = id / Lu;
-    const int side = (int)(r % 2); r /= 2;
+    const long long nprod = (long long)p.batch * p.P;
+    const int side = (int)(r / nprod); r -= side * nprod;
     const int pt = (int)(r % p.P);
     const long long pair = r / p.P;
     int rev, alt;
@@ -94,8 +97,11 @@ __device__ void overlap_recover(int count, int sp, int cl, int ybase, int ystep,
 }
 
 __global__ void __launch_bounds__(128) k_brecover(BivarPlan p, const int64_t* prods, long long p_stride,
-                                                  int64_t* h, uint32_t* err) {
+                                                  int64_t* h, uint32_t* err, uint32_t* err0) {
   const int pair = blockIdx.x;
+  // the KS products' error word leads the workspace (kmx_ws_status): fold the
+  // evaluation's range check into it
+  if (err0 && err0 != err && pair == 0 && threadIdx.x == 0 && *err) atomicOr(err0, *err);
   const int lx = p.lx, ly = p.ly;
   const int lx2 = 2 * lx - 1, ly2 = 2 * ly - 1;
   const int64_t* pr = prods + (long long)pair * p.P * p_stride;
@@ -145,10 +151,12 @@ __global__ void __launch_bounds__(128) k_brecover(BivarPlan p, const int64_t* pr
 }
 
 cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h, int32_t* evals,
-                         int64_t* prods, uint32_t* err, cudaStream_t st, int* nlaunch) {
+                         int64_t* prods, uint32_t* err, cudaStream_t st, int* nlaunch, void* ks_ws,
+                         size_t ks_ws_bytes, uint32_t* err0) {
   *nlaunch = 0;
   prof_reset();
-  const long long ne = (long long)p.batch * p.P * 2 * p.Lu;
+  const long long nprod = (long long)p.batch * p.P;
+  const long long ne = nprod * 2 * p.Lu;
   int grid = (int)std::min<long long>((ne + 255) / 256, 148LL * 32);
   if (grid < 1) grid = 1;
   prof_mark(0, true, st);
@@ -157,23 +165,40 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   (*nlaunch)++;
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  // univariate products (kmx_mul.cu)
-  int split, cw, nbands, tr;
-  mul_geometry(p.Lu, p.Lu, &split, &cw, &nbands, &tr);
-  const long long ps = (long long)nbands * cw;
-  ConvArgs ca;
-  ca.A = evals; ca.a_stride = 2LL * p.Lu;
-  ca.B = evals + p.Lu; ca.b_stride = 2LL * p.Lu;
-  ca.L = p.Lu;
-  ca.P = prods; ca.p_stride = ps;
-  ca.nprod = p.batch * p.P; ca.nbands = nbands; ca.G = split; ca.TI = tr;
-  ca.counter = (int*)(err + 1);
+  long long ps;
   prof_mark(1, true, st);
-  if ((e = launch_conv(ca, st)) != cudaSuccess) return e;
+  if (p.uni) {
+    // univariate products on the integer KS path (Kronecker substitution of
+    // the evaluations themselves): signed ebits-bit coefficients, int64
+    // (two-word two's complement) product coefficients
+    ps = 2LL * p.Lu - 1;
+    const bool was = prof_suspend();
+    const int rc = kmx_ks_mul(p.uni, (int)nprod, p.Lu, p.Lu, p.ebits, reinterpret_cast<const uint32_t*>(evals),
+                              reinterpret_cast<const uint32_t*>(evals + nprod * p.Lu), 1,
+                              reinterpret_cast<uint32_t*>(prods), 2, ks_ws, ks_ws_bytes, KMX_SIGNED, st);
+    prof_resume(was);
+    prof_keep(0);
+    prof_keep(1);
+    if (rc) return rc == KMX_ECUDA ? cudaErrorLaunchFailure : cudaErrorInvalidValue;
+    *nlaunch += kmx_last_launch_count();
+  } else {
+    // univariate products (kmx_mul.cu)
+    int split, cw, nbands, tr;
+    mul_geometry(p.Lu, p.Lu, &split, &cw, &nbands, &tr);
+    ps = (long long)nbands * cw;
+    ConvArgs ca;
+    ca.A = evals; ca.a_stride = p.Lu;
+    ca.B = evals + nprod * p.Lu; ca.b_stride = p.Lu;
+    ca.L = p.Lu;
+    ca.P = prods; ca.p_stride = ps;
+    ca.nprod = (int)nprod; ca.nbands = nbands; ca.G = split; ca.TI = tr;
+    ca.counter = (int*)(err + 1);
+    if ((e = launch_conv(ca, st)) != cudaSuccess) return e;
+    (*nlaunch)++;
+  }
   prof_mark(1, false, st);
-  (*nlaunch)++;
   prof_mark(2, true, st);
-  k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err);
+  k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err, err0);
   prof_mark(2, false, st);
   (*nlaunch)++;
   return cudaGetLastError();
@@ -185,6 +210,26 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
 using namespace kmx;
 
 namespace {
+int env_int_b(const char* n, int d) {
+  const char* v = getenv(n);
+  return v && *v ? atoi(v) : d;
+}
+
+// Univariate product engine: the integer KS path when its product
+// coefficients fit two words and the products are long enough for the tensor
+// cores to pay, else k_conv.  Measured at c3 (256 pairs of 64x64 u16 grids,
+// profiles/r02/bks_uni_c3.json): ks3 wins at Lu = 2080 and 4096 (1.57x /
+// 2.4x over k_conv), ks4 at Lu = 8065 (2.9x).  KMX_BKS_UNI=0 forces k_conv,
+// 1..4 a KS variant.
+int bks_uni(const BivarPlan& p) {
+  const int force = env_int_b("KMX_BKS_UNI", -1);
+  if (force == 0) return 0;
+  if (p.ebits > 32 || kmx_ks_out_words(p.Lu, p.Lu, p.ebits, KMX_SIGNED) != 2) return 0;
+  if (force >= 1 && force <= 4) return force;
+  if (p.Lu < env_int_b("KMX_BKS_KS_MIN", 512)) return 0;
+  return p.Lu <= 4096 ? 3 : 4;
+}
+
 int bks_plan(BivarPlan& p, int variant, int batch, int lx, int ly, int coeff_bits) {
   if (variant < 1 || variant > 4 || batch < 0 || lx < 1 || ly < 1 || coeff_bits < 1 || coeff_bits > 30)
     return KMX_EINVAL;
@@ -203,32 +248,52 @@ int bks_plan(BivarPlan& p, int variant, int batch, int lx, int ly, int coeff_bit
   if (eb > 31) return KMX_EINVAL;
   double bound = (double)p.Lu * (double)(1ULL << eb) * (double)(1ULL << eb) * 2.0;
   if (bound >= 9.2e18) return KMX_EINVAL;
+  p.ebits = eb + 1;  // two's-complement width of the evaluations
+  p.uni = bks_uni(p);
   return KMX_OK;
 }
 
 size_t align256b(size_t x) { return (x + 255) & ~(size_t)255; }
 
-void bks_layout(const BivarPlan& p, size_t* off_ev, size_t* off_pr, size_t* total) {
-  int split, cw, nbands, tr;
-  mul_geometry(p.Lu, p.Lu, &split, &cw, &nbands, &tr);
-  const long long ps = (long long)nbands * cw;
-  size_t o = 256;
-  *off_ev = o;
-  o = align256b(o + (size_t)p.batch * p.P * 2 * p.Lu * 4);
-  *off_pr = o;
-  o = align256b(o + (size_t)p.batch * p.P * ps * 8);
-  *total = o;
+struct BksLayout { size_t ks, err, ev, pr, total; };
+
+// [KS workspace (its error word first: kmx_ws_status)] [error word + conv
+// counter] [evaluations [2][B P][Lu]] [products]
+BksLayout bks_layout(const BivarPlan& p) {
+  BksLayout L;
+  const long long nprod = (long long)p.batch * p.P;
+  L.ks = p.uni ? align256b(kmx_ks_workspace_bytes(p.uni, (int)nprod, p.Lu, p.Lu, p.ebits, KMX_SIGNED)) : 0;
+  size_t o = L.ks;
+  L.err = o; o += 256;
+  L.ev = o; o = align256b(o + (size_t)nprod * 2 * p.Lu * 4);
+  long long ps;
+  if (p.uni) {
+    ps = 2LL * p.Lu - 1;
+  } else {
+    int split, cw, nbands, tr;
+    mul_geometry(p.Lu, p.Lu, &split, &cw, &nbands, &tr);
+    ps = (long long)nbands * cw;
+  }
+  L.pr = o; o = align256b(o + (size_t)nprod * ps * 8);
+  L.total = o;
+  return L;
 }
 }  // namespace
 
 extern "C" {
 
 size_t kmx_bks_workspace_bytes(int variant, int batch, int lx, int ly) {
+  // the k_conv layout: valid for every coefficient bound
   BivarPlan p;
   if (bks_plan(p, variant, batch, lx, ly, 1)) return 0;
-  size_t a, b, t;
-  bks_layout(p, &a, &b, &t);
-  return t;
+  p.uni = 0;
+  return bks_layout(p).total;
+}
+
+size_t kmx_bks_workspace_bytes_cb(int variant, int batch, int lx, int ly, int coeff_bits) {
+  BivarPlan p;
+  if (bks_plan(p, variant, batch, lx, ly, coeff_bits)) return 0;
+  return std::max(bks_layout(p).total, kmx_bks_workspace_bytes(variant, batch, lx, ly));
 }
 
 int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits, const int32_t* f, const int32_t* g,
@@ -236,17 +301,22 @@ int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits, const in
   BivarPlan p;
   int rc = bks_plan(p, variant, batch, lx, ly, coeff_bits);
   if (rc) return rc;
-  size_t oe, op, tot;
-  bks_layout(p, &oe, &op, &tot);
-  if (ws_bytes < tot) return KMX_EINVAL;
+  BksLayout L = bks_layout(p);
+  if (ws_bytes < L.total && p.uni) {  // a workspace sized for k_conv only
+    p.uni = 0;
+    L = bks_layout(p);
+  }
+  if (ws_bytes < L.total) return KMX_EINVAL;
   if (batch == 0) return KMX_OK;
   cudaStream_t st = (cudaStream_t)stream;
   char* w = (char*)workspace;
-  uint32_t* err = (uint32_t*)w;
+  uint32_t* err = (uint32_t*)(w + L.err);
   if (cudaMemsetAsync(err, 0, 8, st) != cudaSuccess) return KMX_ECUDA;  // error flag + work counter
   int nl = 0;
-  cudaError_t e = launch_bivar(p, f, g, h, (int32_t*)(w + oe), (int64_t*)(w + op), err, st, &nl);
+  cudaError_t e = launch_bivar(p, f, g, h, (int32_t*)(w + L.ev), (int64_t*)(w + L.pr), err, st, &nl,
+                               p.uni ? w : nullptr, L.ks, (uint32_t*)w);
   g_launches = nl;
+  if (e == cudaErrorInvalidValue) return KMX_EINVAL;
   return e == cudaSuccess ? KMX_OK : KMX_ECUDA;
 }
 
@@ -263,8 +333,7 @@ int kmx_bks_mul_host(int variant, int batch, int lx, int ly, int coeff_bits, con
   BivarPlan p;
   int rc = bks_plan(p, variant, batch, lx, ly, coeff_bits);
   if (rc) return rc;
-  size_t oe, op, tot;
-  bks_layout(p, &oe, &op, &tot);
+  const size_t tot = kmx_bks_workspace_bytes_cb(variant, batch, lx, ly, coeff_bits);
   const size_t fb = (size_t)batch * lx * ly * 4;
   const size_t hb = (size_t)batch * (2 * lx - 1) * (2 * ly - 1) * 8;
   if (batch == 0) return KMX_OK;

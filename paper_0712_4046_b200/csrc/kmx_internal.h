@@ -182,6 +182,10 @@ struct BiasArgs {
 // 2 finish / brecover, 3 recon, 4 bias, 5 modred
 void prof_mark(int slot, bool begin, cudaStream_t st);
 void prof_reset();
+// nested C-ABI calls (the bivariate path's KS products) keep the caller's slots
+bool prof_suspend();
+void prof_keep(int slot);
+void prof_resume(bool was);
 
 // ------------------------------------------------------------- (Z/nZ)[x]
 // K9: h[i] = (sum_q prod[i][q] 2^(32q)) mod n, tpow[q] = 2^(32q) mod n
@@ -218,10 +222,12 @@ struct BivarPlan {
   int spacing;    // chunk spacing in the evaluation
   int n4;         // four-point half length
   int cbits;      // declared bound |c| < 2^cbits, checked on the device (ERR_INVAL)
+  int uni;        // univariate products: 0 = k_conv (IMAD), 1..4 = the integer KS path (variant)
+  int ebits;      // signed width of the evaluations (two's complement) for the KS path
 };
 cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h,
                          int32_t* evals, int64_t* prods, uint32_t* err, cudaStream_t st,
-                         int* nlaunch);
+                         int* nlaunch, void* ks_ws, size_t ks_ws_bytes, uint32_t* err0);
 
 // ------------------------------------------- wide digits (kmx_wide.cu)
 // Digit widths past the chunked finish / register reconstruction
