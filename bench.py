@@ -23,7 +23,7 @@ environment relaunches itself under torch.distributed.run with N ranks; every
 rank multiplies its own batch (independent pairs, no collective on the data
 path: weak scaling) and the step time is the max over ranks.
 ``--impl reference`` times the reference algorithm's CPU implementation (the
-oracle port of kronmul, within 0-10% of the reference's own time,
+oracle port of kronmul, 0-16% slower per pair than the reference itself,
 profiles/r02/port_vs_reference.json) on all host cores of rank 0.
 """
 from __future__ import annotations
@@ -730,8 +730,8 @@ def run_reference(args, cfg):
                          "sample": f"{per_step} pairs per step of {cfg['desc']} ({VNAME[v]}) through "
                                    f"oracle/ks_oracle.py over {cores} cores (the reference is pure "
                                    f"Python; its restatement runs here because /root/reference is "
-                                   f"absent on the GPU box; measured within 0-10% of the reference's "
-                                   f"own per-pair time, profiles/r02/port_vs_reference.json)",
+                                   f"absent on the GPU box; measured 0-16% slower per pair than the reference's "
+                                   f"own (profiles/r02/port_vs_reference.json), so a GPU/port ratio overstates the GPU/reference ratio by at most that)",
                          "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "poly products/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
