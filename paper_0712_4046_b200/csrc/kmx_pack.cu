@@ -38,8 +38,24 @@ static bool pairable(const PackArgs& a) {
   return true;
 }
 
+bool pack_w1_ok(const PackArgs& a);
+cudaError_t launch_pack_w1(const PackArgs& a, int batch, bool paired, cudaStream_t st);
+
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   static const int use_pair = getenv("KMX_PACK_PAIR") ? atoi(getenv("KMX_PACK_PAIR")) : 1;
+  // one-word coefficients at 2N >= 32, + and - operands from one staged vector
+  // (ks3 / ks4) up to 1024 limbs: the warp-per-job kernel (kmx_pack1.cu).
+  // Measured at c2: ks4 pack 48.8 -> 38.0 us, ks3 37 -> 37.5 us (m = 1184);
+  // single-operand jobs with long operands (ks1 / ks2, m = 2367 / 1184) are
+  // faster on the block kernel below (35 / 38 us vs 56 / 49 us).
+  {
+    int mmax0 = 0;
+    for (int i = 0; i < a.nops; i++) mmax0 = a.op[i].m > mmax0 ? a.op[i].m : mmax0;
+    static const int w1_force = getenv("KMX_PACK_W1") ? atoi(getenv("KMX_PACK_W1")) : -1;
+    const bool paired = use_pair && pairable(a);
+    if (pack_w1_ok(a) && (w1_force == 1 || (paired && mmax0 <= 1024)))
+      return launch_pack_w1(a, batch, paired, st);
+  }
   int mmax = 0;
   for (int i = 0; i < a.nops; i++) mmax = a.op[i].m > mmax ? a.op[i].m : mmax;
   int T = ((mmax + PK_V - 1) / PK_V + 31) & ~31;  // sized to the operand
