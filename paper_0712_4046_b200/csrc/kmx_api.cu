@@ -67,9 +67,9 @@ bool use_tcj(int ma, int mb, long long nprod) {
   return tcj_plan(ma, mb, nullptr, force < 0);
 }
 
-int tc_force() {
-  static const int f = getenv("KMX_TC") && *getenv("KMX_TC") ? atoi(getenv("KMX_TC")) : -1;
-  return f;
+int tc_force() {  // read per call: tests switch KMX_TC inside one process
+  const char* v = getenv("KMX_TC");
+  return v && *v ? atoi(v) : -1;
 }
 bool use_tensor_mul(int ma, int mb) {
   const int force = tc_force();
@@ -136,7 +136,8 @@ struct KsPlan {
   int W, dwords, cnt_max, dslots;
   int nrs;
   ReconStream rs[2];
-  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, off_cmap, off_kara, total;
+  size_t off_err, off_meta, off_opf, off_opg, off_prod, off_spill, off_dbuf, off_scr, off_cmap, off_kara, off_pseg,
+      total;
   bool kara;
   bool wide;  // digits past the fast finish / reconstruction budgets (kmx_wide.cu)
   size_t off_wnum, off_wmaps, off_wscr;
@@ -301,6 +302,9 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
   }
   p.off_cmap = o;
   o = align256(o + (size_t)batch * p.ns * p.fin_chunks);
+  // segmented pack scratch (kmx_packseg.cu)
+  p.off_pseg = o;
+  o = align256(o + pack_seg_scratch_bytes(batch, 2 * p.P, std::max(p.mf, p.mg)));
   // Karatsuba levels above the engines (kmx_kara.cu): sums, sub-products, maps
   p.kara = kara_used(p.mf, p.mg);
   p.off_kara = o;
@@ -394,6 +398,8 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   memset(&pa, 0, sizeof pa);
   pa.nops = 2 * p.P;
   pa.N = p.N; pa.b = p.b; pa.in_words = p.in_words; pa.bias = p.sign; pa.err = err;
+  pa.scratch = w + p.off_pseg;
+  pa.scratch_bytes = pack_seg_scratch_bytes(p.batch, 2 * p.P, std::max(p.mf, p.mg));
   const bool validate = !(p.flags & KMX_NO_VALIDATE);
   for (int s = 0; s < p.P; s++) {
     PackOp& F = pa.op[s];

@@ -34,7 +34,10 @@ struct PackArgs {
   uint32_t* err;
   int stage;                  // set by launch_pack: coefficients staged in shared memory
   int fast1;                  // set by launch_pack: loop-free bitstream windows allowed (KMX_PACK_FAST)
+  void* scratch;              // segmented pack (kmx_packseg.cu): orders and segment carry maps
+  size_t scratch_bytes;
 };
+size_t pack_seg_scratch_bytes(int batch, int nops, int mmax);
 
 // -------------------------------------------------------------- multiply
 // G carries the row-split factor SPLIT (1, 2, 4): bands are CW = 256/SPLIT

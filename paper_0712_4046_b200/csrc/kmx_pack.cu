@@ -39,10 +39,14 @@ static bool pairable(const PackArgs& a) {
 }
 
 bool pack_w1_ok(const PackArgs& a);
+bool pack_seg_wanted(const PackArgs& a, int batch);
+cudaError_t launch_pack_seg(const PackArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_pack_w1(const PackArgs& a, int batch, bool paired, cudaStream_t st);
 
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   static const int use_pair = getenv("KMX_PACK_PAIR") ? atoi(getenv("KMX_PACK_PAIR")) : 1;
+  // long operands, small batches: segments of every operand on separate CTAs
+  if (pack_seg_wanted(a, batch)) return launch_pack_seg(a, batch, st);
   // one-word coefficients at 2N >= 32, + and - operands from one staged vector
   // (ks3 / ks4) up to 1024 limbs: the warp-per-job kernel (kmx_pack1.cu).
   // Measured at c2: ks4 pack 48.8 -> 38.0 us, ks3 37 -> 37.5 us (m = 1184);

@@ -32,7 +32,8 @@ SETTINGS = [
     {"KMX_KARA_MIN": "300", "KMX_TC": "0"},  # Karatsuba over integer-pipe leaves, up to 4 levels
     {"KMX_WIDE": "1"},
     {"KMX_PACK_W1": "0"},       # block-per-job pack everywhere (no warp-per-job kernel)
-    {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one-word shape (single and paired jobs)          # wide-digit finish + multiword reconstruction for every unsigned shape
+    {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one-word shape (single and paired jobs)
+    {"KMX_PACK_SEG": "1"},      # segmented pack (2048-limb segments per CTA) for every shape          # wide-digit finish + multiword reconstruction for every unsigned shape
 ]
 
 
