@@ -5,11 +5,12 @@
 // (kmx_pack.cuh; pack.py:62-110): E + O 2^N, or |E - O 2^N| with the larger
 // stream first, from the unstaged coefficient vectors.
 //
-//   k_pseg_pre  one warp per (pair, op): the range check (pack.py:36-46), the
-//               top-down order of E and O 2^N for the negated packs, the sign
-//               word of the meta and a cleared bit length;
-//   k_pseg_a    one CTA per (pair, op, segment): the segment's digits with
-//               carry-in 0 (thread carry maps + one block scan) and its
+//   k_pseg_pre  one warp per (pair, op): the top-down order of E and O 2^N
+//               for the negated packs, the sign word of the meta, a cleared
+//               bit length, and the signed path's prefix sums;
+//   k_pseg_a    one CTA per (pair, op, segment): the range check of a slice
+//               of the coefficients (pack.py:36-46), the segment's digits
+//               with carry-in 0 (thread carry maps + one block scan) and its
 //               segment carry map;
 //   k_pseg_b    one CTA per (pair, op, segment): the segment's carry-in from
 //               the maps before it, rippled through the (rare) run of
@@ -57,23 +58,6 @@ __global__ void __launch_bounds__(128) k_pseg_pre(SegArgs sa, int nitems) {
   const int pair = item / A.nops, o = item - pair * A.nops;
   const PackOp& P = A.op[o];
   const PackCtx<false> C = seg_ctx(A, pair, o);
-  if (P.validate) {
-    bool bad = false;
-    for (int i = lane; i < C.L; i += 32) {
-      const u32* c = C.cf + (long long)i * C.iw;
-      if (A.bias) {
-        const int v = (int)c[0];
-        if (C.b < 32) bad |= (v < -(1 << (C.b - 1))) || (v >= (1 << (C.b - 1)));
-      } else {
-        for (int w = 0; w < C.iw; w++) {
-          const int lo_bit = 32 * w;
-          if (lo_bit >= C.b) bad |= c[w] != 0u;
-          else if (C.b - lo_bit < 32) bad |= (c[w] >> (C.b - lo_bit)) != 0u;
-        }
-      }
-    }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) raise_err(A.err, ERR_INVAL);
-  }
   if (P.prefix) {  // signed path: prefix sums of the lifted coefficients, natural order
     unsigned long long* out = P.prefix + (long long)pair * P.prefix_pair_stride;
     unsigned long long run = 0ull;
@@ -127,6 +111,24 @@ __global__ void __launch_bounds__(PS_T) k_pseg_a(SegArgs sa) {
   const int m = P.m;
   if (seg * PS_SEG >= m) return;  // shorter op: no such segment (uniform across the block)
   const PackCtx<false> C = seg_ctx(A, pair, o);
+  if (P.validate) {  // range check (pack.py:36-46): this segment's slice of the coefficient words
+    const int nseg_op = (m + PS_SEG - 1) / PS_SEG;
+    const long long nw = (long long)C.L * C.iw;
+    const long long w0 = nw * seg / nseg_op, w1 = nw * (seg + 1) / nseg_op;
+    bool bad = false;
+    for (long long x = w0 + threadIdx.x; x < w1; x += PS_T) {
+      const u32 raw = __ldg(C.cf + x);
+      if (A.bias) {
+        const int v = (int)raw;
+        if (C.b < 32) bad |= (v < -(1 << (C.b - 1))) || (v >= (1 << (C.b - 1)));
+      } else {
+        const int lo_bit = 32 * (int)(x % C.iw);
+        if (lo_bit >= C.b) bad |= raw != 0u;
+        else if (C.b - lo_bit < 32) bad |= (raw >> (C.b - lo_bit)) != 0u;
+      }
+    }
+    if (bad) raise_err(A.err, ERR_INVAL);
+  }
   const bool neg = P.kind & 1;
   const int order = sa.order[item];
   const int S = 2 * C.N;
