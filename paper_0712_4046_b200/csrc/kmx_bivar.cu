@@ -9,6 +9,7 @@
 //   k_brecover half-sums, exact halving and the chunk overlap recovery
 //              (_overlap_recover bipoly.py:151-174; _split_chunks :146-148)
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -64,6 +65,46 @@ __global__ void __launch_bounds__(256) k_beval(BivarPlan p, const int32_t* f, co
   if (bad) raise_err(err, ERR_INVAL);
 }
 
+// Staged form (grids up to 48 KB): one CTA per (pair, side) loads the grid
+// into shared memory with coalesced reads (the range check on the way) and
+// evaluates every point from there -- the chunk walk reads the grid column-
+// wise, which straight from global memory is one 4-byte access per line.
+__global__ void __launch_bounds__(256) k_beval_s(BivarPlan p, const int32_t* f, const int32_t* g, int32_t* ev,
+                                                 uint32_t* err) {
+  extern __shared__ int32_t bs_grid[];
+  const int lx = p.lx, ly = p.ly, Lu = p.Lu, sp = p.spacing;
+  const long long pair = blockIdx.x >> 1;
+  const int side = blockIdx.x & 1;
+  const int32_t* c = (side ? g : f) + pair * lx * ly;
+  const long long lim = 1LL << p.cbits;
+  bool bad = false;
+  for (int x = threadIdx.x; x < lx * ly; x += blockDim.x) {
+    const int32_t v = __ldg(c + x);
+    bad |= (long long)v >= lim || (long long)v <= -lim;
+    bs_grid[x] = v;
+  }
+  if (bad) raise_err(err, ERR_INVAL);
+  __syncthreads();
+  const long long nprod = (long long)p.batch * p.P;
+  for (int pt = 0; pt < p.P; pt++) {
+    int rev, alt;
+    point_flags(p.variant, pt, rev, alt);
+    int32_t* out = ev + ((long long)side * nprod + pair * p.P + pt) * Lu;
+    for (int t = threadIdx.x; t < Lu; t += blockDim.x) {
+      const int qlo = t - lx + 1 <= 0 ? 0 : (t - lx + 1 + sp - 1) / sp;
+      int qhi = t / sp;
+      if (qhi > ly - 1) qhi = ly - 1;
+      long long acc = 0;
+      for (int q = qlo; q <= qhi; q++) {
+        const int k = rev ? (ly - 1 - q) : q;
+        const long long v = bs_grid[(t - q * sp) * ly + k];
+        acc += (alt && (k & 1)) ? -v : v;
+      }
+      out[t] = (int32_t)acc;
+    }
+  }
+}
+
 // ------------------------------------------------------------ k_brecover
 // One CTA per pair.  prods: [pair][P][p_stride] int64 (2Lu-1 valid).
 // h: [pair][2lx-1][2ly-1] int64.
@@ -74,26 +115,52 @@ __device__ __forceinline__ long long halve(long long v, uint32_t* err) {
 
 // lanes t < min(sp, cl): sequential over chunks, chunk k -> output column
 // y = ybase + k*ystep.  fwd(x) / rev(x) fetch the recovered-sum vectors.
-template <class FF, class RF>
-__device__ void overlap_recover(int count, int sp, int cl, int ybase, int ystep, int lx2, int ly2,
-                                int64_t* H, FF fwd, RF rev) {
+// The per-row chains are independent: rows t are spread over the CTAs of
+// the pair (blockIdx.y) and threads; each chain prefetches KB steps of its
+// raw product words (loads only, no side effects, so they are all in flight
+// together) before the dependent recurrence consumes them.
+constexpr int BR_SPLIT = 4;  // CTAs per pair
+template <bool HALVE, class FF, class RF>
+__device__ void overlap_recover(int count, int sp, int cl, int ybase, int ystep, int ly2, int64_t* H, FF fwd,
+                                RF rev, bool& odd, int t0, int tstride) {
   const int low = min(sp, cl);
   const int ov = cl > sp ? cl - sp : 0;
-  for (int t = threadIdx.x; t < low; t += blockDim.x) {
+  constexpr int KB = 8;
+  for (int t = t0; t < low; t += tstride) {
     long long hi_prev = 0, lo_prev = 0;  // high_{k-1}[t], low_{k-1}[t]
-    for (int k = 0; k < count; k++) {
-      long long lo = fwd((long long)k * sp + t);
-      if (t < ov) lo -= hi_prev;
-      long long hi = 0;
-      if (t < ov) hi = rev((long long)(count - 1 - k) * sp + sp + t) - lo_prev;
-      const int y = ybase + k * ystep;
-      H[(long long)t * ly2 + y] = lo;
-      if (t < ov) H[(long long)(sp + t) * ly2 + y] = hi;
-      hi_prev = hi;
-      lo_prev = lo;
+    const bool o = t < ov;
+    for (int k0 = 0; k0 < count; k0 += KB) {
+      long long f[KB], r[KB];
+#pragma unroll
+      for (int i = 0; i < KB; i++) {
+        const int k = k0 + i;
+        f[i] = k < count ? fwd((long long)k * sp + t) : 0;
+        r[i] = (k < count && o) ? rev((long long)(count - 1 - k) * sp + sp + t) : 0;
+      }
+#pragma unroll
+      for (int i = 0; i < KB; i++) {
+        const int k = k0 + i;
+        if (k >= count) break;
+        long long fv = f[i], rv = r[i];
+        if (HALVE) {  // the ring's halving (bipoly.py:47-50), exact over Z
+          odd |= ((fv | rv) & 1) != 0;
+          fv >>= 1;
+          rv >>= 1;
+        }
+        long long lo = fv;
+        long long hi = 0;
+        if (o) {
+          lo -= hi_prev;
+          hi = rv - lo_prev;
+        }
+        const int y = ybase + k * ystep;
+        H[(long long)t * ly2 + y] = lo;
+        if (o) H[(long long)(sp + t) * ly2 + y] = hi;
+        hi_prev = hi;
+        lo_prev = lo;
+      }
     }
   }
-  (void)lx2;
 }
 
 __global__ void __launch_bounds__(128) k_brecover(BivarPlan p, const int64_t* prods, long long p_stride,
@@ -101,53 +168,85 @@ __global__ void __launch_bounds__(128) k_brecover(BivarPlan p, const int64_t* pr
   const int pair = blockIdx.x;
   // the KS products' error word leads the workspace (kmx_ws_status): fold the
   // evaluation's range check into it
-  if (err0 && err0 != err && pair == 0 && threadIdx.x == 0 && *err) atomicOr(err0, *err);
+  if (err0 && err0 != err && pair == 0 && blockIdx.y == 0 && threadIdx.x == 0 && *err) atomicOr(err0, *err);
   const int lx = p.lx, ly = p.ly;
   const int lx2 = 2 * lx - 1, ly2 = 2 * ly - 1;
   const int64_t* pr = prods + (long long)pair * p.P * p_stride;
   int64_t* H = h + (long long)pair * lx2 * ly2;
-  if (p.variant == 1) {  // bipoly.py:177-188: split at spacing 2lx-1
-    const int sp = 2 * lx - 1;
-    for (int id = threadIdx.x; id < lx2 * ly2; id += blockDim.x) {
-      const int i = id / ly2, j = id - i * ly2;
-      H[id] = pr[(long long)j * sp + i];
-    }
-  } else if (p.variant == 3) {  // bipoly.py:209-232
+  bool odd = false;
+  const int nthr = blockDim.x * gridDim.y;
+  const int tid = blockIdx.y * blockDim.x + threadIdx.x;
+  constexpr int U = 4;  // independent elements per thread in flight
+  if (p.variant == 1 || p.variant == 3) {
+    const int total = lx2 * ly2;
     const int64_t* pp = pr;
     const int64_t* pn = pr + p_stride;
-    for (int id = threadIdx.x; id < lx2 * ly2; id += blockDim.x) {
-      const int i = id / ly2, y = id - i * ly2;
-      const int j = y >> 1;
-      long long v;
-      if ((y & 1) == 0) {
-        const long long t = 2LL * lx * j + i;
-        v = halve(pp[t] + pn[t], err);
-      } else {
-        const long long t = 2LL * lx * j + i + lx;  // odd_vec = (...)[lx:]
-        v = halve(pp[t] - pn[t], err);
+    for (int base = tid; base < total; base += U * nthr) {
+      long long a[U], c[U];
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int id = base + u * nthr;
+        a[u] = 0;
+        c[u] = 0;
+        if (id >= total) continue;
+        const int i = id / ly2, y = id - i * ly2;
+        if (p.variant == 1) {  // bipoly.py:177-188: split at spacing 2lx-1
+          a[u] = __ldg(pr + (long long)y * (2 * lx - 1) + i);
+        } else {  // bipoly.py:209-232: even y from the half-sum, odd y from the half-difference
+          const int j = y >> 1;
+          const long long t = 2LL * lx * j + i + ((y & 1) ? lx : 0);  // odd_vec = (...)[lx:]
+          a[u] = __ldg(pp + t);
+          c[u] = __ldg(pn + t);
+        }
       }
-      H[id] = v;
+#pragma unroll
+      for (int u = 0; u < U; u++) {
+        const int id = base + u * nthr;
+        if (id >= total) continue;
+        long long v = a[u];
+        if (p.variant == 3) {
+          const int y = id % ly2;
+          v = (y & 1) ? a[u] - c[u] : a[u] + c[u];
+          odd |= (v & 1) != 0;
+          v >>= 1;
+        }
+        H[id] = v;
+      }
     }
   } else if (p.variant == 2) {  // bipoly.py:191-206
     const int64_t* pf = pr;
     const int64_t* pv = pr + p_stride;
-    overlap_recover(2 * ly - 1, lx, 2 * lx - 1, 0, 1, lx2, ly2, H,
-                    [&](long long x) { return (long long)pf[x]; },
-                    [&](long long x) { return (long long)pv[x]; });
+    overlap_recover<false>(2 * ly - 1, lx, 2 * lx - 1, 0, 1, ly2, H,
+                           [&](long long x) { return (long long)__ldg(pf + x); },
+                           [&](long long x) { return (long long)__ldg(pv + x); }, odd, tid, nthr);
   } else {  // bipoly.py:235-278
     const int n = p.n4;
     const int64_t* pp = pr;
     const int64_t* pn = pr + p_stride;
     const int64_t* rp = pr + 2 * p_stride;
     const int64_t* rn = pr + 3 * p_stride;
-    overlap_recover(ly, 2 * n, 2 * lx - 1, 0, 2, lx2, ly2, H,
-                    [&](long long x) { return halve(pp[x] + pn[x], err); },
-                    [&](long long x) { return halve(rp[x] + rn[x], err); });
-    if (ly > 1)
-      overlap_recover(ly - 1, 2 * n, 2 * lx - 1, 1, 2, lx2, ly2, H,
-                      [&](long long x) { return halve(pp[x + n] - pn[x + n], err); },
-                      [&](long long x) { return halve(rp[x + n] - rn[x + n], err); });
+    // the even and odd recoveries are independent: half the pair's CTAs each
+    const int half = gridDim.y / 2 ? gridDim.y / 2 : 1;
+    const int side = gridDim.y >= 2 ? (int)blockIdx.y / half : -1;  // -1: one CTA does both
+    const int ht0 = (gridDim.y >= 2 ? (int)blockIdx.y % half : 0) * blockDim.x + threadIdx.x;
+    const int hstride = half * blockDim.x;
+    if (side != 1)
+      overlap_recover<true>(ly, 2 * n, 2 * lx - 1, 0, 2, ly2, H,
+                            [&](long long x) { return (long long)__ldg(pp + x) + __ldg(pn + x); },
+                            [&](long long x) { return (long long)__ldg(rp + x) + __ldg(rn + x); }, odd, ht0,
+                            hstride);
+    if (ly > 1 && side != 0)
+      overlap_recover<true>(ly - 1, 2 * n, 2 * lx - 1, 1, 2, ly2, H,
+                            [&](long long x) { return (long long)__ldg(pp + x + n) - __ldg(pn + x + n); },
+                            [&](long long x) { return (long long)__ldg(rp + x + n) - __ldg(rn + x + n); }, odd,
+                            ht0, hstride);
   }
+  if (odd) raise_err(err, ERR_INEXACT);  // inexact halving (bipoly.py:47-50)
+}
+
+static int getenv_b(const char* n, int d) {
+  const char* v = getenv(n);
+  return v && *v ? atoi(v) : d;
 }
 
 cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g, int64_t* h, int32_t* evals,
@@ -160,7 +259,11 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   int grid = (int)std::min<long long>((ne + 255) / 256, 148LL * 32);
   if (grid < 1) grid = 1;
   prof_mark(0, true, st);
-  k_beval<<<grid, 256, 0, st>>>(p, f, g, evals, err);
+  const size_t gsm = (size_t)p.lx * p.ly * 4;
+  if (gsm <= 48 * 1024 && getenv_b("KMX_BEVAL_STAGED", 1))
+    k_beval_s<<<2 * p.batch, 256, gsm, st>>>(p, f, g, evals, err);
+  else
+    k_beval<<<grid, 256, 0, st>>>(p, f, g, evals, err);
   prof_mark(0, false, st);
   (*nlaunch)++;
   cudaError_t e = cudaGetLastError();
@@ -198,7 +301,7 @@ cudaError_t launch_bivar(const BivarPlan& p, const int32_t* f, const int32_t* g,
   }
   prof_mark(1, false, st);
   prof_mark(2, true, st);
-  k_brecover<<<p.batch, 128, 0, st>>>(p, prods, ps, h, err, err0);
+  k_brecover<<<dim3(p.batch, BR_SPLIT), 128, 0, st>>>(p, prods, ps, h, err, err0);
   prof_mark(2, false, st);
   (*nlaunch)++;
   return cudaGetLastError();

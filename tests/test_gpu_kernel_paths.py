@@ -30,10 +30,10 @@ SETTINGS = [
     {"KMX_RECON_MINB": "6", "KMX_RECON_V": "4"},  # recon: 6-CTA register cap; 4 steps per thread
     {"KMX_KARA_MIN": "600"},    # Karatsuba levels on every product above 600 limbs (tensor-core leaves)
     {"KMX_KARA_MIN": "300", "KMX_TC": "0"},  # Karatsuba over integer-pipe leaves, up to 4 levels
-    {"KMX_WIDE": "1"},
+    {"KMX_WIDE": "1"},          # wide-digit finish + multiword reconstruction for every unsigned shape
     {"KMX_PACK_W1": "0"},       # block-per-job pack everywhere (no warp-per-job kernel)
     {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one-word shape (single and paired jobs)
-    {"KMX_PACK_SEG": "1"},      # segmented pack (2048-limb segments per CTA) for every shape          # wide-digit finish + multiword reconstruction for every unsigned shape
+    {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},  # segmented pack everywhere; bivariate: IMAD univariate products, unstaged evaluation
 ]
 
 

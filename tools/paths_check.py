@@ -62,6 +62,25 @@ def main():
             if [got[0], got[B - 1]] != want:
                 print("FAIL shape", (B, lf, lg, b, signed), v)
                 bad += 1
+    # bivariate over Z: the reference's golden grids and a c3-shaped batch
+    # (64 x 64 u16, where the univariate products take the KS path)
+    Z = kmx.ring_z()
+    fns = (kmx.bks_standard, kmx.bks_reciprocal, kmx.bks_negated, kmx.bks_four)
+    for tag, f, g, h in G.bivar_cases():
+        for v, fn in enumerate(fns, 1):
+            if [list(r) for r in fn(kmx.BiPoly(tuple(map(tuple, f))), kmx.BiPoly(tuple(map(tuple, g))), Z).coeffs] != h:
+                print("FAIL bivar golden", tag, v)
+                bad += 1
+    nrng = np.random.default_rng(33)
+    F = nrng.integers(0, 1 << 16, size=(4, 64, 64), dtype=np.int64).astype(np.int32)
+    Gg = nrng.integers(0, 1 << 16, size=(4, 64, 64), dtype=np.int64).astype(np.int32)
+    for v in (1, 2, 3, 4):
+        bb = kmx.BksBatch(v, 4, 64, 64, 16)
+        hb = bb(torch.from_numpy(F).cuda(), torch.from_numpy(Gg).cuda())
+        bb.status()
+        if hb.cpu().tolist()[3] != O.bks(v, F[3].tolist(), Gg[3].tolist()):
+            print("FAIL bivar c3 shape", v)
+            bad += 1
     print("paths_check", {k: os.environ.get(k) for k in os.environ if k.startswith("KMX_")}, "failures", bad)
     sys.exit(1 if bad else 0)
 
