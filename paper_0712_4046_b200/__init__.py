@@ -14,6 +14,9 @@ from .modpoly import (DEFAULT_THRESHOLDS, GPU_THRESHOLDS, AutoThresholds, ModMul
                       choose_variant, mod_mul, mod_mul_host)
 from .ksint import (derive_params, ks1_mul, ks2_mul, ks3_mul, ks4_mul, reconstruct_overlapped)
 from .kstypes import (DEFAULT_MUL_CONFIG, CoeffVec, KsParams, MulConfig, MulStats, OverlapDigits)
+# kronmul.pack's evaluation functions (pack.py:79-110), computed by K1; as in
+# the reference, the package attribute `pack` is the function
+from .pack import pack, pack_batch, pack_negated, pack_negated_reversed, pack_reversed  # noqa: E402
 
 __version__ = "0.1.0"
 
@@ -25,4 +28,5 @@ __all__ = [
     "ks_mul_host", "bks_mul_host", "imad_peak", "tc_peak", "mul_engine", "__version__",
     "ModPoly", "Variant", "AutoThresholds", "DEFAULT_THRESHOLDS", "GPU_THRESHOLDS", "choose_variant",
     "mod_mul", "ModMulBatch", "mod_mul_host",
+    "pack", "pack_reversed", "pack_negated", "pack_negated_reversed", "pack_batch",
 ]

@@ -21,8 +21,8 @@ pytestmark = pytest.mark.gpu
 def kpack():
     if not torch.cuda.is_available():
         pytest.skip("needs a CUDA device")
-    from paper_0712_4046_b200 import pack as P
-    return P
+    import importlib
+    return importlib.import_module("paper_0712_4046_b200.pack")
 
 
 def test_pack_golden(kpack):
