@@ -432,12 +432,17 @@ __global__ void __launch_bounds__(32 * RECON_WARPS) k_recon(ReconArgs a) {
         u64 v0, v1;
         if (W >= 64) { v0 = lo_cur; v1 = h; }
         else { v0 = lo_cur | (h << W); v1 = h >> (64 - W); }
-        u32* dst = H + (long long)(S.pos0 + (long long)j * S.pstride) * ow;
-        dst[0] = (u32)v0;
-        if (ow > 1) dst[1] = (u32)(v0 >> 32);
-        if (ow > 2) dst[2] = (u32)v1;
-        if (ow > 3) dst[3] = (u32)(v1 >> 32);
-        for (int w = 4; w < ow; w++) dst[w] = 0u;
+        const long long kpos = S.pos0 + (long long)j * S.pstride;
+        u32* dst = H + kpos * ow;
+        if (a.bias.enabled) {
+          store_coeff128(dst, ow, (unsigned __int128)v0 | ((unsigned __int128)v1 << 64), kpos, a.bias, pair);
+        } else {
+          dst[0] = (u32)v0;
+          if (ow > 1) dst[1] = (u32)(v0 >> 32);
+          if (ow > 2) dst[2] = (u32)v1;
+          if (ow > 3) dst[3] = (u32)(v1 >> 32);
+          for (int w = 4; w < ow; w++) dst[w] = 0u;
+        }
         const int sdir = (int)fc - (int)eps;
         const u64 nxt = sdir == 0 ? d : (sdir > 0 ? dm1 : dp1);
         const u32 fcn = sdir == 0 ? b0 : (sdir > 0 ? bp1 : bm1);
@@ -458,12 +463,17 @@ __global__ void __launch_bounds__(32 * RECON_WARPS) k_recon(ReconArgs a) {
     u64 v0, v1;
     if (W >= 64) { v0 = lo_cur; v1 = h; }
     else { v0 = lo_cur | (h << W); v1 = h >> (64 - W); }
-    u32* dst = H + (long long)(S.pos0 + (long long)(count - 1) * S.pstride) * ow;
-    dst[0] = (u32)v0;
-    if (ow > 1) dst[1] = (u32)(v0 >> 32);
-    if (ow > 2) dst[2] = (u32)v1;
-    if (ow > 3) dst[3] = (u32)(v1 >> 32);
-    for (int w = 4; w < ow; w++) dst[w] = 0u;
+    const long long kpos = S.pos0 + (long long)(count - 1) * S.pstride;
+    u32* dst = H + kpos * ow;
+    if (a.bias.enabled) {
+      store_coeff128(dst, ow, (unsigned __int128)v0 | ((unsigned __int128)v1 << 64), kpos, a.bias, pair);
+    } else {
+      dst[0] = (u32)v0;
+      if (ow > 1) dst[1] = (u32)(v0 >> 32);
+      if (ow > 2) dst[2] = (u32)v1;
+      if (ow > 3) dst[3] = (u32)(v1 >> 32);
+      for (int w = 4; w < ow; w++) dst[w] = 0u;
+    }
   } else {
     // ---------------- multiword digits
     const int topbits = W - 32 * (NW - 1);
@@ -1327,7 +1337,10 @@ cudaError_t launch_recon_par(const ReconArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_recon(const ReconArgs& a0, cudaStream_t st) {
-  if (!a0.carries && !a0.sequential) return launch_recon_par(a0, st);
+  static const int seq = getenv("KMX_RECON_SEQ") ? atoi(getenv("KMX_RECON_SEQ")) : 0;
+  // the one-thread-per-stream kernel handles the signed correction only for
+  // digits of at most 64 bits (its multiword branch stores unsigned)
+  if (!a0.carries && !a0.sequential && !(seq && a0.dwords <= 2)) return launch_recon_par(a0, st);
   ReconArgs a = a0;
   a.rch = a.dwords >= 32 ? 1 : 32 / a.dwords;  // ~32 words per stream per array per chunk
   switch (a.dwords) {
