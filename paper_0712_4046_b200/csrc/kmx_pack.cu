@@ -71,7 +71,15 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   static const int fast = getenv("KMX_PACK_FAST") ? atoi(getenv("KMX_PACK_FAST")) : 1;
   b.fast1 = fast;
   const int nw = (lmax + PK_PAD) * a.in_words;
-  b.stage = nw <= PK_STAGE_WORDS;
+  // The carry-free pack (no negated op, N >= b) stages vectors up to 80 KB of
+  // opt-in shared memory (unstaged windows cost two global loads each):
+  // config 5 n=4096 b=128 ks1 / ks2 pack 158 / 107 -> 76 / 89 us, n=8192 b=64
+  // ks2 84 -> 50 us.  Larger stages (1 CTA per SM) and the carry paths (ks3 /
+  // ks4: 125 -> 151 us at n=4096 b=128) measured slower: they keep 48 KB.
+  bool carry_free = a.N >= a.b;
+  for (int i = 0; i < a.nops; i++) carry_free &= (a.op[i].kind & 1) == 0;
+  static const int big = getenv("KMX_PACK_STAGE_WORDS") ? atoi(getenv("KMX_PACK_STAGE_WORDS")) : 20480;
+  b.stage = nw <= (carry_free ? big : PK_STAGE_WORDS);
   const size_t smem = b.stage ? (size_t)nw * sizeof(u32) : 0;
   // paired packs halve the block count: only when that still fills the chip
   // (c1, 64 pairs: 256 paired blocks are slower than 512 single ones)
