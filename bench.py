@@ -368,13 +368,26 @@ def measure_variant(g, cfg, cfg_name, v, fd, gd, steps, warmup, graphs=True, mon
         conv_ms = kern[1]
         macs = algorithmic_products(cfg, v) * B
         ach = macs / (conv_ms * 1e-3) if conv_ms > 0 else None
-        rec["roofline"] = {"bound": "imad", "kernel": "k_conv (int32 x int32 -> int64 IMAD.WIDE convolution)",
-                           "achieved": ach / 1e9 if ach else None, "peak": g.imad / 1e9, "unit": "G MAC/s",
-                           "frac": ach / g.imad if ach else None,
-                           "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
-                           "algorithmic_work": f"{macs} coefficient MACs per launch "
-                                               f"({algorithmic_products(cfg, v)} per pair x {B})",
-                           "traffic": g.traffic(cfg_name, v, "conv_dram_bytes")}
+        uni = int(g.L.kmx_bks_uni_engine(v, cfg["lx"], cfg["ly"], cfg["b"]))
+        if uni > 0:
+            # univariate products on the integer KS path (pack -> tcgen05 multiply
+            # -> finish [-> reconstruct]); its MAC rate beside the integer pipe's peak
+            rec["roofline"] = {"bound": "tensor", "kernel": f"univariate products through the integer KS path "
+                                                            f"(ks{uni}: pack, k_tcmul, finish, reconstruct)",
+                               "achieved": ach / 1e9 if ach else None, "unit": "G coefficient-MAC/s",
+                               "frac": None, "frac_of_imad_peak": ach / g.imad if ach else None,
+                               "peak_source": "work-equivalent: the IMAD.WIDE convolution would be bound by "
+                                              "kmx_imad_peak(); the KS path runs on the tensor cores",
+                               "algorithmic_work": f"{macs} coefficient MACs per launch "
+                                                   f"({algorithmic_products(cfg, v)} per pair x {B})"}
+        else:
+            rec["roofline"] = {"bound": "imad", "kernel": "k_conv (int32 x int32 -> int64 IMAD.WIDE convolution)",
+                               "achieved": ach / 1e9 if ach else None, "peak": g.imad / 1e9, "unit": "G MAC/s",
+                               "frac": ach / g.imad if ach else None,
+                               "peak_source": "kmx_imad_peak() microbenchmark measured live in this process",
+                               "algorithmic_work": f"{macs} coefficient MACs per launch "
+                                                   f"({algorithmic_products(cfg, v)} per pair x {B})",
+                               "traffic": g.traffic(cfg_name, v, "conv_dram_bytes")}
     else:
         km = {nm: kern[i] for i, nm in enumerate(KS_SLOTS) if kern[i] > 0}
         if "recon" in km and "finish" not in km:  # K3 + K4 fused (k_finrec)

@@ -153,6 +153,10 @@ size_t kmx_bks_workspace_bytes(int variant, int batch, int lx, int ly);
  * engine; kmx_bks_workspace_bytes() sizes the k_conv engine, which
  * kmx_bks_mul falls back to when the workspace is smaller. */
 size_t kmx_bks_workspace_bytes_cb(int variant, int batch, int lx, int ly, int coeff_bits);
+/* Engine of the univariate products for this shape: 0 = the int32 x int32 ->
+ * int64 IMAD convolution (k_conv), 1..4 = the integer KS path with that
+ * variant (tensor cores). */
+int kmx_bks_uni_engine(int variant, int lx, int ly, int coeff_bits);
 int kmx_bks_mul(int variant, int batch, int lx, int ly, int coeff_bits,
                 const int32_t* f, const int32_t* g, int64_t* h,
                 void* workspace, size_t ws_bytes, void* stream);

@@ -63,6 +63,7 @@ _SIGS = {
     "kmx_reconstruct_host": (_i, [_i, _i, _i, _vp, _vp, _i, _vp, _i, _vp]),
     "kmx_bks_workspace_bytes": (_sz, [_i, _i, _i, _i]),
     "kmx_bks_workspace_bytes_cb": (_sz, [_i, _i, _i, _i, _i]),
+    "kmx_bks_uni_engine": (_i, [_i, _i, _i, _i]),
     "kmx_bks_mul": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp, _vp, _sz, _vp]),
     "kmx_bks_mul_host": (_i, [_i, _i, _i, _i, _i, _vp, _vp, _vp]),
     "kmx_bks_wide_out_words": (_i, [_i, _i, _i]),

@@ -393,6 +393,12 @@ size_t kmx_bks_workspace_bytes(int variant, int batch, int lx, int ly) {
   return bks_layout(p).total;
 }
 
+int kmx_bks_uni_engine(int variant, int lx, int ly, int coeff_bits) {
+  BivarPlan p;
+  int rc = bks_plan(p, variant, 1, lx, ly, coeff_bits);
+  return rc ? rc : p.uni;
+}
+
 size_t kmx_bks_workspace_bytes_cb(int variant, int batch, int lx, int ly, int coeff_bits) {
   BivarPlan p;
   if (bks_plan(p, variant, batch, lx, ly, coeff_bits)) return 0;
