@@ -1192,7 +1192,7 @@ int kmx_mul_engine(int variant, int len_f, int len_g, int coeff_bits, unsigned f
   // Karatsuba levels: the engine of the leaves (the split halves)
   int ma = p.mf, mb = p.mg;
   while (!mul_engine_takes(ma, mb)) {
-    const int mx = ma > mb ? ma : mb, h = (mx + 1) / 2;
+    const int mx = ma > mb ? ma : mb, h = (((mx + 1) / 2) + 3) & ~3;  // kmx_kara.cu node()
     if ((ma < mb ? ma : mb) > h) ma = mb = h + 1;
     else if (ma >= mb) ma = h;
     else mb = h;

@@ -222,7 +222,7 @@ Node node(int ma, int mb, int depth) {
   n.ma = ma;
   n.mb = mb;
   const int mx = std::max(ma, mb), mn = std::min(ma, mb);
-  n.h = (mx + 1) / 2;
+  n.h = (((mx + 1) / 2) + 3) & ~3;  // a multiple of 4 limbs: the a1 / b1 views stay 16-byte aligned (bulk staging)
   n.balanced = mn > n.h;
   const bool engine_ok = mul_engine_takes(ma, mb);
   n.leaf = depth >= KARA_MAX_DEPTH || mn < 64 || (engine_ok && mx < kara_min_limbs());

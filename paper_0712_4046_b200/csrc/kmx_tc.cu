@@ -108,6 +108,7 @@ struct TcShared {
   unsigned long long bar_full[TC_MAXNB];   // B stage built (3 builder warps arrive)
   unsigned long long bar_empty[TC_MAXNB];  // MMAs that read the stage completed (commit)
   unsigned long long bar_done;             // all MMAs of the CTA completed
+  unsigned long long bar_stage;            // bulk copies of the operands landed (TMA, complete_tx)
   unsigned long long s_cout[TC_EPI / 32];
   unsigned long long carry;                // carry into the next tile
   uint32_t tmem_base;
@@ -124,6 +125,7 @@ struct TcArgs {
   int fuse;     // pack the operands in the prologue (pk, P)
   int P;        // products per pair
   size_t ring;  // bytes of the B ring (>= the pack staging area when fused)
+  int bulk;     // stage aligned operands with bulk async copies (KMX_TC_BULK, default 1)
   PackArgs pk;
 };
 
@@ -206,6 +208,7 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
       mbar_init(smem_u32(&sh.bar_empty[i]), 1);
     }
     mbar_init(smem_u32(&sh.bar_done), 1);
+    mbar_init(smem_u32(&sh.bar_stage), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     sh.carry = 0ull;
   }
@@ -230,8 +233,48 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
     pack_op<true>(ta.pk, pair, oa, stage, aw + AP, rg == 0);
     pack_op<true>(ta.pk, pair, ob, stage, bw + BP, rg == 0);
     __syncthreads();  // the ring is free again before the builders use it
+  } else if (ta.bulk && (reinterpret_cast<uintptr_t>(Ag) & 15) == 0 && (reinterpret_cast<uintptr_t>(Bg) & 15) == 0 &&
+             ((sw ? a.b_stride : a.a_stride) & 3) == 0 && ((sw ? a.a_stride : a.b_stride) & 3) == 0 &&
+             (sw ? a.b_stride : a.a_stride) >= ((mA + 3) & ~3) && (sw ? a.a_stride : a.b_stride) >= ((mB + 3) & ~3)) {
+    // Operands staged by two bulk async copies (TMA engine, cp.async.bulk
+    // completing on an mbarrier): all bytes in flight at once with no register
+    // round trip, while the threads zero the padding around them.  The copies
+    // are rounded up to 16 bytes (the operand rows are padded to 4 limbs);
+    // the rounding limbs are zeroed once they have landed.
+    const int La16 = (d.La + 15) & ~15, Lb16 = (d.Lb + 15) & ~15;
+    if (tid == 0) {
+      const uint32_t bar = smem_u32(&sh.bar_stage);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)(La16 + Lb16))
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(apad + G::APAD)),
+                   "l"(Ag), "r"((uint32_t)La16), "r"(bar)
+                   : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                       smem_u32(bpad + TcB<H>::BPAD)),
+                   "l"(Bg), "r"((uint32_t)Lb16), "r"(bar)
+                   : "memory");
+    }
+    uint4* aw = reinterpret_cast<uint4*>(apad);
+    uint4* bq = reinterpret_cast<uint4*>(bpad);
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    constexpr int AQ = G::APAD / 16, BQ = TcB<H>::BPAD / 16;
+    // padding outside the copies' byte ranges (no two writers on one byte)
+    for (int w = tid; w < AQ; w += TC_THREADS) aw[w] = z4;
+    for (int w = AQ + La16 / 16 + tid; w < 2 * AQ + d.La / 16; w += TC_THREADS) aw[w] = z4;
+    for (int w = tid; w < BQ; w += TC_THREADS) bq[w] = z4;
+    for (int w = BQ + Lb16 / 16 + tid; w < 2 * BQ + d.Lb / 16; w += TC_THREADS) bq[w] = z4;
+    __syncthreads();  // the barrier's init (thread 0) precedes every wait
+    mbar_wait(smem_u32(&sh.bar_stage), 0);
+    // the rounding limbs past the operands (row padding, not operand data)
+    uint32_t* a32 = reinterpret_cast<uint32_t*>(apad + G::APAD);
+    uint32_t* b32 = reinterpret_cast<uint32_t*>(bpad + TcB<H>::BPAD);
+    if (tid < (La16 - d.La) / 4) a32[mA + tid] = 0u;
+    if (tid < (Lb16 - d.Lb) / 4) b32[mB + tid] = 0u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   } else {
     // A: zero-padded copy of the longer operand; b: zero-padded copy of the shorter
+    // (unaligned views, e.g. Karatsuba halves: 16-byte loads where possible)
     uint4* aw = reinterpret_cast<uint4*>(apad);
     const int nq = (d.La + 2 * G::APAD) / 16;
     const int qa = G::APAD / 16;
@@ -817,6 +860,7 @@ cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, cons
             a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.nseg, p.smem, p.cost);
   TcArgs ta;
   ta.m = a;
+  ta.bulk = env_int_tc("KMX_TC_BULK", 1);
   ta.KC = p.KC;
   ta.NB = p.NB;
   ta.fuse = pk != nullptr;
