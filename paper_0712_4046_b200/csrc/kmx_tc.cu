@@ -756,7 +756,20 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
     }
   std::vector<TcPlan> out;
   for (const TcPlan& p : v)
-    if (p.cost <= 1.6 * best) out.push_back(p);
+    if (p.cost <= 1.6 * best) {
+      out.push_back(p);
+      // fewer tiles per CTA (more, shorter CTAs): a better last wave on long
+      // products whose CTAs fill an SM each
+      for (int tpc : {p.TPC / 2, (p.TPC * 2) / 3}) {
+        if (tpc < 1 || tpc >= p.TPC) continue;
+        TcPlan q = p;
+        q.TPC = tpc;
+        q.nranges = (p.ntiles + tpc - 1) / tpc;
+        bool dup = false;
+        for (const TcPlan& r : out) dup |= r.H == q.H && r.KC == q.KC && r.NW == q.NW && r.TPC == q.TPC;
+        if (!dup) out.push_back(q);
+      }
+    }
   return out;
 }
 
