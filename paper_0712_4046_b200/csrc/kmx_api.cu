@@ -537,6 +537,12 @@ struct HostCtx {
   size_t cap[4] = {0, 0, 0, 0};
   HostLane lane[HOST_LANES];
   uint32_t* flags = nullptr;        // pinned, one error word per chunk
+  // copy-engine pipeline (ks_mul_host_streams): one H2D stream, two compute
+  // streams, one D2H stream; whole-batch device buffers
+  cudaStream_t s_in = nullptr, s_out = nullptr, s_comp[2] = {nullptr, nullptr};
+  cudaEvent_t ev_in[HOST_MAX_CHUNKS] = {}, ev_done[HOST_MAX_CHUNKS] = {};
+  void* pbuf[4] = {nullptr, nullptr, nullptr, nullptr};  // f+g, h, ws0, ws1
+  size_t pcap[4] = {0, 0, 0, 0};
 };
 
 int ensure_buf(void** buf, size_t* cap, size_t bytes) {
@@ -616,6 +622,73 @@ int ks_mul_host_pipelined(const KsPlan& pfull, HostCtx* c, const uint32_t* f, co
   }
   for (int l = 0; l < HOST_LANES && l < nchunks; l++)
     if (cudaStreamSynchronize(c->lane[l].st) != cudaSuccess) return KMX_ECUDA;
+  g_launches = nl;
+  uint32_t fl = 0;
+  for (int i = 0; i < nchunks; i++) fl |= c->flags[i];
+  return status_from_flag(fl);
+}
+
+// Copy-engine pipeline: every chunk's host->device copy is queued on one
+// stream (back to back at full link speed), its kernels on one of two compute
+// streams (waiting on that copy's event; the two streams overlap one chunk's
+// latency-bound stages with the next one's), and its device->host copy on a
+// fourth stream (waiting on the kernels' event), so the device->host direction
+// -- 3x the bytes of the other at c2 -- streams continuously once the first
+// chunk is done.  KMX_HOST_PIPE=0 selects the lane pipeline above.
+int ks_mul_host_streams(const KsPlan& pfull, HostCtx* c, const uint32_t* f, const uint32_t* g, uint32_t* h,
+                        int out_words, int nchunks) {
+  const int batch = pfull.batch;
+  const int cb = (batch + nchunks - 1) / nchunks;
+  nchunks = (batch + cb - 1) / cb;
+  KsPlan pc, pt;
+  int rc = make_plan(pc, pfull.req_variant, cb, pfull.lf, pfull.lg, pfull.b, pfull.in_words, pfull.flags);
+  if (rc) return rc;
+  const int tail = batch - (nchunks - 1) * cb;
+  rc = make_plan(pt, pfull.req_variant, tail, pfull.lf, pfull.lg, pfull.b, pfull.in_words, pfull.flags);
+  if (rc) return rc;
+  const size_t fpp = (size_t)pfull.lf * pfull.in_words, gpp = (size_t)pfull.lg * pfull.in_words;
+  const size_t hpp = (size_t)pfull.out_len * out_words;
+  const size_t fb = (size_t)batch * fpp * 4, gb = (size_t)batch * gpp * 4, hb = (size_t)batch * hpp * 4;
+  if (!c->flags && cudaMallocHost(&c->flags, HOST_MAX_CHUNKS * sizeof(uint32_t)) != cudaSuccess) return KMX_ENOMEM;
+  auto mk = [](cudaStream_t* s) { return *s || cudaStreamCreateWithFlags(s, cudaStreamNonBlocking) == cudaSuccess; };
+  if (!mk(&c->s_in) || !mk(&c->s_out) || !mk(&c->s_comp[0]) || !mk(&c->s_comp[1])) return KMX_ECUDA;
+  for (int i = 0; i < nchunks; i++) {
+    if (!c->ev_in[i] && cudaEventCreateWithFlags(&c->ev_in[i], cudaEventDisableTiming) != cudaSuccess) return KMX_ECUDA;
+    if (!c->ev_done[i] && cudaEventCreateWithFlags(&c->ev_done[i], cudaEventDisableTiming) != cudaSuccess)
+      return KMX_ECUDA;
+  }
+  if ((rc = ensure_buf(&c->pbuf[0], &c->pcap[0], align256(fb) + gb + 256))) return rc;
+  if ((rc = ensure_buf(&c->pbuf[1], &c->pcap[1], hb))) return rc;
+  if ((rc = ensure_buf(&c->pbuf[2], &c->pcap[2], pc.total))) return rc;
+  if ((rc = ensure_buf(&c->pbuf[3], &c->pcap[3], pc.total))) return rc;
+  uint32_t* df = (uint32_t*)c->pbuf[0];
+  uint32_t* dg = (uint32_t*)((char*)c->pbuf[0] + align256(fb));
+  uint32_t* dh = (uint32_t*)c->pbuf[1];
+  int nl = 0;
+  for (int i = 0; i < nchunks; i++) {
+    const KsPlan& pp = (i == nchunks - 1) ? pt : pc;
+    const size_t o = (size_t)i * cb;
+    const int bi = pp.batch;
+    if (cudaMemcpyAsync(df + o * fpp, f + o * fpp, (size_t)bi * fpp * 4, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
+        cudaMemcpyAsync(dg + o * gpp, g + o * gpp, (size_t)bi * gpp * 4, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
+        cudaEventRecord(c->ev_in[i], c->s_in) != cudaSuccess)
+      return KMX_ECUDA;
+    cudaStream_t sc = c->s_comp[i & 1];
+    if (cudaStreamWaitEvent(sc, c->ev_in[i], 0) != cudaSuccess) return KMX_ECUDA;
+    void* ws = c->pbuf[2 + (i & 1)];
+    rc = run_plan(pp, df + o * fpp, dg + o * gpp, dh + o * hpp, out_words, ws, c->pcap[2 + (i & 1)], sc);
+    if (rc) return rc;
+    nl += g_launches;
+    if (cudaMemcpyAsync(c->flags + i, ws, 4, cudaMemcpyDeviceToHost, sc) != cudaSuccess ||
+        cudaEventRecord(c->ev_done[i], sc) != cudaSuccess)
+      return KMX_ECUDA;
+    if (cudaStreamWaitEvent(c->s_out, c->ev_done[i], 0) != cudaSuccess ||
+        cudaMemcpyAsync(h + o * hpp, dh + o * hpp, (size_t)bi * hpp * 4, cudaMemcpyDeviceToHost, c->s_out) != cudaSuccess)
+      return KMX_ECUDA;
+  }
+  if (cudaStreamSynchronize(c->s_out) != cudaSuccess || cudaStreamSynchronize(c->s_comp[0]) != cudaSuccess ||
+      cudaStreamSynchronize(c->s_comp[1]) != cudaSuccess)
+    return KMX_ECUDA;
   g_launches = nl;
   uint32_t fl = 0;
   for (int i = 0; i < nchunks; i++) fl |= c->flags[i];
@@ -936,7 +1009,10 @@ int kmx_ks_mul_host(int variant, int batch, int len_f, int len_g, int coeff_bits
     size_t nch = hb / ((size_t)(chunk_mb > 0 ? chunk_mb : 2) << 20);
     if (nch > (size_t)HOST_MAX_CHUNKS) nch = HOST_MAX_CHUNKS;
     if (nch > (size_t)batch) nch = batch;
-    if (nch >= 2) return ks_mul_host_pipelined(p, c, f, g, h, out_words, (int)nch);
+    static const int pipe = getenv("KMX_HOST_PIPE") ? atoi(getenv("KMX_HOST_PIPE")) : 1;
+    if (nch >= 2)
+      return pipe ? ks_mul_host_streams(p, c, f, g, h, out_words, (int)nch)
+                  : ks_mul_host_pipelined(p, c, f, g, h, out_words, (int)nch);
   }
   if (!c->st && cudaStreamCreateWithFlags(&c->st, cudaStreamNonBlocking) != cudaSuccess) return KMX_ECUDA;
   if ((rc = ensure(*c, 0, fb + gb + 256))) return rc;
