@@ -1,5 +1,5 @@
-// kmx_pack1.cu -- K1 for one-word coefficients (b <= 32, in_words == 1) at a
-// parity spacing 2N >= 32: one WARP per pack job, no block barriers.
+// kmx_pack1.cu -- K1 for one- and two-word coefficients (b <= 64, in_words <= 2)
+// at a parity spacing 2N >= 32: one WARP per pack job, no block barriers.
 //
 // Same values as pack_op / pack_pair (kmx_pack.cuh; pack.py:62-110): the
 // value at +2^N, -2^N (and the reversed forms) of a coefficient vector, as
@@ -45,11 +45,22 @@ struct Cur1 {
     t += 32;
     if (t >= S) { t -= S; m++; }
   }
-  // 32 bits of the stream at the current window (S >= 32, b <= S)
+  // 32 bits of the stream at the current window (S >= 32, b <= S), for
+  // coefficients of IW words (staged with one zero word of slack per vector)
+  template <int IW>
   __device__ __forceinline__ u32 bits(const u32* sc, int par, int S, int b) const {
-    u32 v = (m >= 0 && t < b) ? (sc[2 * m + par] >> t) : 0u;
+    u32 v = 0u;
+    if (m >= 0 && t < b) {
+      if (IW == 1) {
+        v = sc[2 * m + par] >> t;
+      } else {
+        const u32* c = sc + (2 * m + par) * IW + (t >> 5);
+        const u32 hi = (t >> 5) + 1 < IW ? c[1] : 0u;
+        v = __funnelshift_r(c[0], hi, t & 31);
+      }
+    }
     const int sh = S - t;
-    if (sh < 32) v |= sc[2 * (m + 1) + par] << sh;
+    if (sh < 32) v |= sc[(2 * (m + 1) + par) * IW] << sh;
     return v;
   }
 };
@@ -67,10 +78,11 @@ struct StreamAcc {  // the running top nonzero digit of one output stream
   u32 topv;
 };
 
+template <int IW>
 __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int paired, int njobs) {
   extern __shared__ u32 w1_sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int job = blockIdx.x * W1_WARPS + warp;
+  const int job = blockIdx.x * (blockDim.x >> 5) + warp;
   if (job >= njobs) return;
   const int per_pair = paired ? A.nops / 2 : A.nops;
   const int pair = job / per_pair;
@@ -85,27 +97,31 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
   const u32 biasw = bias ? (1u << (b - 1)) : 0u;
   const bool validate = (o_pos >= 0 && A.op[o_pos].validate) || (o_neg >= 0 && A.op[o_neg].validate);
   const int m = P.m;
-  u32* sc = w1_sm + warp * (L + W1_PAD);
+  u32* sc = w1_sm + warp * (L + W1_PAD) * IW;
   const u32* cf = P.coeffs + (long long)pair * P.coeff_pair_stride;
 
   // ---- stage: range check on the raw words, bias lift, reversal
   bool bad = false;
-  auto put = [&](int i, u32 raw) {
+  auto put = [&](int x, u32 raw) {  // word x of the vector (coefficient x / IW)
+    const int i = IW == 1 ? x : x / IW, w = IW == 1 ? 0 : x - i * IW;
     if (validate) {
       if (bias) {
         const int v = (int)raw;
         if (b < 32) bad |= (v < -(1 << (b - 1))) || (v >= (1 << (b - 1)));
-      } else if (b < 32) {
-        bad |= (raw >> b) != 0u;
+      } else {
+        const int lo_bit = 32 * w;
+        if (lo_bit >= b) bad |= raw != 0u;
+        else if (b - lo_bit < 32) bad |= (raw >> (b - lo_bit)) != 0u;
       }
     }
-    sc[rev ? L - 1 - i : i] = bias ? ((raw + biasw) & bmask) : raw;
+    sc[(rev ? L - 1 - i : i) * IW + w] = bias ? ((raw + biasw) & bmask) : raw;
   };
-  if ((L & 3) == 0 && (reinterpret_cast<uintptr_t>(cf) & 15) == 0) {
+  const int nw = L * IW;
+  if ((nw & 3) == 0 && (reinterpret_cast<uintptr_t>(cf) & 15) == 0) {
     // every load of a batch in flight before any is used (one warp stages the
     // whole vector: memory-level parallelism comes from the batch)
     const uint4* s4 = reinterpret_cast<const uint4*>(cf);
-    const int n4 = L / 4;
+    const int n4 = nw / 4;
     for (int base = 0; base < n4; base += 32 * 8) {
       uint4 r[8];
 #pragma unroll
@@ -125,9 +141,9 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
       }
     }
   } else {
-    for (int x = lane; x < L; x += 32) put(x, __ldg(cf + x));
+    for (int x = lane; x < nw; x += 32) put(x, __ldg(cf + x));
   }
-  for (int x = L + lane; x < L + W1_PAD; x += 32) sc[x] = 0u;
+  for (int x = nw + lane; x < (L + W1_PAD) * IW; x += 32) sc[x] = 0u;
   if (__any_sync(0xffffffffu, bad) && lane == 0) raise_err(A.err, ERR_INVAL);
   __syncwarp();
   // ---- signed path: prefix sums of the lifted coefficients in natural order
@@ -138,7 +154,7 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
     if (lane == 0) out[0] = 0ull;
     for (int i0 = 0; i0 < L; i0 += 32) {
       const int i = i0 + lane;
-      unsigned long long inc = i < L ? sc[rev ? L - 1 - i : i] : 0ull;
+      unsigned long long inc = i < L ? sc[(rev ? L - 1 - i : i) * IW] : 0ull;  // signed: IW == 1
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
@@ -160,8 +176,8 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
         Cur1 ce, co;
         ce.init(q, 0, S);
         co.init(q, N, S);
-        e = ce.bits(sc, 0, S, b);
-        ov = co.bits(sc, 1, S, b);
+        e = ce.template bits<IW>(sc, 0, S, b);
+        ov = co.template bits<IW>(sc, 1, S, b);
       }
       const unsigned diff = __ballot_sync(0xffffffffu, e != ov);
       if (diff) {
@@ -190,8 +206,8 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
     for (int v = 0; v < W1_V; v++) {
       u32 e = 0u, ov = 0u;
       if (q0 + v < m) {
-        e = ce.bits(sc, 0, S, b);
-        ov = co.bits(sc, 1, S, b);
+        e = ce.template bits<IW>(sc, 0, S, b);
+        ov = co.template bits<IW>(sc, 1, S, b);
       }
       ce.next(S);
       co.next(S);
@@ -297,25 +313,32 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
 // staged vectors fit: every op shares the vector length and in_words == 1.
 bool pack_w1_ok(const PackArgs& a) {
   static const int en = getenv("KMX_PACK_W1") ? atoi(getenv("KMX_PACK_W1")) : 1;
-  if (!en || a.in_words != 1 || 2 * a.N < 32 || a.b > 2 * a.N || a.nops < 1) return false;
+  if (!en || a.in_words < 1 || a.in_words > 2 || 2 * a.N < 32 || a.b > 2 * a.N || a.nops < 1) return false;
   for (int i = 0; i < a.nops; i++)
     if (a.op[i].len != a.op[0].len || a.op[i].prefix_pair_stride < 0) return false;
-  const size_t smem = (size_t)W1_WARPS * (a.op[0].len + W1_PAD) * 4;
+  const size_t smem = (size_t)W1_WARPS * (a.op[0].len + W1_PAD) * a.in_words * 4;
   return smem <= 200 * 1024;
+}
+
+template <int IW>
+cudaError_t launch_w1(const PackArgs& a, int njobs, bool paired, cudaStream_t st) {
+  // small batches (config 1: 256 jobs): one warp per CTA, spread over more SMs
+  const int wpc = njobs < 148 * 2 * W1_WARPS ? 1 : W1_WARPS;
+  const size_t smem = (size_t)wpc * (a.op[0].len + W1_PAD) * IW * 4;
+  static size_t s_set = 0;
+  if (smem > 48 * 1024 && smem > s_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_pack_w1<IW>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    s_set = smem;
+  }
+  k_pack_w1<IW><<<(njobs + wpc - 1) / wpc, 32 * wpc, smem, st>>>(a, paired ? 1 : 0, njobs);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_pack_w1(const PackArgs& a, int batch, bool paired, cudaStream_t st) {
   const int njobs = batch * (paired ? a.nops / 2 : a.nops);
   if (njobs == 0) return cudaSuccess;
-  const size_t smem = (size_t)W1_WARPS * (a.op[0].len + W1_PAD) * 4;
-  static size_t s_set = 0;
-  if (smem > 48 * 1024 && smem > s_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_pack_w1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    s_set = smem;
-  }
-  k_pack_w1<<<(njobs + W1_WARPS - 1) / W1_WARPS, 32 * W1_WARPS, smem, st>>>(a, paired ? 1 : 0, njobs);
-  return cudaGetLastError();
+  return a.in_words == 1 ? launch_w1<1>(a, njobs, paired, st) : launch_w1<2>(a, njobs, paired, st);
 }
 
 }  // namespace kmx
