@@ -264,11 +264,19 @@ class Gpu:
         self.stream = torch.cuda.current_stream(self.dev)
         self.imad = kmx.imad_peak(4096)  # live IMAD.WIDE.U32 microbenchmark (limb products/s)
         self.tensor = kmx.tc_peak(2000)  # live dense tcgen05 u8 MMA microbenchmark (MAC/s)
+        self._shape_peaks = {}
         try:
             self.hbm = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
             self.hbm_src = "MEASURED_PEAKS.json hbm_gbs"
         except Exception:
             self.hbm, self.hbm_src = 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+    def tc_shape_peak(self, n):
+        """Dense SS-mode u8 MMA rate at M=128 and this N (kmx_tc_peak_n): the
+        ceiling of K2's own tile shape, where every MMA re-reads its A tile."""
+        if n not in self._shape_peaks:
+            self._shape_peaks[n] = float(self.L.kmx_tc_peak_n(n, 2000))
+        return self._shape_peaks[n]
 
     def barrier(self):
         if self.dist is not None:
@@ -433,6 +441,18 @@ def mul_roofline(g, cfg, cfg_name, v, mul_ms, clocks):
              "traffic": g.traffic(cfg_name, v, "tcmul_dram_bytes"),
              "same_kernel_in_imad_units": {"achieved": lps / 1e9, "unit": "G limb-products/s",
                                            "frac_of_imad_peak": lps / g.imad}}
+        if info.get("engine") == "tensor tiled" and info.get("H"):
+            n_mma = 16 * info["H"]
+            sp = g.tc_shape_peak(n_mma)
+            nprod_ = B * PCOUNT[ks_geometry(cfg, v)["variant"]]
+            issued = info["issued_byte_macs_per_product"] * nprod_ / (mul_ms * 1e-3) if info.get(
+                "issued_byte_macs_per_product") else None
+            r["same_shape_ceiling"] = {
+                "mma_shape": f"M=128 N={n_mma} K=32 (SS, u8)", "peak": 2.0 * sp / 1e12, "unit": "TOPS",
+                "frac_algorithmic": 2.0 * 16.0 * lps / (2.0 * sp) if sp > 0 else None,
+                "frac_issued": issued / sp if (issued and sp > 0) else None,
+                "note": "kmx_tc_peak_n(): the dense rate of the MMA shape K2 issues; frac_issued counts every MAC "
+                        "the tiles issue (incl. the Toeplitz zero padding), frac_algorithmic only the product's"}
         if info.get("engine") == "tensor tiled" and info.get("smem_bytes_per_product"):
             nprod = B * PCOUNT[ks_geometry(cfg, v)["variant"]]
             clk = (clocks or {}).get("sm_mhz") or 1965.0

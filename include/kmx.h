@@ -231,6 +231,11 @@ int kmx_mul_plan(int variant, int batch, int len_f, int len_g, int coeff_bits, u
  * memory, all SMs): the tensor roofline denominator for K2. */
 double kmx_tc_peak(int iters);
 
+/* The same microbenchmark for M=128 and N in {16, 32, 48, 64, 96, 128, 256}:
+ * the SS-mode rate at the tile widths K2 issues (each MMA re-reads its 4 KB A
+ * tile from shared memory), i.e. K2's same-shape ceiling. */
+double kmx_tc_peak_n(int n, int iters);
+
 /* Human-readable message for a return code. */
 const char* kmx_error_string(int code);
 

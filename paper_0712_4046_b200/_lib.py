@@ -78,6 +78,7 @@ _SIGS = {
     "kmx_bks_mod_mul_host": (_i, [_i, _i, _i, _i, ctypes.c_uint64, _vp, _vp, _vp]),
     "kmx_imad_peak": (ctypes.c_double, [_i]),
     "kmx_tc_peak": (ctypes.c_double, [_i]),
+    "kmx_tc_peak_n": (ctypes.c_double, [_i, _i]),
     "kmx_mul_engine": (_i, [_i, _i, _i, _i, _u]),
     "kmx_mul_karatsuba_levels": (_i, [_i, _i, _i, _i, _i, _u]),
     "kmx_mul_plan": (_i, [_i, _i, _i, _i, _i, _u, _i64p]),

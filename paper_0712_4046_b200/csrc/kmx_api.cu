@@ -1280,6 +1280,8 @@ double kmx_imad_peak(int iters) { return measure_imad_peak(iters > 0 ? iters : 4
 
 double kmx_tc_peak(int iters) { return measure_tc_peak(iters > 0 ? iters : 2000); }
 
+double kmx_tc_peak_n(int n, int iters) { return measure_tc_peak_shape(n, iters > 0 ? iters : 2000); }
+
 int kmx_mul_plan(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags, int64_t* out8) {
   KsPlan p;
   int rc = make_plan(p, variant, batch, len_f, len_g, coeff_bits, 0, flags);

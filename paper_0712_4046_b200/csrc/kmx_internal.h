@@ -72,6 +72,7 @@ bool tc_supported(int ma, int mb, size_t stage_bytes = 0);
 // operands never reach global memory (MulArgs A/B unused).
 cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk = nullptr, int P = 1);
 double measure_tc_peak(int iters);
+double measure_tc_peak_shape(int n, int iters);
 // engine choice (kmx_api.cu): the tensor cores for this shape, and whether
 // some engine takes the whole product (else Karatsuba splits it)
 bool mul_use_tensor(int ma, int mb);

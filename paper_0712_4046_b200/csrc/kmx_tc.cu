@@ -652,11 +652,12 @@ cudaError_t launch_h(const TcArgs& ta, int nw, size_t smem, cudaStream_t st) {
 // Dense tcgen05 u8 MMA throughput (M=128, N=256, K=32, SS): one elected
 // thread per CTA issues back-to-back MMAs over 8 resident K-steps into one
 // TMEM accumulator, committing every 32; the roofline denominator for K2.
+template <int N>
 __global__ void __launch_bounds__(128) k_tc_peak(int iters, unsigned long long* sink) {
   extern __shared__ __align__(128) unsigned char pk[];
   __shared__ uint32_t tbase;
   __shared__ __align__(8) unsigned long long bar;
-  constexpr int N = 256, KS = 8;
+  constexpr int KS = 8;
   constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
   unsigned char* A = pk;
   unsigned char* B = pk + KS * 4096;
@@ -699,9 +700,14 @@ __global__ void __launch_bounds__(128) k_tc_peak(int iters, unsigned long long* 
 
 }  // namespace
 
-double measure_tc_peak(int iters) {
-  const size_t smem = 8 * 4096 + 8 * 256 * 32;
-  if (cudaFuncSetAttribute(k_tc_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+// Dense SS-mode u8 MMA rate (multiply-accumulates per second, all SMs) for
+// M = 128 and the given N (16..256): N = 256 is the device peak (the roofline
+// denominator); the smaller N of K2's tiles give the same-shape ceiling,
+// where each MMA re-reads its 4 KB A tile from shared memory.
+template <int N>
+double measure_tc_peak_n(int iters) {
+  const size_t smem = 8 * 4096 + 8 * N * 32;
+  if (cudaFuncSetAttribute(k_tc_peak<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
     return -1.0;
   unsigned long long* sink = nullptr;
   if (cudaMalloc(&sink, 8) != cudaSuccess) return -1.0;
@@ -709,11 +715,11 @@ double measure_tc_peak(int iters) {
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
-  k_tc_peak<<<grid, 128, smem>>>(8, sink);
+  k_tc_peak<N><<<grid, 128, smem>>>(8, sink);
   float best = 1e30f;
   for (int rep = 0; rep < 3; rep++) {
     cudaEventRecord(e0);
-    k_tc_peak<<<grid, 128, smem>>>(iters, sink);
+    k_tc_peak<N><<<grid, 128, smem>>>(iters, sink);
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
     float ms = 0.f;
@@ -724,7 +730,22 @@ double measure_tc_peak(int iters) {
   cudaEventDestroy(e1);
   cudaFree(sink);
   if (cudaGetLastError() != cudaSuccess) return -1.0;
-  return (double)grid * iters * 32 * 128.0 * 256 * 32 / (best * 1e-3);
+  return (double)grid * iters * 32 * 128.0 * N * 32 / (best * 1e-3);
+}
+
+double measure_tc_peak(int iters) { return measure_tc_peak_n<256>(iters); }
+
+double measure_tc_peak_shape(int n, int iters) {
+  switch (n) {
+    case 16: return measure_tc_peak_n<16>(iters);
+    case 32: return measure_tc_peak_n<32>(iters);
+    case 48: return measure_tc_peak_n<48>(iters);
+    case 64: return measure_tc_peak_n<64>(iters);
+    case 96: return measure_tc_peak_n<96>(iters);
+    case 128: return measure_tc_peak_n<128>(iters);
+    case 256: return measure_tc_peak_n<256>(iters);
+    default: return -1.0;
+  }
 }
 
 namespace {
