@@ -689,6 +689,12 @@ int ks_mul_host_streams(const KsPlan& pfull, HostCtx* c, const uint32_t* f, cons
   uint32_t* dg = (uint32_t*)((char*)c->pbuf[0] + align256(fb));
   uint32_t* dh = (uint32_t*)c->pbuf[1];
   int nl = 0;
+  static const int tr = getenv("KMX_HOST_TRACE") ? atoi(getenv("KMX_HOST_TRACE")) : 0;
+  cudaEvent_t tev[3 * HOST_MAX_CHUNKS + 1];
+  if (tr >= 2) {
+    for (int i = 0; i < 3 * nchunks + 1; i++) cudaEventCreate(&tev[i]);
+    cudaEventRecord(tev[3 * nchunks], c->s_in);
+  }
   for (int i = 0; i < nchunks; i++) {
     const KsPlan& pp = plans[i];
     const size_t o = (size_t)starts[i];
@@ -697,24 +703,40 @@ int ks_mul_host_streams(const KsPlan& pfull, HostCtx* c, const uint32_t* f, cons
         cudaMemcpyAsync(dg + o * gpp, g + o * gpp, (size_t)bi * gpp * 4, cudaMemcpyHostToDevice, c->s_in) != cudaSuccess ||
         cudaEventRecord(c->ev_in[i], c->s_in) != cudaSuccess)
       return KMX_ECUDA;
-    cudaStream_t sc = c->s_comp[i & 1];
+    if (tr >= 2) cudaEventRecord(tev[3 * i], c->s_in);
+    static const int ncs = getenv("KMX_HOST_COMP_STREAMS") ? atoi(getenv("KMX_HOST_COMP_STREAMS")) : 2;
+    const int cs = ncs >= 2 ? (i & 1) : 0;
+    cudaStream_t sc = c->s_comp[cs];
     if (cudaStreamWaitEvent(sc, c->ev_in[i], 0) != cudaSuccess) return KMX_ECUDA;
-    void* ws = c->pbuf[2 + (i & 1)];
-    rc = run_plan(pp, df + o * fpp, dg + o * gpp, dh + o * hpp, out_words, ws, c->pcap[2 + (i & 1)], sc);
+    void* ws = c->pbuf[2 + cs];
+    rc = run_plan(pp, df + o * fpp, dg + o * gpp, dh + o * hpp, out_words, ws, c->pcap[2 + cs], sc);
     if (rc) return rc;
     nl += g_launches;
     if (cudaMemcpyAsync(c->flags + i, ws, 4, cudaMemcpyDeviceToHost, sc) != cudaSuccess ||
         cudaEventRecord(c->ev_done[i], sc) != cudaSuccess)
       return KMX_ECUDA;
+    if (tr >= 2) cudaEventRecord(tev[3 * i + 1], sc);
     if (cudaStreamWaitEvent(c->s_out, c->ev_done[i], 0) != cudaSuccess ||
         cudaMemcpyAsync(h + o * hpp, dh + o * hpp, (size_t)bi * hpp * 4, cudaMemcpyDeviceToHost, c->s_out) != cudaSuccess)
       return KMX_ECUDA;
+    if (tr >= 2) cudaEventRecord(tev[3 * i + 2], c->s_out);
   }
   static const int trace = getenv("KMX_HOST_TRACE") ? atoi(getenv("KMX_HOST_TRACE")) : 0;
   const auto t_enq = std::chrono::steady_clock::now();
   if (cudaStreamSynchronize(c->s_out) != cudaSuccess || cudaStreamSynchronize(c->s_comp[0]) != cudaSuccess ||
       cudaStreamSynchronize(c->s_comp[1]) != cudaSuccess)
     return KMX_ECUDA;
+  if (tr >= 2) {
+    for (int i = 0; i < nchunks; i++) {
+      float a = 0, b = 0, d = 0;
+      cudaEventElapsedTime(&a, tev[3 * nchunks], tev[3 * i]);
+      cudaEventElapsedTime(&b, tev[3 * nchunks], tev[3 * i + 1]);
+      cudaEventElapsedTime(&d, tev[3 * nchunks], tev[3 * i + 2]);
+      fprintf(stderr, "  chunk %d (%d pairs): h2d done %.1f us, kernels done %.1f us, d2h done %.1f us\n", i,
+              plans[i].batch, 1e3 * a, 1e3 * b, 1e3 * d);
+    }
+    for (int i = 0; i < 3 * nchunks + 1; i++) cudaEventDestroy(tev[i]);
+  }
   if (trace) {
     const auto t_end = std::chrono::steady_clock::now();
     fprintf(stderr, "kmx host: %d chunks, enqueue %.1f us, enqueue-to-done %.1f us\n", nchunks,
