@@ -527,11 +527,354 @@ __global__ void __launch_bounds__(32 * NW) k_tcmul(TcArgs ta) {
   if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
 }
 
+// ------------------------------------------------- persistent, specialized
+// Short products (one CTA range per product, one accumulation segment): a
+// persistent CTA walks products z = blockIdx.x, + gridDim.x, ... with the
+// warps specialized and every hand-off on an mbarrier, so one product's
+// operand copy, B build, MMAs and epilogue overlap its neighbours':
+//   warp 0 (lane 0)  MMA issue into TMEM accumulator buf = i & 1;
+//   warps 1-3        B builders (as k_tcmul), ring phases continue across
+//                    products; warp 1 lane 0 also clears the operands'
+//                    rounding limbs once their bulk copies land;
+//   warps 4-7        epilogue of product i from accumulator buf while the
+//                    MMAs of product i+1 fill the other; warp 4 lane 0
+//                    prefetches product i+2's operands into buffer buf (TMA
+//                    bulk copies) as soon as product i's MMAs completed.
+// Operand buffers, TMEM accumulators and the staging area are doubled; the
+// epilogue has its own staging area (the B ring stays live).
+struct TcSharedP {
+  unsigned long long bar_full[TC_MAXNB];
+  unsigned long long bar_empty[TC_MAXNB];
+  unsigned long long bar_stage[2];      // bulk copies of product i landed (complete_tx)
+  unsigned long long bar_ready[2];      // ... and its rounding limbs cleared
+  unsigned long long bar_acc_full[2];   // MMAs of product i done (tcgen05.commit)
+  unsigned long long bar_acc_empty[2];  // epilogue drained accumulator buf (4 warps)
+  unsigned long long s_cout[TC_EPI / 32];
+  unsigned long long carry;
+  uint32_t tmem_base;
+  uint32_t warp_map[TC_EPI / 32];
+};
+
+template <int H>
+__host__ __device__ inline size_t tcp_abuf(int La) { return round128((size_t)La + 2 * TcG<H>::APAD + 16); }
+template <int H>
+__host__ __device__ inline size_t tcp_bbuf(int Lb) { return round128((size_t)Lb + 2 * TcB<H>::BPAD + 16); }
+template <int H>
+__host__ __device__ inline size_t tcp_smem(int La, int Lb, int KC, int NB) {
+  return round128(sizeof(TcSharedP)) + 2 * tcp_abuf<H>(La) + 2 * tcp_bbuf<H>(Lb) + (size_t)NB * KC * TcG<H>::STEPB +
+         (size_t)4096 * H;
+}
+
+template <int H>
+__global__ void __launch_bounds__(256, 1) k_tcmul_p(TcArgs ta) {
+  using G = TcG<H>;
+  constexpr int THREADS = 256;
+  const MulArgs& a = ta.m;
+  extern __shared__ __align__(128) unsigned char tsm[];
+  TcSharedP& sh = *reinterpret_cast<TcSharedP*>(tsm);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const bool sw = a.mb > a.ma;
+  const int mA = sw ? a.mb : a.ma, mB = sw ? a.ma : a.mb;
+  const long long astr = sw ? a.b_stride : a.a_stride, bstr = sw ? a.a_stride : a.b_stride;
+  const uint32_t* Abase = sw ? a.B : a.A;
+  const uint32_t* Bbase = sw ? a.A : a.B;
+  const TcDims d = tc_dims<H>(mA, mB);
+  const int mp = a.ma + a.mb;
+  const int ntl = d.ntiles;  // all tiles of a product in this CTA
+  const int KC = ta.KC, NB = ta.NB;
+  const int La16 = (d.La + 15) & ~15, Lb16 = (d.Lb + 15) & ~15;
+  unsigned char* abuf[2];
+  unsigned char* bbuf[2];
+  abuf[0] = tsm + round128(sizeof(TcSharedP));
+  abuf[1] = abuf[0] + tcp_abuf<H>(d.La);
+  bbuf[0] = abuf[1] + tcp_abuf<H>(d.La);
+  bbuf[1] = bbuf[0] + tcp_bbuf<H>(d.Lb);
+  unsigned char* bring = bbuf[1] + tcp_bbuf<H>(d.Lb);
+  unsigned long long* stg = reinterpret_cast<unsigned long long*>(bring + (size_t)NB * KC * G::STEPB);
+  // the CTA span of K-steps (the same for every product of the launch)
+  int cs_lo = d.S, cs_hi = 0;
+  for (int t = 0; t < ntl; t++) {
+    int slo, shi;
+    tc_tile_steps<H>(d, t, slo, shi);
+    if (slo < shi) { cs_lo = min(cs_lo, slo); cs_hi = max(cs_hi, shi); }
+  }
+  const int clo = cs_lo < cs_hi ? cs_lo / KC : 0;
+  const int chi = cs_lo < cs_hi ? (cs_hi + KC - 1) / KC : 0;
+  const int nchunk = chi - clo;
+  uint32_t acc_cols = 32;
+  while (acc_cols < (uint32_t)(ntl * G::N)) acc_cols <<= 1;
+  const uint32_t cols = 2 * acc_cols;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
+                 "r"(cols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  const int nmine = blockIdx.x < a.nprod ? (a.nprod - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+  auto prefetch = [&](int i) {  // thread-level: product i of this CTA into buffer i & 1
+    const long long z = blockIdx.x + (long long)i * gridDim.x;
+    const uint32_t bar = smem_u32(&sh.bar_stage[i & 1]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"((uint32_t)(La16 + Lb16))
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(abuf[i & 1] + G::APAD)),
+                 "l"(Abase + z * astr), "r"((uint32_t)La16), "r"(bar)
+                 : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(bbuf[i & 1] + TcB<H>::BPAD)),
+                 "l"(Bbase + z * bstr), "r"((uint32_t)Lb16), "r"(bar)
+                 : "memory");
+  };
+  // zero pads of both buffers (outside every copy's byte range)
+  for (int bsel = 0; bsel < 2; bsel++) {
+    uint4* aw = reinterpret_cast<uint4*>(abuf[bsel]);
+    uint4* bq = reinterpret_cast<uint4*>(bbuf[bsel]);
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    constexpr int AQ = G::APAD / 16, BQ = TcB<H>::BPAD / 16;
+    for (int w = tid; w < AQ; w += THREADS) aw[w] = z4;
+    for (int w = AQ + La16 / 16 + tid; w < 2 * AQ + d.La / 16 + 1; w += THREADS) aw[w] = z4;
+    for (int w = tid; w < BQ; w += THREADS) bq[w] = z4;
+    for (int w = BQ + Lb16 / 16 + tid; w < 2 * BQ + d.Lb / 16 + 1; w += THREADS) bq[w] = z4;
+  }
+  if (tid == 0) {
+    for (int i = 0; i < TC_MAXNB; i++) {
+      mbar_init(smem_u32(&sh.bar_full[i]), 3);
+      mbar_init(smem_u32(&sh.bar_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(smem_u32(&sh.bar_stage[i]), 1);
+      mbar_init(smem_u32(&sh.bar_ready[i]), 1);
+      mbar_init(smem_u32(&sh.bar_acc_full[i]), 1);
+      mbar_init(smem_u32(&sh.bar_acc_empty[i]), 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sh.tmem_base;
+  if (tid == 0) {
+    if (nmine > 0) prefetch(0);
+    if (nmine > 1) prefetch(1);
+  }
+
+  if (warp == 0) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      long long kg = 0;  // ring chunk counter across products
+      for (int i = 0; i < nmine; i++) {
+        const int buf = i & 1;
+        const uint32_t ph = (uint32_t)((i >> 1) & 1);
+        mbar_wait(smem_u32(&sh.bar_ready[buf]), ph);
+        mbar_wait(smem_u32(&sh.bar_acc_empty[buf]), ph ^ 1u);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sA = smem_u32(abuf[buf]) + G::APAD;
+        const uint32_t dacc = tmem + (uint32_t)buf * acc_cols;
+        uint32_t started = 0u;
+        for (int c = clo; c < chi; c++, kg++) {
+          const int st = (int)(kg % NB);
+          mbar_wait(smem_u32(&sh.bar_full[st]), (uint32_t)((kg / NB) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const int sb = c * KC, se = min(d.S, sb + KC);
+          const uint32_t sB = smem_u32(bring + (size_t)st * KC * G::STEPB);
+          for (int t = 0; t < ntl; t++) {
+            int slo, shi;
+            tc_tile_steps<H>(d, t, slo, shi);
+            const int s0 = max(slo, sb), s1 = min(shi, se);
+            const uint32_t abase = sA + (uint32_t)(t * G::T + d.ulo);
+            const uint32_t dcol = dacc + (uint32_t)(t * G::N);
+            for (int s = s0; s < s1; s++) {
+              const uint64_t ad = sdesc(abase + 32u * (uint32_t)s, 16, G::SBO_A);
+              const uint64_t bd = sdesc(sB + (uint32_t)((s - sb) * G::STEPB), 128, 256);
+              mma_i8(dcol, ad, bd, G::IDESC, (started >> t) & 1u);
+              started |= 1u << t;
+            }
+          }
+          mma_commit(smem_u32(&sh.bar_empty[st]));
+        }
+        mma_commit(smem_u32(&sh.bar_acc_full[buf]));
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    // ---------------- B builders (3 warps, 6 half-warps)
+    const int hb = 2 * (warp - 1) + (lane >> 4), nl = lane & 15;
+    const int A0 = (13 + nl) >> 2, r0 = (13 + nl) & 3;
+    const uint32_t psel = (uint32_t)(r0 + 3) | ((uint32_t)(r0 + 2) << 4) | ((uint32_t)(r0 + 1) << 8) |
+                          ((uint32_t)r0 << 12);
+    constexpr int NHB = 6;
+    long long kg = 0;
+    for (int i = 0; i < nmine; i++) {
+      const int buf = i & 1;
+      const uint32_t ph = (uint32_t)((i >> 1) & 1);
+      if (warp == 1) {
+        mbar_wait(smem_u32(&sh.bar_stage[buf]), ph);
+        if (lane == 0) {  // the rounding limbs past the operands (row padding, not operand data)
+          uint32_t* a32 = reinterpret_cast<uint32_t*>(abuf[buf] + G::APAD);
+          uint32_t* b32 = reinterpret_cast<uint32_t*>(bbuf[buf] + TcB<H>::BPAD);
+          for (int w = mA; w < La16 / 4; w++) a32[w] = 0u;
+          for (int w = mB; w < Lb16 / 4; w++) b32[w] = 0u;
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          mbar_arrive(smem_u32(&sh.bar_ready[buf]));
+        }
+        __syncwarp();
+      }
+      mbar_wait(smem_u32(&sh.bar_ready[buf]), ph);
+      const uint32_t* bw = reinterpret_cast<const uint32_t*>(bbuf[buf]) + TcB<H>::BPAD / 4;
+      for (int c = clo; c < chi; c++, kg++) {
+        const int st = (int)(kg % NB);
+        if (kg >= NB) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((kg / NB) - 1) & 1));
+        unsigned char* bb = bring + (size_t)st * KC * G::STEPB;
+        const int sb = c * KC, se = min(d.S, sb + KC);
+        const int nitems = (se - sb) * 2 * H;
+        for (int ib = 0; ib < nitems; ib += 2 * NHB) {
+          uint32_t wv[2];
+          int doff[2];
+          bool valid[2];
+#pragma unroll
+          for (int x = 0; x < 2; x++) {
+            const int it = ib + x * NHB + hb;
+            valid[x] = it < nitems;
+            const int sl = valid[x] ? it / (2 * H) : 0;
+            const int rem = valid[x] ? it - sl * 2 * H : 0;
+            const int kc = rem & 1, j = rem >> 1;
+            const int u0 = d.ulo + 32 * (sb + sl);
+            const int w0 = 128 * j - u0 - 16 * kc - 16;
+            wv[x] = bw[(w0 >> 2) + nl];
+            doff[x] = sl * G::STEPB + 256 * ((nl >> 3) + 2 * j) + 128 * kc + 16 * (nl & 7);
+          }
+#pragma unroll
+          for (int x = 0; x < 2; x++) {
+            uint32_t W[5];
+#pragma unroll
+            for (int q = 0; q < 5; q++) W[q] = __shfl_sync(0xffffffffu, wv[x], A0 - 3 + q, 16);
+            if (valid[x]) {
+              uint4 o;
+              o.x = __byte_perm(W[3], W[4], psel);
+              o.y = __byte_perm(W[2], W[3], psel);
+              o.z = __byte_perm(W[1], W[2], psel);
+              o.w = __byte_perm(W[0], W[1], psel);
+              *reinterpret_cast<uint4*>(bb + doff[x]) = o;
+            }
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(&sh.bar_full[st]));
+      }
+    }
+  } else {
+    // ---------------- epilogue (warps 4-7: TMEM lane quarter ew)
+    const int ew = warp - 4, m = tid - 128;
+    for (int i = 0; i < nmine; i++) {
+      const int buf = i & 1;
+      const uint32_t ph = (uint32_t)((i >> 1) & 1);
+      const long long z = blockIdx.x + (long long)i * gridDim.x;
+      mbar_wait(smem_u32(&sh.bar_acc_full[buf]), ph);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      // product i's operands are no longer read: prefetch product i + 2
+      if (m == 0 && i + 2 < nmine) prefetch(i + 2);
+      const uint32_t dacc = tmem + (uint32_t)buf * acc_cols;
+      uint32_t* Pz = a.P + z * a.p_stride;
+      if (m == 0) sh.carry = 0ull;
+      for (int t = 0; t < ntl; t++) {
+        int slo, shi;
+        tc_tile_steps<H>(d, t, slo, shi);
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // previous tile's readers are done
+#pragma unroll
+        for (int j = 0; j < H; j++) {
+          unsigned long long ls[4] = {0ull, 0ull, 0ull, 0ull};
+          if (slo < shi) {
+            uint32_t v[16];
+            tmem_ld16(dacc + ((uint32_t)(32 * ew) << 16) + (uint32_t)(t * G::N + 16 * j), v);
+#pragma unroll
+            for (int q = 0; q < 4; q++)
+              ls[q] = (unsigned long long)v[4 * q] + ((unsigned long long)v[4 * q + 1] << 8) +
+                      ((unsigned long long)v[4 * q + 2] << 16) + ((unsigned long long)v[4 * q + 3] << 24);
+          }
+          unsigned long long* dst = stg + 4 * (m & 7) + 32 * j + 32 * H * (m >> 3);
+#pragma unroll
+          for (int q = 0; q < 4; q++) dst[q] = ls[q];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        uint32_t dg[4 * H];
+        unsigned long long x = 0ull;
+#pragma unroll
+        for (int q = 0; q < 4 * H; q++) {
+          x = (x >> 32) + stg[4 * H * m + q];
+          dg[q] = (uint32_t)x;
+        }
+        const unsigned long long cout = x >> 32;
+        unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
+        if (lane == 31) sh.s_cout[ew] = cout;
+        uint32_t ones = 0xFFFFFFFFu;
+#pragma unroll
+        for (int q = 1; q < 4 * H; q++) ones &= dg[q];
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (lane == 0) xin = ew ? sh.s_cout[ew - 1] : sh.carry;
+        const unsigned long long s0 = (unsigned long long)dg[0] + xin;
+        const bool all1 = ones == 0xFFFFFFFFu;
+        const uint32_t g = all1 && (s0 >> 32) != 0ull;
+        const uint32_t p = all1 && ((s0 + 1ull) >> 32) != 0ull;
+        uint32_t F = g | (p << 1);
+#pragma unroll
+        for (int dd = 1; dd < 32; dd <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
+          if (lane >= dd) F = cm2(F, y);
+        }
+        if (lane == 31) sh.warp_map[ew] = F;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
+        uint32_t Wm = CM2_ID;
+        for (int w = 0; w < ew; w++) Wm = cm2(sh.warp_map[w], Wm);
+        E = lane ? cm2(E, Wm) : Wm;
+        const uint32_t Fin = cm2(F, Wm);
+        unsigned long long acc = s0 + (E & 1u);
+        dg[0] = (uint32_t)acc;
+#pragma unroll
+        for (int q = 1; q < 4 * H; q++) {
+          acc = (acc >> 32) + dg[q];
+          dg[q] = (uint32_t)acc;
+        }
+        const int L = t * G::LIMBS + 4 * H * m;
+        if (L + 4 * H <= mp) {
+#pragma unroll
+          for (int q = 0; q < H; q++)
+            *reinterpret_cast<uint4*>(Pz + L + 4 * q) =
+                make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4 * H; q++)
+            if (L + q < mp) Pz[L + q] = dg[q];
+        }
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // every reader of sh.carry is done
+        if (m == 127) sh.carry = cout + (Fin & 1u);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      // band spills: zero, the product's final carry on its top band
+      for (int bi = m; bi < a.nbands; bi += 128) {
+        unsigned long long* sp = a.spill + (z * a.nbands + bi) * 2;
+        sp[0] = bi == 2 * H * ntl - 1 ? sh.carry : 0ull;
+        sp[1] = 0ull;
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // sh.carry read by all before the next product resets it
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(&sh.bar_acc_empty[buf]));
+    }
+  }
+  (void)nchunk;
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(cols));
+}
+
 // ---------------------------------------------------------------- planning
 struct TcPlan {
   int H, NW, KC, NB, TPC, nranges, ntiles, nseg;
   size_t smem;
   double cost;  // modelled cycles per product
+  int persist = 0;  // k_tcmul_p (persistent, warp-specialized)
 };
 
 int env_int_tc(const char* n, int dflt) {
@@ -759,6 +1102,25 @@ bool tc_supported(int ma, int mb, size_t stage_bytes) {
 namespace {
 cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, const PackArgs* pk, int P);
 
+// The persistent kernel takes a tiling whose product fits one CTA range and
+// one accumulation segment, with both accumulators in TMEM.
+bool tcp_ok(int ma, int mb, const TcPlan& p) {
+  if (p.nseg != 1) return false;
+  const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
+  size_t smem = 0;
+  int ntl = 0, N = 16 * p.H;
+  switch (p.H) {
+#define KMX_TCP_CASE(HH) \
+    case HH: { const TcDims d = tc_dims<HH>(mA, mB); ntl = d.ntiles; smem = tcp_smem<HH>(d.La, d.Lb, p.KC, p.NB); break; }
+    KMX_TCP_CASE(1) KMX_TCP_CASE(2) KMX_TCP_CASE(3) KMX_TCP_CASE(4) KMX_TCP_CASE(6) KMX_TCP_CASE(8)
+#undef KMX_TCP_CASE
+    default: return false;
+  }
+  uint32_t acc = 32;
+  while (acc < (uint32_t)(ntl * N)) acc <<= 1;
+  return ntl <= 32 && 2 * acc <= 512 && smem <= 200 * 1024;
+}
+
 // Candidate tilings: every feasible H with KC in {8, 16} and NW in {4, 8},
 // keeping those the model puts within 1.6x of its best.
 std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
@@ -775,10 +1137,33 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
       KMX_CAND_H(1) KMX_CAND_H(2) KMX_CAND_H(3) KMX_CAND_H(4) KMX_CAND_H(6) KMX_CAND_H(8)
 #undef KMX_CAND_H
     }
+  if (env_int_tc("KMX_TC_PERSIST", 0) == 2) {  // the persistent forms only (a forced test path)
+    std::vector<TcPlan> only;
+    for (const TcPlan& p : v)
+      if (tcp_ok(ma, mb, p)) {
+        TcPlan q = p;
+        q.persist = 1; q.NW = 8; q.TPC = q.ntiles; q.nranges = 1;
+        only.push_back(q);
+      }
+    if (!only.empty()) return only;
+  }
   std::vector<TcPlan> out;
+  // the persistent forms join the candidates only on request: measured at c2
+  // they run 2.4x slower than the one-shot kernel (one MMA pipeline and one
+  // 4-warp epilogue per CTA, 1-3 CTAs per SM, against ~8 one-shot CTAs whose
+  // epilogues overlap each other's MMAs), and were never chosen
+  const int pers = env_int_tc("KMX_TC_PERSIST", 0);
   for (const TcPlan& p : v)
     if (p.cost <= 1.6 * best) {
       out.push_back(p);
+      if (pers && tcp_ok(ma, mb, p)) {  // the persistent form of the same tiling
+        TcPlan q = p;
+        q.persist = 1;
+        q.NW = 8;
+        q.TPC = q.ntiles;
+        q.nranges = 1;
+        out.push_back(q);
+      }
       // fewer tiles per CTA (more, shorter CTAs): a better last wave on long
       // products whose CTAs fill an SM each
       for (int tpc : {p.TPC / 2, (p.TPC * 2) / 3}) {
@@ -880,6 +1265,10 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
   }
   if (!tc_plan(a.ma, a.mb, a.nprod, stage, p)) return cudaErrorNotSupported;
   if (a.nprod == 0) return cudaSuccess;
+  if (!pk && env_int_tc("KMX_TC_PERSIST", 0) == 2 && tcp_ok(a.ma, a.mb, p)) {  // forced test path
+    p.persist = 1; p.NW = 8; p.TPC = p.ntiles; p.nranges = 1;
+    return launch_plan(a, p, st, nullptr, 1);
+  }
   if (!pk) {
     bool launched = false;
     if (tc_tuned_plan(a, st, p, &launched) && launched) return cudaGetLastError();
@@ -888,10 +1277,67 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
 }
 
 namespace {
+template <int H>
+cudaError_t launch_persist_h(const TcArgs& ta, int ma, int mb, cudaStream_t st) {
+  const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
+  const TcDims d = tc_dims<H>(mA, mB);
+  const size_t smem = tcp_smem<H>(d.La, d.Lb, ta.KC, ta.NB);
+  static size_t s_set = 0;
+  if (smem > 48 * 1024 && smem > s_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_tcmul_p<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    s_set = smem;
+  }
+  int per_sm = 0;
+  cudaError_t e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_tcmul_p<H>, 256, smem);
+  if (e != cudaSuccess) return e;
+  uint32_t acc = 32;
+  while (acc < (uint32_t)(d.ntiles * 16 * H)) acc <<= 1;
+  const int by_tmem = (int)(512 / (2 * acc));
+  if (per_sm > by_tmem) per_sm = by_tmem;
+  if (per_sm < 1) per_sm = 1;
+  long long grid = (long long)tc_num_sms() * per_sm;
+  if (grid > ta.m.nprod) grid = ta.m.nprod;
+  if (grid < 1) return cudaSuccess;
+  k_tcmul_p<H><<<(unsigned)grid, 256, smem, st>>>(ta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_persist(const MulArgs& a, const TcPlan& p, cudaStream_t st) {
+  TcArgs ta;
+  memset(&ta, 0, sizeof ta);
+  ta.m = a;
+  ta.KC = p.KC;
+  ta.NB = p.NB;
+  ta.TPC = p.ntiles;
+  ta.nranges = 1;
+  ta.nseg = 1;
+  ta.bulk = 1;
+  if (a.nprod == 0) return cudaSuccess;
+  switch (p.H) {
+    case 1: return launch_persist_h<1>(ta, a.ma, a.mb, st);
+    case 2: return launch_persist_h<2>(ta, a.ma, a.mb, st);
+    case 3: return launch_persist_h<3>(ta, a.ma, a.mb, st);
+    case 4: return launch_persist_h<4>(ta, a.ma, a.mb, st);
+    case 6: return launch_persist_h<6>(ta, a.ma, a.mb, st);
+    default: return launch_persist_h<8>(ta, a.ma, a.mb, st);
+  }
+}
+
 cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, const PackArgs* pk, int P) {
   if (env_int_tc("KMX_TC_VERBOSE", 0))
-    fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d nseg=%d smem=%zu cost=%.0f\n",
-            a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.nseg, p.smem, p.cost);
+    fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d nseg=%d smem=%zu cost=%.0f%s\n",
+            a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.nseg, p.smem, p.cost,
+            p.persist ? " persistent" : "");
+  if (p.persist && !pk) {
+    // eligible only with bulk-copy-aligned operands (checked here, per launch)
+    const bool swp = a.mb > a.ma;
+    const long long as = swp ? a.b_stride : a.a_stride, bs = swp ? a.a_stride : a.b_stride;
+    const int mA = swp ? a.mb : a.ma, mB = swp ? a.ma : a.mb;
+    const bool al = ((reinterpret_cast<uintptr_t>(a.A) | reinterpret_cast<uintptr_t>(a.B)) & 15) == 0 &&
+                    (as & 3) == 0 && (bs & 3) == 0 && as >= ((mA + 3) & ~3) && bs >= ((mB + 3) & ~3);
+    if (al) return launch_persist(a, p, st);
+  }
   TcArgs ta;
   ta.m = a;
   ta.bulk = env_int_tc("KMX_TC_BULK", 1);

@@ -33,7 +33,8 @@ SETTINGS = [
     {"KMX_WIDE": "1"},          # wide-digit finish + multiword reconstruction for every unsigned shape
     {"KMX_PACK_W1": "0"},       # block-per-job pack everywhere (no warp-per-job kernel)
     {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one-word shape (single and paired jobs)
-    {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},  # segmented pack everywhere; bivariate: IMAD univariate products, unstaged evaluation
+    {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},
+    {"KMX_TC_PERSIST": "2", "KMX_TC": "1"},  # persistent warp-specialized tensor-core kernel wherever it applies  # segmented pack everywhere; bivariate: IMAD univariate products, unstaged evaluation
 ]
 
 
