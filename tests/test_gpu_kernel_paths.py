@@ -32,9 +32,9 @@ SETTINGS = [
     {"KMX_KARA_MIN": "300", "KMX_TC": "0"},  # Karatsuba over integer-pipe leaves, up to 4 levels
     {"KMX_WIDE": "1"},          # wide-digit finish + multiword reconstruction for every unsigned shape
     {"KMX_PACK_W1": "0"},       # block-per-job pack everywhere (no warp-per-job kernel)
-    {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one-word shape (single and paired jobs)
-    {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},
-    {"KMX_TC_PERSIST": "2", "KMX_TC": "1"},  # persistent warp-specialized tensor-core kernel wherever it applies  # segmented pack everywhere; bivariate: IMAD univariate products, unstaged evaluation
+    {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one- and two-word shape (single and paired jobs)
+    {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},  # segmented pack; bivariate: IMAD products, unstaged evaluation
+    {"KMX_TC_PERSIST": "2", "KMX_TC": "1"},  # persistent warp-specialized tensor-core kernel wherever it applies
 ]
 
 
