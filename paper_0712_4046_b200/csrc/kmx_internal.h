@@ -71,6 +71,16 @@ bool tc_supported(int ma, int mb, size_t stage_bytes = 0);
 // (pack ops s and P + s of its pair) straight into shared memory; the packed
 // operands never reach global memory (MulArgs A/B unused).
 cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk = nullptr, int P = 1);
+// K2 with swizzled sliding windows and a phase table (kmx_tcs.cu): same
+// MulArgs contract; pitch = 32 / 64 / 128 (= the MMA's N).
+struct TcsPlan {
+  int pitch, KS, ntiles;
+  size_t smem;
+  long long mmas;  // MMAs per product
+  double cost;     // modelled SM cycles per product
+};
+bool tcs_plan(int ma, int mb, int pitch, TcsPlan& p);
+cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st);
 double measure_tc_peak(int iters);
 double measure_tc_peak_shape(int n, int iters);
 // engine choice (kmx_api.cu): the tensor cores for this shape, and whether

@@ -875,7 +875,38 @@ struct TcPlan {
   size_t smem;
   double cost;  // modelled cycles per product
   int persist = 0;  // k_tcmul_p (persistent, warp-specialized)
+  int swz = 0;      // k_tcswz (kmx_tcs.cu): the pitch (32 / 64 / 128), 0 = this file's kernels
+  TcsPlan sp;       // its plan
 };
+
+// KMX_TCS: -1 (default) the swizzled-window kernel joins the tuner's
+// candidates and is the untuned default wherever it takes the shape; 0 off;
+// 1 always (model-chosen pitch, no timing); 32 / 64 / 128 force that pitch.
+int tcs_mode() {
+  const char* v = getenv("KMX_TCS");
+  return v && *v ? atoi(v) : -1;
+}
+// the swizzled-window plan of lowest modelled cost (or the forced pitch)
+bool tcs_best(int ma, int mb, TcPlan& out) {
+  const int mode = tcs_mode();
+  if (mode == 0) return false;
+  bool ok = false;
+  for (int pitch : {32, 64, 128}) {
+    if (mode >= 32 && mode != pitch) continue;
+    TcsPlan sp;
+    if (!tcs_plan(ma, mb, pitch, sp)) continue;
+    if (!ok || sp.cost < out.sp.cost) {
+      out = TcPlan();
+      out.swz = pitch;
+      out.sp = sp;
+      out.H = pitch / 16; out.NW = 4; out.KC = sp.KS; out.NB = 1; out.TPC = 1;
+      out.nranges = sp.ntiles; out.ntiles = sp.ntiles; out.nseg = 1;
+      out.smem = sp.smem; out.cost = sp.cost;
+      ok = true;
+    }
+  }
+  return ok;
+}
 
 int env_int_tc(const char* n, int dflt) {
   const char* v = getenv(n);
@@ -1148,6 +1179,18 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
     if (!only.empty()) return only;
   }
   std::vector<TcPlan> out;
+  if (tcs_mode() != 0)
+    for (int pitch : {32, 64, 128}) {
+      if (tcs_mode() >= 32 && tcs_mode() != pitch) continue;
+      TcPlan q;
+      q.sp = TcsPlan();
+      if (!tcs_plan(ma, mb, pitch, q.sp)) continue;
+      q.swz = pitch;
+      q.H = pitch / 16; q.NW = 4; q.KC = q.sp.KS; q.NB = 1; q.TPC = 1;
+      q.nranges = q.sp.ntiles; q.ntiles = q.sp.ntiles; q.nseg = 1;
+      q.smem = q.sp.smem; q.cost = q.sp.cost;
+      out.push_back(q);
+    }
   // the persistent forms join the candidates only on request: measured at c2
   // they run 2.4x slower than the one-shot kernel (one MMA pipeline and one
   // 4-warp epilogue per CTA, 1-3 CTAs per SM, against ~8 one-shot CTAs whose
@@ -1246,8 +1289,8 @@ bool tc_tuned_plan(const MulArgs& a, cudaStream_t st, TcPlan& p, bool* launched)
     g_tune[key] = p;
   }
   if (env_int_tc("KMX_TC_VERBOSE", 0))
-    fprintf(stderr, "kmx_tc autotune: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d (%.4f ms of %zu candidates)\n", a.ma,
-            a.mb, a.nprod, p.H, p.NW, p.KC, best_ms, cands.size());
+    fprintf(stderr, "kmx_tc autotune: ma=%d mb=%d nprod=%d -> %s H=%d NW=%d KC=%d (%.4f ms of %zu candidates)\n", a.ma,
+            a.mb, a.nprod, p.swz ? "swizzled-window" : "tiled", p.H, p.NW, p.KC, best_ms, cands.size());
   // re-run the winner last so the buffers hold its (identical) output in order
   if (launch_plan(a, p, st, nullptr, 1) != cudaSuccess) return false;
   *launched = true;
@@ -1265,6 +1308,10 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
   }
   if (!tc_plan(a.ma, a.mb, a.nprod, stage, p)) return cudaErrorNotSupported;
   if (a.nprod == 0) return cudaSuccess;
+  if (!pk && tcs_mode() > 0) {  // forced: the swizzled-window kernel, no timing runs
+    TcPlan q;
+    if (tcs_best(a.ma, a.mb, q)) return launch_plan(a, q, st, nullptr, 1);
+  }
   if (!pk && env_int_tc("KMX_TC_PERSIST", 0) == 2 && tcp_ok(a.ma, a.mb, p)) {  // forced test path
     p.persist = 1; p.NW = 8; p.TPC = p.ntiles; p.nranges = 1;
     return launch_plan(a, p, st, nullptr, 1);
@@ -1329,6 +1376,7 @@ cudaError_t launch_plan(const MulArgs& a, const TcPlan& p, cudaStream_t st, cons
     fprintf(stderr, "kmx_tc: ma=%d mb=%d nprod=%d -> H=%d NW=%d KC=%d NB=%d TPC=%d ranges=%d nseg=%d smem=%zu cost=%.0f%s\n",
             a.ma, a.mb, a.nprod, p.H, p.NW, p.KC, p.NB, p.TPC, p.nranges, p.nseg, p.smem, p.cost,
             p.persist ? " persistent" : "");
+  if (p.swz && !pk) return launch_tcs(a, p.sp, st);
   if (p.persist && !pk) {
     // eligible only with bulk-copy-aligned operands (checked here, per launch)
     const bool swp = a.mb > a.ma;
@@ -1406,6 +1454,16 @@ bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]) {
     std::lock_guard<std::mutex> lk(g_tune_mu);
     auto it = g_tune.find(TuneKey{current_device(), ma, mb, nprod});
     if (it != g_tune.end()) p = it->second;
+  }
+  if (p.swz) {
+    out[0] = 4; out[1] = p.H; out[2] = 4; out[3] = p.KC; out[4] = 1;
+    out[5] = p.sp.mmas;
+    // per MMA the A tile (128 x 32 B) and B tile (N x 32 B) are read; per CTA the
+    // table (16 bytes per byte of b's chunk) and the a-window are written once
+    out[6] = p.sp.mmas * (4096LL + 32LL * p.swz) +
+             (long long)p.sp.ntiles * (16LL * 4 * (ma < mb ? ma : mb) + 127LL * p.swz + 4LL * (ma < mb ? ma : mb));
+    out[7] = 128LL * p.swz * 32 * p.sp.mmas;
+    return true;
   }
   switch (p.H) {
     case 1: tc_count<1>(ma, mb, p, out); break;

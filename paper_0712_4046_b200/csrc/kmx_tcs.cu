@@ -1,0 +1,412 @@
+// kmx_tcs.cu — K2 on the tensor cores without a per-K-step operand build:
+// the byte convolution c[k] = sum_j a[k-j] b[j] of two packed operands
+// (bignat.py:327-330, the classical product mul() reduces to) as
+// tcgen05.mma kind::i8 with
+//
+//   A = sliding windows over the RAW bytes of a.  The bytes are stored once,
+//       XOR-swizzled by their absolute shared-memory address, and read
+//       through a SWIZZLE_32B / 64B / 128B K-major descriptor: rows are
+//       PITCH = 32 / 64 / 128 bytes apart, so the M = 128 rows of one tile
+//       span 128 * PITCH byte positions, and stepping K by 32 bytes only moves
+//       the descriptor's start address (measured: the hardware swizzles on
+//       absolute address bits, base_offset = 0, any 32-byte-aligned start;
+//       tools/microbench/tc_swz.cu);
+//   B = N = PITCH shifted, reversed copies of b.  They are never built per
+//       K-step: ONE table of 8 byte phases
+//           T[x][r][i] = b[r + c - 8x - i],   r < 8, i < 16   (128 B per x)
+//       read with LBO = 256, SBO = 128 (SWIZZLE_NONE) makes row n = r + 8g,
+//       K-half q of K-step s the entry x = 4s + g + 2q -- linear in g and q,
+//       so a plain descriptor addresses it and consecutive K-steps advance
+//       the start by 512 bytes.  Row n then holds b[beta_n - u],
+//       beta_n = (n % 8) - 8 (n / 8) + N - 8: the N rows cover the N byte
+//       offsets between two A rows (in a permuted order the epilogue undoes).
+//
+// D[m][n] = c[k0 + PITCH m + beta_n]: TMEM lane m owns PITCH contiguous
+// byte positions = PITCH/4 product limbs, so the epilogue needs no
+// shared-memory transpose: limb sums from the lane's own columns, a local
+// carry chain, and one block scan of {0,1} carry maps.
+//
+// Compared with k_tcmul (kmx_tc.cu: 16H shifted copies rebuilt per K-step, N =
+// 16H <= 128 at 38H builder cycles per step) the table costs 16 bytes of
+// shared-memory writes per byte of b ONCE per CTA, N is 64 or 128 at no
+// extra build cost, and a c2 ks4 product (2436 x 2436 bytes) is one tile of
+// 79 MMAs instead of two tiles of 108.
+//
+// One CTA per (product, tile).  Long operands walk K in chunks of KS steps:
+// per chunk the CTA stages the a-window the tile needs (127 PITCH + 32 KS
+// bytes) and the table of that chunk of b; accumulation continues in TMEM.
+#include <cstdio>
+#include <cstdlib>
+
+#include "kmx_internal.h"
+#include "kmx_common.cuh"
+#include "kmx_tcutil.cuh"
+
+namespace kmx {
+
+namespace {
+
+template <int PITCH>
+struct SG {
+  static constexpr int N = PITCH;
+  static constexpr int T = 128 * PITCH;        // byte positions per tile
+  static constexpr int LIMBS = 32 * PITCH;     // product limbs per tile
+  static constexpr int LPT = PITCH / 4;        // limbs per TMEM lane
+  static constexpr int BPT = PITCH / 8;        // 256-limb bands per tile
+  static constexpr int AMAX = 127 * PITCH;     // offset of the last A row
+  static constexpr uint32_t LT = PITCH == 128 ? 2u : PITCH == 64 ? 4u : 6u;  // descriptor layout type
+  static constexpr uint32_t MASK = PITCH / 16 - 1;  // swizzle: address bits [4,4+B) ^= bits [7,7+B)
+  static constexpr uint32_t IDESC = (2u << 4) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+};
+
+struct TcsDims {
+  int La, Lb, ulo, S, ntiles;
+};
+template <int PITCH>
+__host__ __device__ inline TcsDims tcs_dims(int mA, int mB) {
+  TcsDims d;
+  d.La = 4 * mA;
+  d.Lb = 4 * mB;
+  d.ulo = -32 * ((d.Lb - 1 + 31) / 32);
+  d.S = fdiv32(SG<PITCH>::N - 1 - d.ulo) + 1;
+  d.ntiles = (d.La + d.Lb - 1 + SG<PITCH>::T - 1) / SG<PITCH>::T;
+  return d;
+}
+// K-steps [slo, shi) in which some row of tile t reads a byte of a
+template <int PITCH>
+__host__ __device__ inline void tcs_tile_steps(const TcsDims& d, int t, int& slo, int& shi) {
+  const int k0 = t * SG<PITCH>::T;
+  slo = -fdiv32(k0 + SG<PITCH>::AMAX + 31 + d.ulo);
+  if (slo < 0) slo = 0;
+  shi = fdiv32(d.La - k0 - 1 - d.ulo) + 1;
+  if (shi > d.S) shi = d.S;
+}
+
+struct TcsShared {
+  unsigned long long bar_mma;  // the chunk's MMAs completed (tcgen05.commit)
+  unsigned long long s_cout[4];
+  uint32_t tmem_base;
+  uint32_t warp_map[4];
+};
+
+__host__ __device__ inline size_t r128(size_t x) { return (x + 127) & ~(size_t)127; }
+__host__ __device__ inline size_t r1024(size_t x) { return (x + 1023) & ~(size_t)1023; }
+template <int PITCH>
+__host__ __device__ inline size_t tcs_abytes(int KS) { return r1024((size_t)SG<PITCH>::AMAX + 32 * KS + 64); }
+template <int PITCH>
+__host__ __device__ inline int tcs_rawbytes(int KS) { return (int)r128((size_t)32 * KS + PITCH + 64); }
+template <int PITCH>
+__host__ __device__ inline int tcs_entries(int KS) { return 4 * KS + PITCH / 8 + 2; }
+template <int PITCH>
+__host__ __device__ inline size_t tcs_smem(int KS) {
+  return 1024 + r128(sizeof(TcsShared)) + tcs_abytes<PITCH>(KS) + tcs_rawbytes<PITCH>(KS) +
+         (size_t)tcs_entries<PITCH>(KS) * 128;
+}
+
+struct TcsArgs {
+  MulArgs m;
+  int KS;      // K-steps per chunk
+  int ntiles;  // CTAs per product
+};
+
+__device__ __forceinline__ uint64_t sdesc_lt(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t lt) {
+  return sdesc(addr, lbo, sbo) | ((uint64_t)lt << 61);
+}
+
+template <int PITCH>
+__global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
+  using G = SG<PITCH>;
+  const MulArgs& a = ta.m;
+  extern __shared__ __align__(1024) unsigned char ssm_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int z = blockIdx.x / ta.ntiles, t = blockIdx.x % ta.ntiles;
+  unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
+  const int KS = ta.KS;
+  unsigned char* abuf = ssm;                                     // swizzled a-window
+  unsigned char* braw = abuf + tcs_abytes<PITCH>(KS);            // raw bytes of b's chunk
+  unsigned char* tab = braw + tcs_rawbytes<PITCH>(KS);           // phase table
+  TcsShared& sh = *reinterpret_cast<TcsShared*>(tab + (size_t)tcs_entries<PITCH>(KS) * 128);
+
+  // operand roles: a slides (longer), b goes through the table (shorter)
+  const bool sw = a.mb > a.ma;
+  const uint32_t* Ag = sw ? a.B + (long long)z * a.b_stride : a.A + (long long)z * a.a_stride;
+  const uint32_t* Bg = sw ? a.A + (long long)z * a.a_stride : a.B + (long long)z * a.b_stride;
+  const int mA = sw ? a.mb : a.ma, mB = sw ? a.ma : a.mb;
+  const TcsDims d = tcs_dims<PITCH>(mA, mB);
+  const int mp = a.ma + a.mb;
+  const int k0 = t * G::T;
+  int slo, shi;
+  tcs_tile_steps<PITCH>(d, t, slo, shi);
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
+                 "r"((uint32_t)G::N));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(smem_u32(&sh.bar_mma), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+
+  const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+  const uint32_t abase = smem_u32(abuf);
+  const int cc = G::N - 8 - d.ulo;  // T[x][r][i] = b[r + cc - 8x - i]
+  uint32_t tmem = 0u;
+  uint32_t phase = 0u;
+  bool first = true;
+  for (int sb = slo; sb < shi; sb += KS) {
+    const int se = min(shi, sb + KS);
+    if (!first) {
+      // the previous chunk's MMAs still read the buffers
+      mbar_wait(smem_u32(&sh.bar_mma), phase);
+      phase ^= 1u;
+    }
+    // ---- a-window: logical byte o of the region is a[aw0 + o]
+    {
+      const int aw0 = k0 + d.ulo + 32 * sb;  // multiple of 32
+      const int nq = (G::AMAX + 32 * (se - sb) + 15) / 16;
+      for (int q = tid; q < nq; q += 128) {
+        const int j = (aw0 + 16 * q) >> 2;  // first limb of the 16-byte chunk (aw0 may be negative: multiple of 4)
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (j + 3 >= 0 && j < mA) {
+          if (a16 && j >= 0 && j + 3 < mA) {
+            v = __ldg(reinterpret_cast<const uint4*>(Ag + j));
+          } else {
+            v.x = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
+            v.y = (j + 1 >= 0 && j + 1 < mA) ? __ldg(Ag + j + 1) : 0u;
+            v.z = (j + 2 >= 0 && j + 2 < mA) ? __ldg(Ag + j + 2) : 0u;
+            v.w = (j + 3 >= 0 && j + 3 < mA) ? __ldg(Ag + j + 3) : 0u;
+          }
+        }
+        const uint32_t L = abase + 16u * (uint32_t)q;
+        const uint32_t P = L ^ (((L >> 7) & G::MASK) << 4);
+        *reinterpret_cast<uint4*>(abuf + (P - abase)) = v;
+      }
+    }
+    // ---- raw bytes of b this chunk's table reads: braw[k] = b[jb + k],
+    // jb a multiple of 4 at or below the lowest index r + cc - 8x - i
+    const int x0 = 4 * sb, nx = 4 * (se - sb) + G::N / 8 - 2;  // entries x0 .. x0 + nx - 1 are read
+    const int jlo = cc - 8 * (x0 + nx - 1) - 15;
+    const int jb = (jlo >> 2) << 2;  // arithmetic shift: floor to a multiple of 4
+    {
+      const int nw = (7 + cc - 8 * x0 - jb) / 4 + 1;
+      uint32_t* bw = reinterpret_cast<uint32_t*>(braw);
+      for (int w = tid; w < nw; w += 128) {
+        const int j = (jb >> 2) + w;
+        bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
+      }
+    }
+    __syncthreads();
+    // ---- table: thread (r = tid % 8, run = tid / 8) builds entries x = x0 + run, + 16, ...
+    {
+      const int r = tid & 7, run = tid >> 3;
+      const uint32_t* bw = reinterpret_cast<const uint32_t*>(braw);
+      for (int xi = run; xi < nx; xi += 16) {
+        // chunk bytes i = 0..15: braw[e - i], e = r + cc - 8 (x0 + xi) - jb  (>= 15)
+        const int e = r + cc - 8 * (x0 + xi) - jb;
+        const int wq = e >> 2, sh2 = e & 3;
+        // bytes e, e-1, e-2, e-3 -> word 0 of the chunk, ...: from words wq-k and wq-k-1
+        const uint32_t w0 = bw[wq], w1 = bw[wq - 1], w2 = bw[wq - 2], w3 = bw[wq - 3], w4 = wq >= 4 ? bw[wq - 4] : 0u;
+        // selector: output byte 0 = byte sh2 of hi word, then descending through lo word
+        // __byte_perm(lo, hi, s): bytes 0-3 = lo, 4-7 = hi
+        const uint32_t s0 = (uint32_t)(4 + sh2), s1 = (uint32_t)(3 + sh2), s2 = (uint32_t)(2 + sh2), s3 = (uint32_t)(1 + sh2);
+        const uint32_t sel = s0 | (s1 << 4) | (s2 << 8) | (s3 << 12);
+        uint4 o;
+        o.x = __byte_perm(w1, w0, sel);
+        o.y = __byte_perm(w2, w1, sel);
+        o.z = __byte_perm(w3, w2, sel);
+        o.w = __byte_perm(w4, w3, sel);
+        *reinterpret_cast<uint4*>(tab + (size_t)xi * 128 + r * 16) = o;
+      }
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (first) tmem = sh.tmem_base;
+    if (tid == 0) {
+      uint64_t ad = sdesc_lt(abase, 16, 8 * PITCH, G::LT);
+      uint64_t bd = sdesc(smem_u32(tab), 256, 128);
+      uint32_t acc = first ? 0u : 1u;
+      for (int s = sb; s < se; s++) {
+        mma_i8(tmem, ad, bd, G::IDESC, acc);
+        acc = 1u;
+        ad += 2;   // + 32 bytes
+        bd += 32;  // + 512 bytes
+      }
+      mma_commit(smem_u32(&sh.bar_mma));
+    }
+    first = false;
+  }
+  if (!first) mbar_wait(smem_u32(&sh.bar_mma), phase);
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (first) {  // no K-step touches this tile (cannot happen for t < ntiles; kept for safety)
+    __syncthreads();
+    tmem = sh.tmem_base;
+  }
+
+  // ---- epilogue: lane m = tid owns limbs [LPT m, LPT m + LPT) of the tile
+  constexpr int LPT = G::LPT;
+  uint32_t dg[LPT];
+  unsigned long long x = 0ull;
+#pragma unroll
+  for (int c = 0; c < G::N / 16; c++) {
+    // limbs 4c .. 4c+3 live in columns [N - 16 - 16c, N - 16c): the upper 8
+    // columns (g odd) hold byte offsets 16c .. 16c+7, the lower 8 hold 16c+8 .. 16c+15
+    uint32_t v[16];
+    if (!first) {
+      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(G::N - 16 - 16 * c), v);
+    } else {
+#pragma unroll
+      for (int q = 0; q < 16; q++) v[q] = 0u;
+    }
+#pragma unroll
+    for (int q = 0; q < 4; q++) {
+      const int o = q < 2 ? 8 + 4 * q : 4 * (q - 2);
+      const unsigned long long ls = (unsigned long long)v[o] + ((unsigned long long)v[o + 1] << 8) +
+                                    ((unsigned long long)v[o + 2] << 16) + ((unsigned long long)v[o + 3] << 24);
+      x = (x >> 32) + ls;
+      dg[4 * c + q] = (uint32_t)x;
+    }
+  }
+  const unsigned long long cout = x >> 32;
+  unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
+  if (lane == 31) sh.s_cout[warp] = cout;
+  uint32_t ones = 0xFFFFFFFFu;
+#pragma unroll
+  for (int q = 1; q < LPT; q++) ones &= dg[q];
+  __syncthreads();
+  if (lane == 0) xin = warp ? sh.s_cout[warp - 1] : 0ull;
+  // overflow of (digits + xin + o) past the lane's LPT limbs, o in {0,1} from the previous lane
+  const unsigned long long s0 = (unsigned long long)dg[0] + xin;
+  const bool all1 = ones == 0xFFFFFFFFu;
+  const uint32_t gg = all1 && (s0 >> 32) != 0ull;
+  const uint32_t pp = all1 && ((s0 + 1ull) >> 32) != 0ull;
+  uint32_t F = gg | (pp << 1);
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
+    if (lane >= dd) F = cm2(F, y);
+  }
+  if (lane == 31) sh.warp_map[warp] = F;
+  __syncthreads();
+  uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
+  uint32_t Wm = CM2_ID;
+  for (int w = 0; w < warp; w++) Wm = cm2(sh.warp_map[w], Wm);
+  // the tile's carry-in is 0: evaluate the composed maps at 0
+  E = lane ? cm2(E, Wm) : Wm;
+  const uint32_t Fin = cm2(F, Wm);
+  unsigned long long acc = s0 + (E & 1u);
+  dg[0] = (uint32_t)acc;
+#pragma unroll
+  for (int q = 1; q < LPT; q++) {
+    acc = (acc >> 32) + dg[q];
+    dg[q] = (uint32_t)acc;
+  }
+  uint32_t* Pz = a.P + (long long)z * a.p_stride;
+  const int L = t * G::LIMBS + LPT * tid;
+  if (L + LPT <= mp) {
+#pragma unroll
+    for (int q = 0; q < LPT / 4; q++)
+      *reinterpret_cast<uint4*>(Pz + L + 4 * q) = make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < LPT; q++)
+      if (L + q < mp) Pz[L + q] = dg[q];
+  }
+  // band spills: zero inside the tile, the tile's carry on its top band
+  {
+    const int b0 = G::BPT * t, b1 = min(a.nbands, G::BPT * (t + 1));
+    if (tid < b1 - b0 && tid != G::BPT - 1) {
+      unsigned long long* sp = a.spill + ((long long)z * a.nbands + b0 + tid) * 2;
+      sp[0] = 0ull;
+      sp[1] = 0ull;
+    }
+    if (tid == 127 && b0 + G::BPT - 1 < b1) {
+      unsigned long long* sp = a.spill + ((long long)z * a.nbands + b0 + G::BPT - 1) * 2;
+      sp[0] = cout + (Fin & 1u);
+      sp[1] = 0ull;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)G::N));
+}
+
+int tcs_env(const char* n, int dflt) {
+  const char* v = getenv(n);
+  return v && *v ? atoi(v) : dflt;
+}
+
+template <int PITCH>
+bool tcs_plan_p(int ma, int mb, TcsPlan& p) {
+  const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
+  if (mB < 1) return false;
+  const TcsDims d = tcs_dims<PITCH>(mA, mB);
+  if (d.Lb > 65536) return false;  // u32 accumulators: at most 65536 byte products of < 2^16 per sum
+  int ksmax = tcs_env("KMX_TCS_KS", 128);
+  if (ksmax < 8) ksmax = 8;
+  if (ksmax > 256) ksmax = 256;
+  const int nch = (d.S + ksmax - 1) / ksmax;
+  int KS = (d.S + nch - 1) / nch;
+  p.pitch = PITCH;
+  p.KS = KS;
+  p.ntiles = d.ntiles;
+  p.smem = tcs_smem<PITCH>(KS);
+  long long mmas = 0;
+  for (int t = 0; t < d.ntiles; t++) {
+    int slo, shi;
+    tcs_tile_steps<PITCH>(d, t, slo, shi);
+    if (shi > slo) mmas += shi - slo;
+  }
+  p.mmas = mmas;
+  // modelled SM cycles per product: shared-memory operand reads at ~110 B/clk,
+  // never below the tensor floor
+  const double per = (4096.0 + 32.0 * PITCH) / 110.0;
+  const double fl = 128.0 * PITCH * 32 / 8192.0;
+  p.cost = (double)mmas * (per > fl ? per : fl);
+  return p.smem <= 200 * 1024;
+}
+
+template <int PITCH>
+cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
+  static size_t s_set = 0;
+  if (p.smem > 48 * 1024 && p.smem > s_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_tcswz<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e != cudaSuccess) return e;
+    s_set = p.smem;
+  }
+  TcsArgs ta;
+  ta.m = a;
+  ta.KS = p.KS;
+  ta.ntiles = p.ntiles;
+  const long long grid = (long long)a.nprod * p.ntiles;
+  k_tcswz<PITCH><<<(unsigned)grid, 128, p.smem, st>>>(ta);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tcs_plan(int ma, int mb, int pitch, TcsPlan& p) {
+  switch (pitch) {
+    case 32: return tcs_plan_p<32>(ma, mb, p);
+    case 64: return tcs_plan_p<64>(ma, mb, p);
+    case 128: return tcs_plan_p<128>(ma, mb, p);
+    default: return false;
+  }
+}
+
+cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
+  if (a.nprod == 0) return cudaSuccess;
+  if (tcs_env("KMX_TC_VERBOSE", 0))
+    fprintf(stderr, "kmx_tcs: ma=%d mb=%d nprod=%d -> pitch=%d KS=%d tiles=%d smem=%zu mmas=%lld\n", a.ma, a.mb, a.nprod,
+            p.pitch, p.KS, p.ntiles, p.smem, p.mmas);
+  switch (p.pitch) {
+    case 32: return launch_p<32>(a, p, st);
+    case 64: return launch_p<64>(a, p, st);
+    default: return launch_p<128>(a, p, st);
+  }
+}
+
+}  // namespace kmx
