@@ -75,11 +75,12 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk =
 // MulArgs contract; pitch = 32 / 64 / 128 (= the MMA's N).
 struct TcsPlan {
   int pitch, KS, ntiles;
+  int persist, NS;  // the persistent warp-specialized form and its operand stages
   size_t smem;
   long long mmas;  // MMAs per product
   double cost;     // modelled SM cycles per product
 };
-bool tcs_plan(int ma, int mb, int pitch, TcsPlan& p);
+bool tcs_plan(int ma, int mb, int pitch, int persist, TcsPlan& p);
 cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st);
 double measure_tc_peak(int iters);
 double measure_tc_peak_shape(int n, int iters);

@@ -886,6 +886,12 @@ int tcs_mode() {
   const char* v = getenv("KMX_TCS");
   return v && *v ? atoi(v) : -1;
 }
+// KMX_TCS_PERSIST: -1 (default) both forms are tuner candidates; 0 one-shot
+// CTAs only; 1 the persistent form only (wherever its plan exists).
+int tcs_persist_mode() {
+  const char* v = getenv("KMX_TCS_PERSIST");
+  return v && *v ? atoi(v) : -1;
+}
 // the swizzled-window plan of lowest modelled cost (or the forced pitch)
 bool tcs_best(int ma, int mb, TcPlan& out) {
   const int mode = tcs_mode();
@@ -894,7 +900,7 @@ bool tcs_best(int ma, int mb, TcPlan& out) {
   for (int pitch : {32, 64, 128}) {
     if (mode >= 32 && mode != pitch) continue;
     TcsPlan sp;
-    if (!tcs_plan(ma, mb, pitch, sp)) continue;
+    if (!(tcs_persist_mode() == 1 && tcs_plan(ma, mb, pitch, 1, sp)) && !tcs_plan(ma, mb, pitch, 0, sp)) continue;
     if (!ok || sp.cost < out.sp.cost) {
       out = TcPlan();
       out.swz = pitch;
@@ -1180,11 +1186,13 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
   }
   std::vector<TcPlan> out;
   if (tcs_mode() != 0)
+    for (int form = 0; form < 2; form++)
     for (int pitch : {32, 64, 128}) {
       if (tcs_mode() >= 32 && tcs_mode() != pitch) continue;
+      if (tcs_persist_mode() >= 0 && tcs_persist_mode() != form) continue;
       TcPlan q;
       q.sp = TcsPlan();
-      if (!tcs_plan(ma, mb, pitch, q.sp)) continue;
+      if (!tcs_plan(ma, mb, pitch, form, q.sp)) continue;
       q.swz = pitch;
       q.H = pitch / 16; q.NW = 4; q.KC = q.sp.KS; q.NB = 1; q.TPC = 1;
       q.nranges = q.sp.ntiles; q.ntiles = q.sp.ntiles; q.nseg = 1;
@@ -1290,7 +1298,8 @@ bool tc_tuned_plan(const MulArgs& a, cudaStream_t st, TcPlan& p, bool* launched)
   }
   if (env_int_tc("KMX_TC_VERBOSE", 0))
     fprintf(stderr, "kmx_tc autotune: ma=%d mb=%d nprod=%d -> %s H=%d NW=%d KC=%d (%.4f ms of %zu candidates)\n", a.ma,
-            a.mb, a.nprod, p.swz ? "swizzled-window" : "tiled", p.H, p.NW, p.KC, best_ms, cands.size());
+            a.mb, a.nprod, p.swz ? (p.sp.persist ? "swizzled-window persistent" : "swizzled-window") : "tiled", p.H, p.NW,
+            p.KC, best_ms, cands.size());
   // re-run the winner last so the buffers hold its (identical) output in order
   if (launch_plan(a, p, st, nullptr, 1) != cudaSuccess) return false;
   *launched = true;

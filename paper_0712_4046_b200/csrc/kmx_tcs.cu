@@ -37,6 +37,7 @@
 // bytes) and the table of that chunk of b; accumulation continues in TMEM.
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "kmx_internal.h"
 #include "kmx_common.cuh"
@@ -94,7 +95,7 @@ __host__ __device__ inline size_t r1024(size_t x) { return (x + 1023) & ~(size_t
 template <int PITCH>
 __host__ __device__ inline size_t tcs_abytes(int KS) { return r1024((size_t)SG<PITCH>::AMAX + 32 * KS + 64); }
 template <int PITCH>
-__host__ __device__ inline int tcs_rawbytes(int KS) { return (int)r128((size_t)32 * KS + PITCH + 64); }
+__host__ __device__ inline int tcs_rawbytes(int KS) { return (int)r128((size_t)32 * KS + PITCH + 96); }
 template <int PITCH>
 __host__ __device__ inline int tcs_entries(int KS) { return 4 * KS + PITCH / 8 + 2; }
 template <int PITCH>
@@ -103,14 +104,111 @@ __host__ __device__ inline size_t tcs_smem(int KS) {
          (size_t)tcs_entries<PITCH>(KS) * 128;
 }
 
+constexpr int TCS_MAXT = 48;  // tiles per product the persistent kernel orders
 struct TcsArgs {
   MulArgs m;
   int KS;      // K-steps per chunk
   int ntiles;  // CTAs per product
+  int NS;      // persistent kernel: operand stages in the ring
+  unsigned char order[TCS_MAXT];  // persistent kernel: tiles by descending K-steps
 };
 
 __device__ __forceinline__ uint64_t sdesc_lt(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t lt) {
   return sdesc(addr, lbo, sbo) | ((uint64_t)lt << 61);
+}
+
+
+// One K-chunk's operands for tile k0: the swizzled a-window, the raw bytes of
+// b's chunk and its phase table.  128 threads (ptid); BAR = 0: __syncthreads
+// between the raw bytes and the table, else the named barrier BAR.
+template <int PITCH, int BAR>
+__device__ __forceinline__ void tcs_build(unsigned char* abuf, unsigned char* braw, unsigned char* tab,
+                                          const uint32_t* __restrict__ Ag, const uint32_t* __restrict__ Bg, int mA,
+                                          int mB, bool a16, const TcsDims& d, int k0, int sb, int se, int ptid) {
+  using G = SG<PITCH>;
+  const uint32_t abase = smem_u32(abuf);
+  const int cc = G::N - 8 - d.ulo;  // T[x][r][i] = b[r + cc - 8x - i]
+  // ---- a-window: logical byte o of the region is a[aw0 + o]
+  {
+    const int aw0 = k0 + d.ulo + 32 * sb;  // multiple of 32
+    const int nq = (G::AMAX + 32 * (se - sb) + 15) / 16;
+    for (int q0 = 0; q0 < nq; q0 += 4 * 128) {
+      uint4 v[4];
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int q = q0 + 128 * k + ptid;
+        const int j = (aw0 + 16 * q) >> 2;  // first limb of the 16-byte chunk (a multiple of 4, may be negative)
+        v[k] = make_uint4(0u, 0u, 0u, 0u);
+        if (q < nq && j + 3 >= 0 && j < mA) {
+          if (a16 && j >= 0 && j + 3 < mA) {
+            v[k] = __ldg(reinterpret_cast<const uint4*>(Ag + j));
+          } else {
+            v[k].x = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
+            v[k].y = (j + 1 >= 0 && j + 1 < mA) ? __ldg(Ag + j + 1) : 0u;
+            v[k].z = (j + 2 >= 0 && j + 2 < mA) ? __ldg(Ag + j + 2) : 0u;
+            v[k].w = (j + 3 >= 0 && j + 3 < mA) ? __ldg(Ag + j + 3) : 0u;
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; k++) {
+        const int q = q0 + 128 * k + ptid;
+        if (q < nq) {
+          const uint32_t L = abase + 16u * (uint32_t)q;
+          const uint32_t P = L ^ (((L >> 7) & G::MASK) << 4);
+          *reinterpret_cast<uint4*>(abuf + (P - abase)) = v[k];
+        }
+      }
+    }
+  }
+  // ---- raw bytes of b this chunk's table reads: braw[k] = b[jb + k],
+  // jb a multiple of 4 at or below the lowest index r + cc - 8x - i
+  const int x0 = 4 * sb, nx = 4 * (se - sb) + G::N / 8 - 2;  // entries x0 .. x0 + nx - 1 are read
+  const int jlo = cc - 8 * (x0 + nx - 1) - 15;
+  const int jb = ((jlo >> 2) << 2) - 16;  // floor to a multiple of 4, four spare words below (the sliding window's trailing loads)
+  {
+    const int nw = (7 + cc - 8 * x0 - jb) / 4 + 1;
+    uint32_t* bw = reinterpret_cast<uint32_t*>(braw);
+    for (int w = ptid; w < nw; w += 128) {
+      const int j = (jb >> 2) + w;
+      bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
+    }
+  }
+  if (BAR == 0) __syncthreads();
+  else asm volatile("bar.sync %0, 128;" ::"n"(BAR) : "memory");
+  // ---- table: thread (r = ptid % 8, run = ptid / 8) builds a contiguous run
+  // of entries; consecutive entries move the 16-byte window down by 8 bytes,
+  // so five words slide through registers with two new loads per entry
+  {
+    const int r = ptid & 7, run = ptid >> 3;
+    const int XB = (nx + 15) / 16;
+    const int xa = run * XB, xe = min(nx, xa + XB);
+    if (xa < xe) {
+      const uint32_t* bw = reinterpret_cast<const uint32_t*>(braw);
+      // entry bytes i = 0..15: braw[e - i], e = r + cc - 8 (x0 + x) - jb  (>= 15 + 8)
+      const int e = r + cc - 8 * (x0 + xa) - jb;
+      int wq = e >> 2;
+      const int sh2 = e & 3;
+      // output byte k of a word = byte (4 + sh2 - k) of {lo, hi}
+      const uint32_t sel = (uint32_t)(4 + sh2) | ((uint32_t)(3 + sh2) << 4) | ((uint32_t)(2 + sh2) << 8) |
+                           ((uint32_t)(1 + sh2) << 12);
+      uint32_t w0 = bw[wq], w1 = bw[wq - 1], w2 = bw[wq - 2], w3 = bw[wq - 3], w4 = bw[wq - 4];
+      unsigned char* dst = tab + (size_t)xa * 128 + r * 16;
+      for (int x = xa; x < xe; x++) {
+        uint4 o;
+        o.x = __byte_perm(w1, w0, sel);
+        o.y = __byte_perm(w2, w1, sel);
+        o.z = __byte_perm(w3, w2, sel);
+        o.w = __byte_perm(w4, w3, sel);
+        *reinterpret_cast<uint4*>(dst) = o;
+        dst += 128;
+        wq -= 2;
+        w0 = w2; w1 = w3; w2 = w4;
+        w3 = bw[wq - 3];
+        w4 = bw[wq - 4];
+      }
+    }
+  }
 }
 
 template <int PITCH>
@@ -150,7 +248,6 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
 
   const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
   const uint32_t abase = smem_u32(abuf);
-  const int cc = G::N - 8 - d.ulo;  // T[x][r][i] = b[r + cc - 8x - i]
   uint32_t tmem = 0u;
   uint32_t phase = 0u;
   bool first = true;
@@ -161,64 +258,7 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
       mbar_wait(smem_u32(&sh.bar_mma), phase);
       phase ^= 1u;
     }
-    // ---- a-window: logical byte o of the region is a[aw0 + o]
-    {
-      const int aw0 = k0 + d.ulo + 32 * sb;  // multiple of 32
-      const int nq = (G::AMAX + 32 * (se - sb) + 15) / 16;
-      for (int q = tid; q < nq; q += 128) {
-        const int j = (aw0 + 16 * q) >> 2;  // first limb of the 16-byte chunk (aw0 may be negative: multiple of 4)
-        uint4 v = make_uint4(0u, 0u, 0u, 0u);
-        if (j + 3 >= 0 && j < mA) {
-          if (a16 && j >= 0 && j + 3 < mA) {
-            v = __ldg(reinterpret_cast<const uint4*>(Ag + j));
-          } else {
-            v.x = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
-            v.y = (j + 1 >= 0 && j + 1 < mA) ? __ldg(Ag + j + 1) : 0u;
-            v.z = (j + 2 >= 0 && j + 2 < mA) ? __ldg(Ag + j + 2) : 0u;
-            v.w = (j + 3 >= 0 && j + 3 < mA) ? __ldg(Ag + j + 3) : 0u;
-          }
-        }
-        const uint32_t L = abase + 16u * (uint32_t)q;
-        const uint32_t P = L ^ (((L >> 7) & G::MASK) << 4);
-        *reinterpret_cast<uint4*>(abuf + (P - abase)) = v;
-      }
-    }
-    // ---- raw bytes of b this chunk's table reads: braw[k] = b[jb + k],
-    // jb a multiple of 4 at or below the lowest index r + cc - 8x - i
-    const int x0 = 4 * sb, nx = 4 * (se - sb) + G::N / 8 - 2;  // entries x0 .. x0 + nx - 1 are read
-    const int jlo = cc - 8 * (x0 + nx - 1) - 15;
-    const int jb = (jlo >> 2) << 2;  // arithmetic shift: floor to a multiple of 4
-    {
-      const int nw = (7 + cc - 8 * x0 - jb) / 4 + 1;
-      uint32_t* bw = reinterpret_cast<uint32_t*>(braw);
-      for (int w = tid; w < nw; w += 128) {
-        const int j = (jb >> 2) + w;
-        bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
-      }
-    }
-    __syncthreads();
-    // ---- table: thread (r = tid % 8, run = tid / 8) builds entries x = x0 + run, + 16, ...
-    {
-      const int r = tid & 7, run = tid >> 3;
-      const uint32_t* bw = reinterpret_cast<const uint32_t*>(braw);
-      for (int xi = run; xi < nx; xi += 16) {
-        // chunk bytes i = 0..15: braw[e - i], e = r + cc - 8 (x0 + xi) - jb  (>= 15)
-        const int e = r + cc - 8 * (x0 + xi) - jb;
-        const int wq = e >> 2, sh2 = e & 3;
-        // bytes e, e-1, e-2, e-3 -> word 0 of the chunk, ...: from words wq-k and wq-k-1
-        const uint32_t w0 = bw[wq], w1 = bw[wq - 1], w2 = bw[wq - 2], w3 = bw[wq - 3], w4 = wq >= 4 ? bw[wq - 4] : 0u;
-        // selector: output byte 0 = byte sh2 of hi word, then descending through lo word
-        // __byte_perm(lo, hi, s): bytes 0-3 = lo, 4-7 = hi
-        const uint32_t s0 = (uint32_t)(4 + sh2), s1 = (uint32_t)(3 + sh2), s2 = (uint32_t)(2 + sh2), s3 = (uint32_t)(1 + sh2);
-        const uint32_t sel = s0 | (s1 << 4) | (s2 << 8) | (s3 << 12);
-        uint4 o;
-        o.x = __byte_perm(w1, w0, sel);
-        o.y = __byte_perm(w2, w1, sel);
-        o.z = __byte_perm(w3, w2, sel);
-        o.w = __byte_perm(w4, w3, sel);
-        *reinterpret_cast<uint4*>(tab + (size_t)xi * 128 + r * 16) = o;
-      }
-    }
+    tcs_build<PITCH, 0>(abuf, braw, tab, Ag, Bg, mA, mB, a16, d, k0, sb, se, tid);
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
@@ -334,13 +374,248 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)G::N));
 }
 
+
+// ------------------------------------------------- persistent, specialized
+// The same tiles through a persistent CTA (one per SM): work items (product,
+// tile) in a static round-robin, heaviest tile class first, with the warps
+// specialized and every hand-off on an mbarrier:
+//   warps 0-3  epilogue of item i from TMEM accumulator i & 1 (lane quarter =
+//              warp) while the MMAs of item i+1 fill the other accumulator;
+//   warps 4-7  producers: the a-window, b's raw bytes and the phase table of
+//              the next K-chunk into stage sc % NS of the operand ring;
+//   warp 8     lane 0 issues the MMAs of each full stage and commits the
+//              stage back to the producers.
+// One product's operand build, MMAs and epilogue overlap its neighbours', and
+// the K-chunks of long products are built while the previous chunk's MMAs run.
+struct TcsSharedP {
+  unsigned long long bar_full[4];       // stage built (128 producer threads arrive)
+  unsigned long long bar_empty[4];      // the MMAs that read the stage completed (commit)
+  unsigned long long bar_acc_full[2];   // the item's MMAs completed (commit)
+  unsigned long long bar_acc_empty[2];  // the epilogue drained the accumulator (128 threads)
+  unsigned long long s_cout[4];
+  uint32_t tmem_base;
+  uint32_t warp_map[4];
+};
+template <int PITCH>
+__host__ __device__ inline size_t tcs_stage_bytes(int KS) {
+  return tcs_abytes<PITCH>(KS) + tcs_rawbytes<PITCH>(KS) + r1024((size_t)tcs_entries<PITCH>(KS) * 128);
+}
+template <int PITCH>
+__host__ __device__ inline size_t tcsp_smem(int KS, int NS) {
+  return 1024 + (size_t)NS * tcs_stage_bytes<PITCH>(KS) + r128(sizeof(TcsSharedP));
+}
+
+template <int PITCH>
+__global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
+  using G = SG<PITCH>;
+  const MulArgs& a = ta.m;
+  extern __shared__ __align__(1024) unsigned char ssm_raw[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
+  const int KS = ta.KS, NS = ta.NS;
+  const size_t stage_bytes = tcs_stage_bytes<PITCH>(KS);
+  TcsSharedP& sh = *reinterpret_cast<TcsSharedP*>(ssm + (size_t)NS * stage_bytes);
+  const bool sw = a.mb > a.ma;
+  const int mA = sw ? a.mb : a.ma, mB = sw ? a.ma : a.mb;
+  const long long astr = sw ? a.b_stride : a.a_stride, bstr = sw ? a.a_stride : a.b_stride;
+  const uint32_t* Abase = sw ? a.B : a.A;
+  const uint32_t* Bbase = sw ? a.A : a.B;
+  const TcsDims d = tcs_dims<PITCH>(mA, mB);
+  const int mp = a.ma + a.mb;
+  const long long nitems = (long long)a.nprod * ta.ntiles;
+  constexpr uint32_t COLS = 2 * G::N < 32 ? 32 : 2 * G::N;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
+                 "r"(COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    for (int i = 0; i < 4; i++) {
+      mbar_init(smem_u32(&sh.bar_full[i]), 128);
+      mbar_init(smem_u32(&sh.bar_empty[i]), 1);
+    }
+    for (int i = 0; i < 2; i++) {
+      mbar_init(smem_u32(&sh.bar_acc_full[i]), 1);
+      mbar_init(smem_u32(&sh.bar_acc_empty[i]), 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = sh.tmem_base;
+
+  if (warp >= 4 && warp < 8) {
+    // ---------------- producers
+    const int ptid = tid - 128;
+    long long sc = 0;
+    for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
+      const int t = ta.order[it / a.nprod];
+      const long long z = it % a.nprod;
+      const uint32_t* Ag = Abase + z * astr;
+      const uint32_t* Bg = Bbase + z * bstr;
+      const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+      int slo, shi;
+      tcs_tile_steps<PITCH>(d, t, slo, shi);
+      for (int sb = slo; sb < shi; sb += KS, sc++) {
+        const int st = (int)(sc % NS);
+        if (sc >= NS) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((sc / NS) - 1) & 1));
+        unsigned char* abuf = ssm + (size_t)st * stage_bytes;
+        unsigned char* braw = abuf + tcs_abytes<PITCH>(KS);
+        unsigned char* tab = braw + tcs_rawbytes<PITCH>(KS);
+        tcs_build<PITCH, 1>(abuf, braw, tab, Ag, Bg, mA, mB, a16, d, t * G::T, sb, min(shi, sb + KS), ptid);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(smem_u32(&sh.bar_full[st]));
+      }
+    }
+  } else if (warp == 8) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      long long sc = 0, ac = 0;
+      for (long long it = blockIdx.x; it < nitems; it += gridDim.x, ac++) {
+        const int t = ta.order[it / a.nprod];
+        int slo, shi;
+        tcs_tile_steps<PITCH>(d, t, slo, shi);
+        const int buf = (int)(ac & 1);
+        if (ac >= 2) mbar_wait(smem_u32(&sh.bar_acc_empty[buf]), (uint32_t)(((ac >> 1) - 1) & 1));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t dcol = tmem + (uint32_t)(buf * G::N);
+        uint32_t acc = 0u;
+        for (int sb = slo; sb < shi; sb += KS, sc++) {
+          const int st = (int)(sc % NS);
+          mbar_wait(smem_u32(&sh.bar_full[st]), (uint32_t)((sc / NS) & 1));
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          const uint32_t sbase = smem_u32(ssm + (size_t)st * stage_bytes);
+          uint64_t ad = sdesc_lt(sbase, 16, 8 * PITCH, G::LT);
+          uint64_t bd = sdesc(sbase + (uint32_t)(tcs_abytes<PITCH>(KS) + tcs_rawbytes<PITCH>(KS)), 256, 128);
+          const int se = min(shi, sb + KS);
+          for (int s = sb; s < se; s++) {
+            mma_i8(dcol, ad, bd, G::IDESC, acc);
+            acc = 1u;
+            ad += 2;   // + 32 bytes
+            bd += 32;  // + 512 bytes
+          }
+          mma_commit(smem_u32(&sh.bar_empty[st]));
+        }
+        mma_commit(smem_u32(&sh.bar_acc_full[buf]));
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (warps 0-3: TMEM lane quarter = warp)
+    constexpr int LPT = G::LPT;
+    long long ac = 0;
+    for (long long it = blockIdx.x; it < nitems; it += gridDim.x, ac++) {
+      const int t = ta.order[it / a.nprod];
+      const long long z = it % a.nprod;
+      int slo, shi;
+      tcs_tile_steps<PITCH>(d, t, slo, shi);
+      const int buf = (int)(ac & 1);
+      mbar_wait(smem_u32(&sh.bar_acc_full[buf]), (uint32_t)((ac >> 1) & 1));
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      uint32_t dg[LPT];
+      unsigned long long x = 0ull;
+#pragma unroll
+      for (int c = 0; c < G::N / 16; c++) {
+        uint32_t v[16];
+        if (slo < shi) {
+          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(buf * G::N + G::N - 16 - 16 * c), v);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; q++) v[q] = 0u;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int o = q < 2 ? 8 + 4 * q : 4 * (q - 2);
+          const unsigned long long ls = (unsigned long long)v[o] + ((unsigned long long)v[o + 1] << 8) +
+                                        ((unsigned long long)v[o + 2] << 16) + ((unsigned long long)v[o + 3] << 24);
+          x = (x >> 32) + ls;
+          dg[4 * c + q] = (uint32_t)x;
+        }
+      }
+      // the accumulator is in registers: hand it back to the MMA warp
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      mbar_arrive(smem_u32(&sh.bar_acc_empty[buf]));
+      const unsigned long long cout = x >> 32;
+      unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
+      if (lane == 31) sh.s_cout[warp] = cout;
+      uint32_t ones = 0xFFFFFFFFu;
+#pragma unroll
+      for (int q = 1; q < LPT; q++) ones &= dg[q];
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      if (lane == 0) xin = warp ? sh.s_cout[warp - 1] : 0ull;
+      const unsigned long long s0 = (unsigned long long)dg[0] + xin;
+      const bool all1 = ones == 0xFFFFFFFFu;
+      const uint32_t gg = all1 && (s0 >> 32) != 0ull;
+      const uint32_t pp = all1 && ((s0 + 1ull) >> 32) != 0ull;
+      uint32_t F = gg | (pp << 1);
+#pragma unroll
+      for (int dd = 1; dd < 32; dd <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
+        if (lane >= dd) F = cm2(F, y);
+      }
+      if (lane == 31) sh.warp_map[warp] = F;
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
+      uint32_t Wm = CM2_ID;
+      for (int w = 0; w < warp; w++) Wm = cm2(sh.warp_map[w], Wm);
+      E = lane ? cm2(E, Wm) : Wm;
+      const uint32_t Fin = cm2(F, Wm);
+      unsigned long long acc = s0 + (E & 1u);
+      dg[0] = (uint32_t)acc;
+#pragma unroll
+      for (int q = 1; q < LPT; q++) {
+        acc = (acc >> 32) + dg[q];
+        dg[q] = (uint32_t)acc;
+      }
+      uint32_t* Pz = a.P + z * a.p_stride;
+      const int L = t * G::LIMBS + LPT * tid;
+      if (L + LPT <= mp) {
+#pragma unroll
+        for (int q = 0; q < LPT / 4; q++)
+          *reinterpret_cast<uint4*>(Pz + L + 4 * q) = make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < LPT; q++)
+          if (L + q < mp) Pz[L + q] = dg[q];
+      }
+      const int b0 = G::BPT * t, b1 = min(a.nbands, G::BPT * (t + 1));
+      if (tid < b1 - b0 && tid != G::BPT - 1) {
+        unsigned long long* sp = a.spill + (z * a.nbands + b0 + tid) * 2;
+        sp[0] = 0ull;
+        sp[1] = 0ull;
+      }
+      if (tid == 127 && b0 + G::BPT - 1 < b1) {
+        unsigned long long* sp = a.spill + (z * a.nbands + b0 + G::BPT - 1) * 2;
+        sp[0] = cout + (Fin & 1u);
+        sp[1] = 0ull;
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(COLS));
+}
+
 int tcs_env(const char* n, int dflt) {
   const char* v = getenv(n);
   return v && *v ? atoi(v) : dflt;
 }
 
+int tcs_num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
 template <int PITCH>
-bool tcs_plan_p(int ma, int mb, TcsPlan& p) {
+bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
   if (mB < 1) return false;
   const TcsDims d = tcs_dims<PITCH>(mA, mB);
@@ -348,12 +623,25 @@ bool tcs_plan_p(int ma, int mb, TcsPlan& p) {
   int ksmax = tcs_env("KMX_TCS_KS", 128);
   if (ksmax < 8) ksmax = 8;
   if (ksmax > 256) ksmax = 256;
+  p.persist = persist;
+  p.NS = 0;
+  if (persist) {
+    if (d.ntiles > TCS_MAXT) return false;
+    // three stages of the largest chunk that fits (two when one chunk is the whole K span)
+    int NS = tcs_env("KMX_TCS_NS", 3);
+    if (NS < 2) NS = 2;
+    if (NS > 4) NS = 4;
+    const size_t cap = 200 * 1024;
+    while (ksmax > 8 && tcsp_smem<PITCH>(d.S < ksmax ? d.S : ksmax, NS) > cap) ksmax -= 8;
+    if (tcsp_smem<PITCH>(d.S < ksmax ? d.S : ksmax, NS) > cap) return false;
+    p.NS = NS;
+  }
   const int nch = (d.S + ksmax - 1) / ksmax;
-  int KS = (d.S + nch - 1) / nch;
+  const int KS = (d.S + nch - 1) / nch;
   p.pitch = PITCH;
   p.KS = KS;
   p.ntiles = d.ntiles;
-  p.smem = tcs_smem<PITCH>(KS);
+  p.smem = persist ? tcsp_smem<PITCH>(KS, p.NS) : tcs_smem<PITCH>(KS);
   long long mmas = 0;
   for (int t = 0; t < d.ntiles; t++) {
     int slo, shi;
@@ -371,16 +659,53 @@ bool tcs_plan_p(int ma, int mb, TcsPlan& p) {
 
 template <int PITCH>
 cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
-  static size_t s_set = 0;
-  if (p.smem > 48 * 1024 && p.smem > s_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_tcswz<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
-    if (e != cudaSuccess) return e;
-    s_set = p.smem;
-  }
   TcsArgs ta;
+  memset(&ta, 0, sizeof ta);
   ta.m = a;
   ta.KS = p.KS;
   ta.ntiles = p.ntiles;
+  ta.NS = p.NS;
+  if (p.persist) {
+    static size_t s_set = 0;
+    if (p.smem > 48 * 1024 && p.smem > s_set) {
+      cudaError_t e = cudaFuncSetAttribute(k_tcswz_p<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      if (e != cudaSuccess) return e;
+      s_set = p.smem;
+    }
+    // tiles by descending K-steps: the round-robin hands every CTA the same mix
+    const int mA = a.ma > a.mb ? a.ma : a.mb, mB = a.ma > a.mb ? a.mb : a.ma;
+    const TcsDims d = tcs_dims<PITCH>(mA, mB);
+    int steps[TCS_MAXT];
+    for (int t = 0; t < p.ntiles; t++) {
+      int slo, shi;
+      tcs_tile_steps<PITCH>(d, t, slo, shi);
+      steps[t] = shi - slo;
+      ta.order[t] = (unsigned char)t;
+    }
+    for (int i = 1; i < p.ntiles; i++)
+      for (int j = i; j > 0 && steps[ta.order[j]] > steps[ta.order[j - 1]]; j--) {
+        const unsigned char x = ta.order[j];
+        ta.order[j] = ta.order[j - 1];
+        ta.order[j - 1] = x;
+      }
+    int per_sm = (int)((220 * 1024) / (p.smem + 1024));
+    const int by_tmem = 512 / (2 * PITCH < 32 ? 32 : 2 * PITCH);
+    if (per_sm > by_tmem) per_sm = by_tmem;
+    if (per_sm < 1) per_sm = 1;
+    const int cps = tcs_env("KMX_TCS_CPS", 0);
+    if (cps > 0 && cps < per_sm) per_sm = cps;
+    long long grid = (long long)tcs_num_sms() * per_sm;
+    const long long nitems = (long long)a.nprod * p.ntiles;
+    if (grid > nitems) grid = nitems;
+    k_tcswz_p<PITCH><<<(unsigned)grid, 288, p.smem, st>>>(ta);
+    return cudaGetLastError();
+  }
+  static size_t s_set1 = 0;
+  if (p.smem > 48 * 1024 && p.smem > s_set1) {
+    cudaError_t e = cudaFuncSetAttribute(k_tcswz<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    if (e != cudaSuccess) return e;
+    s_set1 = p.smem;
+  }
   const long long grid = (long long)a.nprod * p.ntiles;
   k_tcswz<PITCH><<<(unsigned)grid, 128, p.smem, st>>>(ta);
   return cudaGetLastError();
@@ -388,11 +713,11 @@ cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
 
 }  // namespace
 
-bool tcs_plan(int ma, int mb, int pitch, TcsPlan& p) {
+bool tcs_plan(int ma, int mb, int pitch, int persist, TcsPlan& p) {
   switch (pitch) {
-    case 32: return tcs_plan_p<32>(ma, mb, p);
-    case 64: return tcs_plan_p<64>(ma, mb, p);
-    case 128: return tcs_plan_p<128>(ma, mb, p);
+    case 32: return tcs_plan_p<32>(ma, mb, persist, p);
+    case 64: return tcs_plan_p<64>(ma, mb, persist, p);
+    case 128: return tcs_plan_p<128>(ma, mb, persist, p);
     default: return false;
   }
 }
@@ -400,8 +725,8 @@ bool tcs_plan(int ma, int mb, int pitch, TcsPlan& p) {
 cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
   if (a.nprod == 0) return cudaSuccess;
   if (tcs_env("KMX_TC_VERBOSE", 0))
-    fprintf(stderr, "kmx_tcs: ma=%d mb=%d nprod=%d -> pitch=%d KS=%d tiles=%d smem=%zu mmas=%lld\n", a.ma, a.mb, a.nprod,
-            p.pitch, p.KS, p.ntiles, p.smem, p.mmas);
+    fprintf(stderr, "kmx_tcs: ma=%d mb=%d nprod=%d -> pitch=%d KS=%d tiles=%d smem=%zu mmas=%lld%s NS=%d\n", a.ma, a.mb,
+            a.nprod, p.pitch, p.KS, p.ntiles, p.smem, p.mmas, p.persist ? " persistent" : "", p.NS);
   switch (p.pitch) {
     case 32: return launch_p<32>(a, p, st);
     case 64: return launch_p<64>(a, p, st);
