@@ -76,6 +76,7 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk =
 struct TcsPlan {
   int pitch, KS, ntiles;
   int persist, NS;  // the persistent warp-specialized form and its operand stages
+  int nch;          // accumulation chains per tile (2 past 64 KB of the shorter operand)
   size_t smem;
   long long mmas;  // MMAs per product
   double cost;     // modelled SM cycles per product

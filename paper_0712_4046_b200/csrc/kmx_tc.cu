@@ -1133,7 +1133,10 @@ namespace {
 
 bool tc_supported(int ma, int mb, size_t stage_bytes) {
   TcPlan p;
-  return tc_plan(ma, mb, 1 << 20, stage_bytes, p);
+  if (tc_plan(ma, mb, 1 << 20, stage_bytes, p)) return true;
+  // the swizzled-window kernel stages a window per K-chunk, not whole operands:
+  // any length of the longer operand, up to 32768 limbs of the shorter
+  return stage_bytes == 0 && tcs_best(ma, mb, p);
 }
 
 namespace {
@@ -1315,15 +1318,21 @@ cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, 
     for (int i = 0; i < pk->nops; i++) lmax = pk->op[i].len > lmax ? pk->op[i].len : lmax;
     stage = (size_t)(lmax + PK_PAD) * pk->in_words * 4;
   }
-  if (!tc_plan(a.ma, a.mb, a.nprod, stage, p)) return cudaErrorNotSupported;
+  const bool tiled_ok = tc_plan(a.ma, a.mb, a.nprod, stage, p);
+  if (!tiled_ok && pk) return cudaErrorNotSupported;
   if (a.nprod == 0) return cudaSuccess;
-  if (!pk && tcs_mode() > 0) {  // forced: the swizzled-window kernel, no timing runs
-    TcPlan q;
-    if (tcs_best(a.ma, a.mb, q)) return launch_plan(a, q, st, nullptr, 1);
-  }
-  if (!pk && env_int_tc("KMX_TC_PERSIST", 0) == 2 && tcp_ok(a.ma, a.mb, p)) {  // forced test path
+  if (!pk && tiled_ok && env_int_tc("KMX_TC_PERSIST", 0) == 2 && tcp_ok(a.ma, a.mb, p)) {  // forced test path
     p.persist = 1; p.NW = 8; p.TPC = p.ntiles; p.nranges = 1;
     return launch_plan(a, p, st, nullptr, 1);
+  }
+  if (!pk) {
+    TcPlan q;
+    const bool swz_ok = tcs_best(a.ma, a.mb, q);
+    if (!tiled_ok && !swz_ok) return cudaErrorNotSupported;
+    if (swz_ok && tcs_mode() > 0) return launch_plan(a, q, st, nullptr, 1);  // forced, no timing runs
+    // untuned default: the swizzled-window kernel wherever it takes the shape
+    // (faster than the tiled kernel at every measured shape)
+    if (swz_ok) p = q;
   }
   if (!pk) {
     bool launched = false;
@@ -1457,8 +1466,10 @@ void tc_count(int ma, int mb, const TcPlan& p, long long out[8]) {
 // out = {1, H, NW, KC, TPC, MMAs per product, smem operand bytes per product,
 // issued byte MACs per product}.  false if the shape is not tensor-core.
 bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]) {
-  TcPlan p;
-  if (!tc_plan(ma, mb, nprod, 0, p)) return false;
+  TcPlan p, q;
+  const bool tiled_ok = tc_plan(ma, mb, nprod, 0, p);
+  if (tcs_best(ma, mb, q)) p = q;  // the untuned default
+  else if (!tiled_ok) return false;
   {
     std::lock_guard<std::mutex> lk(g_tune_mu);
     auto it = g_tune.find(TuneKey{current_device(), ma, mb, nprod});

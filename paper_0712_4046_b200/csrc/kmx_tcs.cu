@@ -109,6 +109,7 @@ struct TcsArgs {
   MulArgs m;
   int KS;      // K-steps per chunk
   int ntiles;  // CTAs per product
+  int nch;     // accumulation chains per tile (K-step s -> chain (s - slo) % nch): 2 past 64 KB of b
   int NS;      // persistent kernel: operand stages in the ring
   unsigned char order[TCS_MAXT];  // persistent kernel: tiles by descending K-steps
 };
@@ -117,98 +118,180 @@ __device__ __forceinline__ uint64_t sdesc_lt(uint32_t addr, uint32_t lbo, uint32
   return sdesc(addr, lbo, sbo) | ((uint64_t)lt << 61);
 }
 
+// The MMA is issued from WARP-UNIFORM code: every lane of the issuing warp
+// runs the loop and computes the (uniform) descriptors, one elected lane
+// executes the instruction.  With the loop inside an `if (lane == 0)` branch
+// ptxas cannot prove the operands uniform and wraps every UTCIMMA in a
+// vote / elect / 5x R2UR waterfall (~90 cycles per MMA, measured); issued
+// this way the descriptors live in uniform registers.
+__device__ __forceinline__ void mma_i8_elect(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                             uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|q, 0xffffffff;\n\t"
+      "@q tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t mbar) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\t"
+      "elect.sync _|q, 0xffffffff;\n\t"
+      "@q tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(mbar)
+      : "memory");
+}
+
 
 // One K-chunk's operands for tile k0: the swizzled a-window, the raw bytes of
-// b's chunk and its phase table.  128 threads (ptid); BAR = 0: __syncthreads
-// between the raw bytes and the table, else the named barrier BAR.
-template <int PITCH, int BAR>
-__device__ __forceinline__ void tcs_build(unsigned char* abuf, unsigned char* braw, unsigned char* tab,
-                                          const uint32_t* __restrict__ Ag, const uint32_t* __restrict__ Bg, int mA,
-                                          int mB, bool a16, const TcsDims& d, int k0, int sb, int se, int ptid) {
+// b's chunk and its phase table, built by 128 threads (ptid) in three steps
+// so a persistent producer can issue the NEXT chunk's global loads before it
+// builds the current chunk's table:
+//   tcs_load   global -> registers (the a-window's 16-byte pieces, b's words)
+//   tcs_store  registers -> shared memory (a swizzled by address, b raw)
+//   tcs_table  b raw -> phase table (after a barrier over the 128 threads)
+constexpr int TCS_NA = 10;   // 16-byte a pieces per thread: (127*128 + 32*128) / 16 / 128
+constexpr int TCS_NBW = 9;   // b words per thread: (32*128 + 128 + 96) / 4 / 128
+constexpr int TCS_KSMAX = 128;
+struct TcsRegs {
+  uint4 va[TCS_NA];
+  uint32_t vb[TCS_NBW];
+};
+template <int PITCH>
+struct TcsChunk {  // geometry of one chunk (all warp-uniform)
+  int aw0, nq, x0, nx, jb, nw;
+  __device__ __forceinline__ TcsChunk(const TcsDims& d, int k0, int sb, int se) {
+    using G = SG<PITCH>;
+    const int cc = G::N - 8 - d.ulo;  // T[x][r][i] = b[r + cc - 8x - i]
+    aw0 = k0 + d.ulo + 32 * sb;       // region byte o is a[aw0 + o]; a multiple of 32
+    nq = (G::AMAX + 32 * (se - sb) + 15) / 16;
+    x0 = 4 * sb;
+    nx = 4 * (se - sb) + G::N / 8 - 2;  // entries x0 .. x0 + nx - 1 are read
+    const int jlo = cc - 8 * (x0 + nx - 1) - 15;  // lowest index r + cc - 8x - i
+    jb = ((jlo >> 2) << 2) - 16;  // braw[k] = b[jb + k]: a multiple of 4, four spare words below (sliding loads)
+    nw = (7 + cc - 8 * x0 - jb) / 4 + 1;
+  }
+};
+
+template <int PITCH>
+__device__ __forceinline__ void tcs_load(TcsRegs& R, const TcsChunk<PITCH>& c, const uint32_t* __restrict__ Ag,
+                                         const uint32_t* __restrict__ Bg, int mA, int mB, bool a16, int ptid) {
+#pragma unroll
+  for (int k = 0; k < TCS_NA; k++) {
+    const int q = 128 * k + ptid;
+    const int j = (c.aw0 + 16 * q) >> 2;  // first limb of the piece (a multiple of 4, may be negative)
+    uint4 v = make_uint4(0u, 0u, 0u, 0u);
+    if (q < c.nq && j + 3 >= 0 && j < mA) {
+      if (a16 && j >= 0 && j + 3 < mA) {
+        v = __ldg(reinterpret_cast<const uint4*>(Ag + j));
+      } else {
+        v.x = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
+        v.y = (j + 1 >= 0 && j + 1 < mA) ? __ldg(Ag + j + 1) : 0u;
+        v.z = (j + 2 >= 0 && j + 2 < mA) ? __ldg(Ag + j + 2) : 0u;
+        v.w = (j + 3 >= 0 && j + 3 < mA) ? __ldg(Ag + j + 3) : 0u;
+      }
+    }
+    R.va[k] = v;
+  }
+#pragma unroll
+  for (int k = 0; k < TCS_NBW; k++) {
+    const int w = 128 * k + ptid;
+    const int j = (c.jb >> 2) + w;
+    R.vb[k] = (w < c.nw && j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
+  }
+}
+
+template <int PITCH>
+__device__ __forceinline__ void tcs_store(const TcsRegs& R, const TcsChunk<PITCH>& c, unsigned char* abuf,
+                                          unsigned char* braw, int ptid) {
   using G = SG<PITCH>;
   const uint32_t abase = smem_u32(abuf);
-  const int cc = G::N - 8 - d.ulo;  // T[x][r][i] = b[r + cc - 8x - i]
-  // ---- a-window: logical byte o of the region is a[aw0 + o]
-  {
-    const int aw0 = k0 + d.ulo + 32 * sb;  // multiple of 32
-    const int nq = (G::AMAX + 32 * (se - sb) + 15) / 16;
-    for (int q0 = 0; q0 < nq; q0 += 4 * 128) {
-      uint4 v[4];
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const int q = q0 + 128 * k + ptid;
-        const int j = (aw0 + 16 * q) >> 2;  // first limb of the 16-byte chunk (a multiple of 4, may be negative)
-        v[k] = make_uint4(0u, 0u, 0u, 0u);
-        if (q < nq && j + 3 >= 0 && j < mA) {
-          if (a16 && j >= 0 && j + 3 < mA) {
-            v[k] = __ldg(reinterpret_cast<const uint4*>(Ag + j));
-          } else {
-            v[k].x = (j >= 0 && j < mA) ? __ldg(Ag + j) : 0u;
-            v[k].y = (j + 1 >= 0 && j + 1 < mA) ? __ldg(Ag + j + 1) : 0u;
-            v[k].z = (j + 2 >= 0 && j + 2 < mA) ? __ldg(Ag + j + 2) : 0u;
-            v[k].w = (j + 3 >= 0 && j + 3 < mA) ? __ldg(Ag + j + 3) : 0u;
-          }
+  for (int k = 0; k < TCS_NA; k++) {
+    const int q = 128 * k + ptid;
+    if (q < c.nq) {
+      const uint32_t L = abase + 16u * (uint32_t)q;
+      const uint32_t P = L ^ (((L >> 7) & G::MASK) << 4);
+      *reinterpret_cast<uint4*>(abuf + (P - abase)) = R.va[k];
+    }
+  }
+  uint32_t* bw = reinterpret_cast<uint32_t*>(braw);
+#pragma unroll
+  for (int k = 0; k < TCS_NBW; k++) {
+    const int w = 128 * k + ptid;
+    if (w < c.nw) bw[w] = R.vb[k];
+  }
+}
+
+// thread (r = ptid % 8, run = ptid / 8) builds a contiguous run of entries;
+// consecutive entries move the 16-byte window down by 8 bytes, so five words
+// slide through registers with two new loads per entry
+template <int PITCH>
+__device__ __forceinline__ void tcs_table(const TcsChunk<PITCH>& c, const TcsDims& d, const unsigned char* braw,
+                                          unsigned char* tab, int ptid) {
+  using G = SG<PITCH>;
+  const int cc = G::N - 8 - d.ulo;
+  const int r = ptid & 7, run = ptid >> 3;
+  const int XB = (c.nx + 15) / 16;
+  const int xa = run * XB, xe = min(c.nx, xa + XB);
+  if (xa < xe) {
+    const uint32_t* bw = reinterpret_cast<const uint32_t*>(braw);
+    // entry bytes i = 0..15: braw[e - i], e = r + cc - 8 (x0 + x) - jb  (>= 15 + 16)
+    const int e = r + cc - 8 * (c.x0 + xa) - c.jb;
+    int wq = e >> 2;
+    const int sh2 = e & 3;
+    // output byte k of a word = byte (4 + sh2 - k) of {lo, hi}
+    const uint32_t sel = (uint32_t)(4 + sh2) | ((uint32_t)(3 + sh2) << 4) | ((uint32_t)(2 + sh2) << 8) |
+                         ((uint32_t)(1 + sh2) << 12);
+    uint32_t w0 = bw[wq], w1 = bw[wq - 1], w2 = bw[wq - 2], w3 = bw[wq - 3], w4 = bw[wq - 4];
+    unsigned char* dst = tab + (size_t)xa * 128 + r * 16;
+    for (int x = xa; x < xe; x++) {
+      uint4 o;
+      o.x = __byte_perm(w1, w0, sel);
+      o.y = __byte_perm(w2, w1, sel);
+      o.z = __byte_perm(w3, w2, sel);
+      o.w = __byte_perm(w4, w3, sel);
+      *reinterpret_cast<uint4*>(dst) = o;
+      dst += 128;
+      wq -= 2;
+      w0 = w2; w1 = w3; w2 = w4;
+      w3 = bw[wq - 3];
+      w4 = bw[wq - 4];
+    }
+  }
+}
+
+
+// Epilogue, first half: TMEM lane m's LPT limb sums -> digits with carry-in 0.
+// Limbs 4c .. 4c+3 live in columns [N - 16 - 16c, N - 16c): the upper 8 columns
+// (g odd) hold byte offsets 16c .. 16c+7, the lower 8 hold 16c+8 .. 16c+15.
+// The chains' partial sums are added in 64 bits.  Returns the carry out.
+template <int PITCH>
+__device__ __forceinline__ unsigned long long tcs_limbs(uint32_t tacc, int nch, bool have,
+                                                        uint32_t (&dg)[SG<PITCH>::LPT]) {
+  using G = SG<PITCH>;
+  unsigned long long x = 0ull;
+#pragma unroll
+  for (int c = 0; c < G::N / 16; c++) {
+    unsigned long long ls[4] = {0ull, 0ull, 0ull, 0ull};
+    if (have) {
+      for (int ch = 0; ch < nch; ch++) {
+        uint32_t v[16];
+        tmem_ld16(tacc + (uint32_t)(ch * G::N + G::N - 16 - 16 * c), v);
+#pragma unroll
+        for (int q = 0; q < 4; q++) {
+          const int o = q < 2 ? 8 + 4 * q : 4 * (q - 2);
+          ls[q] += (unsigned long long)v[o] + ((unsigned long long)v[o + 1] << 8) +
+                   ((unsigned long long)v[o + 2] << 16) + ((unsigned long long)v[o + 3] << 24);
         }
       }
+    }
 #pragma unroll
-      for (int k = 0; k < 4; k++) {
-        const int q = q0 + 128 * k + ptid;
-        if (q < nq) {
-          const uint32_t L = abase + 16u * (uint32_t)q;
-          const uint32_t P = L ^ (((L >> 7) & G::MASK) << 4);
-          *reinterpret_cast<uint4*>(abuf + (P - abase)) = v[k];
-        }
-      }
+    for (int q = 0; q < 4; q++) {
+      x = (x >> 32) + ls[q];
+      dg[4 * c + q] = (uint32_t)x;
     }
   }
-  // ---- raw bytes of b this chunk's table reads: braw[k] = b[jb + k],
-  // jb a multiple of 4 at or below the lowest index r + cc - 8x - i
-  const int x0 = 4 * sb, nx = 4 * (se - sb) + G::N / 8 - 2;  // entries x0 .. x0 + nx - 1 are read
-  const int jlo = cc - 8 * (x0 + nx - 1) - 15;
-  const int jb = ((jlo >> 2) << 2) - 16;  // floor to a multiple of 4, four spare words below (the sliding window's trailing loads)
-  {
-    const int nw = (7 + cc - 8 * x0 - jb) / 4 + 1;
-    uint32_t* bw = reinterpret_cast<uint32_t*>(braw);
-    for (int w = ptid; w < nw; w += 128) {
-      const int j = (jb >> 2) + w;
-      bw[w] = (j >= 0 && j < mB) ? __ldg(Bg + j) : 0u;
-    }
-  }
-  if (BAR == 0) __syncthreads();
-  else asm volatile("bar.sync %0, 128;" ::"n"(BAR) : "memory");
-  // ---- table: thread (r = ptid % 8, run = ptid / 8) builds a contiguous run
-  // of entries; consecutive entries move the 16-byte window down by 8 bytes,
-  // so five words slide through registers with two new loads per entry
-  {
-    const int r = ptid & 7, run = ptid >> 3;
-    const int XB = (nx + 15) / 16;
-    const int xa = run * XB, xe = min(nx, xa + XB);
-    if (xa < xe) {
-      const uint32_t* bw = reinterpret_cast<const uint32_t*>(braw);
-      // entry bytes i = 0..15: braw[e - i], e = r + cc - 8 (x0 + x) - jb  (>= 15 + 8)
-      const int e = r + cc - 8 * (x0 + xa) - jb;
-      int wq = e >> 2;
-      const int sh2 = e & 3;
-      // output byte k of a word = byte (4 + sh2 - k) of {lo, hi}
-      const uint32_t sel = (uint32_t)(4 + sh2) | ((uint32_t)(3 + sh2) << 4) | ((uint32_t)(2 + sh2) << 8) |
-                           ((uint32_t)(1 + sh2) << 12);
-      uint32_t w0 = bw[wq], w1 = bw[wq - 1], w2 = bw[wq - 2], w3 = bw[wq - 3], w4 = bw[wq - 4];
-      unsigned char* dst = tab + (size_t)xa * 128 + r * 16;
-      for (int x = xa; x < xe; x++) {
-        uint4 o;
-        o.x = __byte_perm(w1, w0, sel);
-        o.y = __byte_perm(w2, w1, sel);
-        o.z = __byte_perm(w3, w2, sel);
-        o.w = __byte_perm(w4, w3, sel);
-        *reinterpret_cast<uint4*>(dst) = o;
-        dst += 128;
-        wq -= 2;
-        w0 = w2; w1 = w3; w2 = w4;
-        w3 = bw[wq - 3];
-        w4 = bw[wq - 4];
-      }
-    }
-  }
+  return x >> 32;
 }
 
 template <int PITCH>
@@ -216,7 +299,8 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
   using G = SG<PITCH>;
   const MulArgs& a = ta.m;
   extern __shared__ __align__(1024) unsigned char ssm_raw[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
   const int z = blockIdx.x / ta.ntiles, t = blockIdx.x % ta.ntiles;
   unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
   const int KS = ta.KS;
@@ -238,7 +322,7 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
-                 "r"((uint32_t)G::N));
+                 "r"((uint32_t)(ta.nch * G::N)));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
   if (tid == 0) {
@@ -258,23 +342,33 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
       mbar_wait(smem_u32(&sh.bar_mma), phase);
       phase ^= 1u;
     }
-    tcs_build<PITCH, 0>(abuf, braw, tab, Ag, Bg, mA, mB, a16, d, k0, sb, se, tid);
+    {
+      const TcsChunk<PITCH> ck(d, k0, sb, se);
+      TcsRegs R;
+      tcs_load<PITCH>(R, ck, Ag, Bg, mA, mB, a16, tid);
+      tcs_store<PITCH>(R, ck, abuf, braw, tid);
+      __syncthreads();
+      tcs_table<PITCH>(ck, d, braw, tab, tid);
+    }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (first) tmem = sh.tmem_base;
-    if (tid == 0) {
+    if (first) tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
+    if (warp == 0) {
       uint64_t ad = sdesc_lt(abase, 16, 8 * PITCH, G::LT);
       uint64_t bd = sdesc(smem_u32(tab), 256, 128);
-      uint32_t acc = first ? 0u : 1u;
+      // K-step s accumulates into chain (s - slo) & (nch - 1): with more than
+      // 64 KB of b the u32 sums are exact only per half of the K-steps (at
+      // most 65536 byte products < 2^16 each); the epilogue adds the chains
+      const int nch = ta.nch;
       for (int s = sb; s < se; s++) {
-        mma_i8(tmem, ad, bd, G::IDESC, acc);
-        acc = 1u;
+        const uint32_t ch = (uint32_t)(s - slo) & (uint32_t)(nch - 1);
+        mma_i8_elect(tmem + ch * G::N, ad, bd, G::IDESC, (s - slo) >= nch ? 1u : 0u);
         ad += 2;   // + 32 bytes
         bd += 32;  // + 512 bytes
       }
-      mma_commit(smem_u32(&sh.bar_mma));
+      mma_commit_elect(smem_u32(&sh.bar_mma));
     }
     first = false;
   }
@@ -282,34 +376,15 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (first) {  // no K-step touches this tile (cannot happen for t < ntiles; kept for safety)
     __syncthreads();
-    tmem = sh.tmem_base;
+    tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
   }
 
   // ---- epilogue: lane m = tid owns limbs [LPT m, LPT m + LPT) of the tile
   constexpr int LPT = G::LPT;
   uint32_t dg[LPT];
-  unsigned long long x = 0ull;
-#pragma unroll
-  for (int c = 0; c < G::N / 16; c++) {
-    // limbs 4c .. 4c+3 live in columns [N - 16 - 16c, N - 16c): the upper 8
-    // columns (g odd) hold byte offsets 16c .. 16c+7, the lower 8 hold 16c+8 .. 16c+15
-    uint32_t v[16];
-    if (!first) {
-      tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(G::N - 16 - 16 * c), v);
-    } else {
-#pragma unroll
-      for (int q = 0; q < 16; q++) v[q] = 0u;
-    }
-#pragma unroll
-    for (int q = 0; q < 4; q++) {
-      const int o = q < 2 ? 8 + 4 * q : 4 * (q - 2);
-      const unsigned long long ls = (unsigned long long)v[o] + ((unsigned long long)v[o + 1] << 8) +
-                                    ((unsigned long long)v[o + 2] << 16) + ((unsigned long long)v[o + 3] << 24);
-      x = (x >> 32) + ls;
-      dg[4 * c + q] = (uint32_t)x;
-    }
-  }
-  const unsigned long long cout = x >> 32;
+  // (a tile with fewer K-steps than chains never wrote the later chains)
+  const unsigned long long cout =
+      tcs_limbs<PITCH>(tmem + ((uint32_t)(32 * warp) << 16), min(ta.nch, shi - slo), !first, dg);
   unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
   if (lane == 31) sh.s_cout[warp] = cout;
   uint32_t ones = 0xFFFFFFFFu;
@@ -371,7 +446,7 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)G::N));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(ta.nch * G::N)));
 }
 
 
@@ -410,7 +485,8 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
   using G = SG<PITCH>;
   const MulArgs& a = ta.m;
   extern __shared__ __align__(1024) unsigned char ssm_raw[];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
   unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
   const int KS = ta.KS, NS = ta.NS;
   const size_t stage_bytes = tcs_stage_bytes<PITCH>(KS);
@@ -423,7 +499,8 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
   const TcsDims d = tcs_dims<PITCH>(mA, mB);
   const int mp = a.ma + a.mb;
   const long long nitems = (long long)a.nprod * ta.ntiles;
-  constexpr uint32_t COLS = 2 * G::N < 32 ? 32 : 2 * G::N;
+  uint32_t COLS = 32;  // two accumulator buffers x nch chains
+  while (COLS < (uint32_t)(2 * ta.nch * G::N)) COLS <<= 1;
 
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
@@ -444,34 +521,70 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  const uint32_t tmem = sh.tmem_base;
+  const uint32_t tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
 
   if (warp >= 4 && warp < 8) {
-    // ---------------- producers
+    // ---------------- producers: the next chunk's global loads are in flight
+    // while the current chunk's table is built
     const int ptid = tid - 128;
     long long sc = 0;
-    for (long long it = blockIdx.x; it < nitems; it += gridDim.x) {
-      const int t = ta.order[it / a.nprod];
+    long long it = blockIdx.x;
+    int t = 0, slo = 0, shi = 0, sb = 0;
+    const uint32_t *Ag = nullptr, *Bg = nullptr;
+    bool a16 = false;
+    bool valid = it < nitems;
+    auto open_item = [&]() {
+      t = ta.order[it / a.nprod];
       const long long z = it % a.nprod;
-      const uint32_t* Ag = Abase + z * astr;
-      const uint32_t* Bg = Bbase + z * bstr;
-      const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
-      int slo, shi;
+      Ag = Abase + z * astr;
+      Bg = Bbase + z * bstr;
+      a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
       tcs_tile_steps<PITCH>(d, t, slo, shi);
-      for (int sb = slo; sb < shi; sb += KS, sc++) {
-        const int st = (int)(sc % NS);
-        if (sc >= NS) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((sc / NS) - 1) & 1));
-        unsigned char* abuf = ssm + (size_t)st * stage_bytes;
-        unsigned char* braw = abuf + tcs_abytes<PITCH>(KS);
-        unsigned char* tab = braw + tcs_rawbytes<PITCH>(KS);
-        tcs_build<PITCH, 1>(abuf, braw, tab, Ag, Bg, mA, mB, a16, d, t * G::T, sb, min(shi, sb + KS), ptid);
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(smem_u32(&sh.bar_full[st]));
+      sb = slo;
+    };
+    TcsRegs R;
+    if (valid) {
+      open_item();
+      while (valid && slo >= shi) {  // (no empty tiles for t < ntiles; kept for safety)
+        it += gridDim.x;
+        valid = it < nitems;
+        if (valid) open_item();
       }
     }
+    if (valid) {
+      const TcsChunk<PITCH> ck(d, t * G::T, sb, min(shi, sb + KS));
+      tcs_load<PITCH>(R, ck, Ag, Bg, mA, mB, a16, ptid);
+    }
+    while (valid) {
+      const int st = (int)(sc % NS);
+      if (sc >= NS) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((sc / NS) - 1) & 1));
+      unsigned char* abuf = ssm + (size_t)st * stage_bytes;
+      unsigned char* braw = abuf + tcs_abytes<PITCH>(KS);
+      unsigned char* tab = braw + tcs_rawbytes<PITCH>(KS);
+      const TcsChunk<PITCH> ck(d, t * G::T, sb, min(shi, sb + KS));
+      tcs_store<PITCH>(R, ck, abuf, braw, ptid);
+      // advance to the next chunk (of this item or the next) and start its loads
+      sb += KS;
+      if (sb >= shi) {
+        do {
+          it += gridDim.x;
+          valid = it < nitems;
+          if (valid) open_item();
+        } while (valid && slo >= shi);
+      }
+      if (valid) {
+        const TcsChunk<PITCH> cn(d, t * G::T, sb, min(shi, sb + KS));
+        tcs_load<PITCH>(R, cn, Ag, Bg, mA, mB, a16, ptid);
+      }
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      tcs_table<PITCH>(ck, d, braw, tab, ptid);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(smem_u32(&sh.bar_full[st]));
+      sc++;
+    }
   } else if (warp == 8) {
-    // ---------------- MMA issuer
-    if (lane == 0) {
+    // ---------------- MMA issuer (warp-uniform loop, one elected lane issues)
+    {
       long long sc = 0, ac = 0;
       for (long long it = blockIdx.x; it < nitems; it += gridDim.x, ac++) {
         const int t = ta.order[it / a.nprod];
@@ -480,8 +593,8 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
         const int buf = (int)(ac & 1);
         if (ac >= 2) mbar_wait(smem_u32(&sh.bar_acc_empty[buf]), (uint32_t)(((ac >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-        const uint32_t dcol = tmem + (uint32_t)(buf * G::N);
-        uint32_t acc = 0u;
+        const uint32_t dcol = tmem + (uint32_t)(buf * ta.nch * G::N);
+        const int nch = ta.nch;
         for (int sb = slo; sb < shi; sb += KS, sc++) {
           const int st = (int)(sc % NS);
           mbar_wait(smem_u32(&sh.bar_full[st]), (uint32_t)((sc / NS) & 1));
@@ -490,15 +603,15 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
           uint64_t ad = sdesc_lt(sbase, 16, 8 * PITCH, G::LT);
           uint64_t bd = sdesc(sbase + (uint32_t)(tcs_abytes<PITCH>(KS) + tcs_rawbytes<PITCH>(KS)), 256, 128);
           const int se = min(shi, sb + KS);
-          for (int s = sb; s < se; s++) {
-            mma_i8(dcol, ad, bd, G::IDESC, acc);
-            acc = 1u;
+          for (int s = sb; s < se; s++) {  // chain (s - slo) & (nch - 1), as in k_tcswz
+            const uint32_t ch = (uint32_t)(s - slo) & (uint32_t)(nch - 1);
+            mma_i8_elect(dcol + ch * G::N, ad, bd, G::IDESC, (s - slo) >= nch ? 1u : 0u);
             ad += 2;   // + 32 bytes
             bd += 32;  // + 512 bytes
           }
-          mma_commit(smem_u32(&sh.bar_empty[st]));
+          mma_commit_elect(smem_u32(&sh.bar_empty[st]));
         }
-        mma_commit(smem_u32(&sh.bar_acc_full[buf]));
+        mma_commit_elect(smem_u32(&sh.bar_acc_full[buf]));
       }
     }
     __syncwarp();
@@ -515,29 +628,11 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
       mbar_wait(smem_u32(&sh.bar_acc_full[buf]), (uint32_t)((ac >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t dg[LPT];
-      unsigned long long x = 0ull;
-#pragma unroll
-      for (int c = 0; c < G::N / 16; c++) {
-        uint32_t v[16];
-        if (slo < shi) {
-          tmem_ld16(tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(buf * G::N + G::N - 16 - 16 * c), v);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; q++) v[q] = 0u;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; q++) {
-          const int o = q < 2 ? 8 + 4 * q : 4 * (q - 2);
-          const unsigned long long ls = (unsigned long long)v[o] + ((unsigned long long)v[o + 1] << 8) +
-                                        ((unsigned long long)v[o + 2] << 16) + ((unsigned long long)v[o + 3] << 24);
-          x = (x >> 32) + ls;
-          dg[4 * c + q] = (uint32_t)x;
-        }
-      }
+      const unsigned long long cout = tcs_limbs<PITCH>(
+          tmem + ((uint32_t)(32 * warp) << 16) + (uint32_t)(buf * ta.nch * G::N), min(ta.nch, shi - slo), slo < shi, dg);
       // the accumulator is in registers: hand it back to the MMA warp
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(smem_u32(&sh.bar_acc_empty[buf]));
-      const unsigned long long cout = x >> 32;
       unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
       if (lane == 31) sh.s_cout[warp] = cout;
       uint32_t ones = 0xFFFFFFFFu;
@@ -619,10 +714,13 @@ bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
   if (mB < 1) return false;
   const TcsDims d = tcs_dims<PITCH>(mA, mB);
-  if (d.Lb > 65536) return false;  // u32 accumulators: at most 65536 byte products of < 2^16 per sum
+  // u32 accumulators: at most 65536 byte products of < 2^16 per sum -> two chains up to 128 KB of b
+  if (d.Lb > 131072) return false;
+  p.nch = d.Lb > 65536 ? 2 : 1;
+  if (persist && 2 * p.nch * PITCH > 512) return false;
   int ksmax = tcs_env("KMX_TCS_KS", 128);
   if (ksmax < 8) ksmax = 8;
-  if (ksmax > 256) ksmax = 256;
+  if (ksmax > TCS_KSMAX) ksmax = TCS_KSMAX;
   p.persist = persist;
   p.NS = 0;
   if (persist) {
@@ -665,6 +763,7 @@ cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
   ta.KS = p.KS;
   ta.ntiles = p.ntiles;
   ta.NS = p.NS;
+  ta.nch = p.nch;
   if (p.persist) {
     static size_t s_set = 0;
     if (p.smem > 48 * 1024 && p.smem > s_set) {
@@ -689,7 +788,7 @@ cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
         ta.order[j - 1] = x;
       }
     int per_sm = (int)((220 * 1024) / (p.smem + 1024));
-    const int by_tmem = 512 / (2 * PITCH < 32 ? 32 : 2 * PITCH);
+    const int by_tmem = 512 / (2 * p.nch * PITCH);
     if (per_sm > by_tmem) per_sm = by_tmem;
     if (per_sm < 1) per_sm = 1;
     const int cps = tcs_env("KMX_TCS_CPS", 0);

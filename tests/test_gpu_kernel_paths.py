@@ -22,19 +22,25 @@ SETTINGS = [
     {"KMX_FINISH_CHUNKS": "1"},  # chunk-parallel finish (k_finmap + k_finchunk) everywhere
     {"KMX_FINISH_CHUNKS": "0", "KMX_SPLIT": "1"},  # warp-per-stream finish; every batch split over two streams
     {"KMX_TC": "0"},            # integer-pipe multiply everywhere
-    {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands)
+    {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands): swizzled-window kernel
+    {"KMX_TC": "1", "KMX_TCS": "0"},  # the tiled tensor-core kernel (k_tcmul) wherever supported
+    {"KMX_TC": "1", "KMX_TCS": "32"},  # swizzled-window kernel, pitch 32 (N = 32), one-shot CTAs
+    {"KMX_TC": "1", "KMX_TCS": "128", "KMX_TCS_KS": "24"},  # pitch 128, many short K-chunks per tile
+    {"KMX_TC": "1", "KMX_TCS": "64", "KMX_TCS_PERSIST": "1"},  # persistent warp-specialized form, pitch 64
+    {"KMX_TC": "1", "KMX_TCS": "128", "KMX_TCS_PERSIST": "1", "KMX_TCS_KS": "40", "KMX_TCS_NS": "2"},  # persistent, pitch 128, short chunks, 2 stages
     {"KMX_TC": "1", "KMX_TCJ": "1", "KMX_PACK_PAIR": "2"},  # chunked single-tile tensor-core kernel; paired packs at every batch size
     {"KMX_RECON_BIAS_SMEM": "0", "KMX_RECON_WARP": "1"},  # signed prefix sums from L2; warp-per-stream recon
     {"KMX_RECON_SPEC": "1", "KMX_RECON_MINB": "0"},  # recon: speculative stores from round 1; uncapped registers
     {"KMX_RECON_SPEC": "0", "KMX_PACK_FAST": "0"},  # recon: separate output walk; looped pack windows only
     {"KMX_RECON_MINB": "6", "KMX_RECON_V": "4"},  # recon: 6-CTA register cap; 4 steps per thread
     {"KMX_KARA_MIN": "600"},    # Karatsuba levels on every product above 600 limbs (tensor-core leaves)
+    {"KMX_KARA_MIN": "600", "KMX_TCS": "0"},  # the same over the tiled kernel's leaves
     {"KMX_KARA_MIN": "300", "KMX_TC": "0"},  # Karatsuba over integer-pipe leaves, up to 4 levels
     {"KMX_WIDE": "1"},          # wide-digit finish + multiword reconstruction for every unsigned shape
     {"KMX_PACK_W1": "0"},       # block-per-job pack everywhere (no warp-per-job kernel)
     {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one- and two-word shape (single and paired jobs)
     {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},  # segmented pack; bivariate: IMAD products, unstaged evaluation
-    {"KMX_TC_PERSIST": "2", "KMX_TC": "1"},  # persistent warp-specialized tensor-core kernel wherever it applies
+    {"KMX_TC_PERSIST": "2", "KMX_TC": "1", "KMX_TCS": "0"},  # persistent form of the tiled tensor-core kernel wherever it applies
 ]
 
 
