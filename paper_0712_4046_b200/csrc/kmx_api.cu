@@ -450,21 +450,6 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   ma.nprod = p.batch * p.P; ma.nbands = p.nbands; ma.G = p.G; ma.TI = p.TI;
   ma.counter = (int*)cnt;
   ma.err = err;
-  prof_begin(1, st);
-  if (p.kara) {
-    int nl = 0;
-    if ((e = launch_kara(ma, w + p.off_kara, st, &nl)) != cudaSuccess) return KMX_ECUDA;
-    g_launches += nl - 1;
-  } else if (tc && !fuse && use_tcj(p.mf, p.mg, (long long)p.batch * p.P)) {
-    if ((e = launch_tcmulj(ma, st)) != cudaSuccess) return KMX_ECUDA;
-  } else if (tc) {
-    if ((e = launch_tcmul(ma, st, fuse ? &pa : nullptr, p.P)) != cudaSuccess) return KMX_ECUDA;
-  } else {
-    if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
-  }
-  prof_end(1, st);
-  g_launches++;
-
   FinishArgs fa;
   memset(&fa, 0, sizeof fa);
   for (int i = 0; i < p.ns; i++) fa.s[i] = p.st[i];
@@ -478,6 +463,26 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.bias = bfix;
   fa.cmaps = (uint8_t*)(w + p.off_cmap);
   fa.nchunks = p.fin_chunks;
+  bool finished = false;  // K3 already ran inside K2
+  prof_begin(1, st);
+  if (p.kara) {
+    int nl = 0;
+    if ((e = launch_kara(ma, w + p.off_kara, st, &nl)) != cudaSuccess) return KMX_ECUDA;
+    g_launches += nl - 1;
+  } else if (tc && !fuse && use_tcj(p.mf, p.mg, (long long)p.batch * p.P)) {
+    if ((e = launch_tcmulj(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  } else if (tc) {
+    // single-tile products with a warp-per-stream K3: K2 + K3 in one kernel
+    if (!fuse && !p.wide && launch_tcmul_finish(ma, fa, p.batch, st, &e)) {
+      if (e != cudaSuccess) return KMX_ECUDA;
+      finished = true;
+    } else if ((e = launch_tcmul(ma, st, fuse ? &pa : nullptr, p.P)) != cudaSuccess) return KMX_ECUDA;
+  } else {
+    if ((e = launch_mul(ma, st)) != cudaSuccess) return KMX_ECUDA;
+  }
+  prof_end(1, st);
+  g_launches++;
+
   ReconArgs ra;
   memset(&ra, 0, sizeof ra);
   if (p.wide) return run_wide(p, fa, w, st);
@@ -493,17 +498,19 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     // ks2 / ks4: finish + reconstruct in one kernel (k_finrec) when both fit it
     bool fused = false;
     prof_begin(3, st);
-    if ((e = launch_finrec(fa, ra, p.batch, st, &fused)) != cudaSuccess) return KMX_ECUDA;
+    if (!finished && (e = launch_finrec(fa, ra, p.batch, st, &fused)) != cudaSuccess) return KMX_ECUDA;
     if (fused) {
       prof_end(3, st);
       g_launches++;
       return KMX_OK;
     }
   }
-  prof_begin(2, st);
-  if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
-  prof_end(2, st);
-  g_launches++;
+  if (!finished) {
+    prof_begin(2, st);
+    if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
+    prof_end(2, st);
+    g_launches++;
+  }
 
   if (p.nrs) {
     prof_begin(3, st);

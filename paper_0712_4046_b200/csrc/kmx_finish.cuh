@@ -47,7 +47,13 @@ __device__ __forceinline__ u32 dig_word(const u32* buf, int lb, int w, int W) {
 // One output stream (index si of pair `pair`) by one warp; buf: FIN_HALO +
 // FW_CH words of this warp's shared memory (16-byte aligned).  Digit-buffer
 // streams (mode 1) go to the sink.
-template <class Sink>
+// NC = false: the products were written by this kernel (the fused K2 + K3 of
+// kmx_tcs.cu): plain loads instead of the read-only ld.global.nc path.
+template <bool NC>
+__device__ __forceinline__ uint4 fin_ld4(const uint4* p) {
+  return NC ? __ldg(p) : *p;
+}
+template <class Sink, bool NC = true>
 __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair, int si, u32* buf, Sink sink) {
   const int lane = threadIdx.x & 31;
   const Stream S = si == 0 ? a.s[0] : (si == 1 ? a.s[1] : (si == 2 ? a.s[2] : a.s[3]));
@@ -91,8 +97,8 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
       const bool bstart = q0 > 0 && q0 < mp && (q0 & cmask) == 0;
       const int bidx = (q0 >> lgC) - 1;
       if (full) {
-        const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(Pp + q0));
-        const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(Pp + q0) + 1);
+        const uint4 x0 = fin_ld4<NC>(reinterpret_cast<const uint4*>(Pp + q0));
+        const uint4 x1 = fin_ld4<NC>(reinterpret_cast<const uint4*>(Pp + q0) + 1);
         pv[0] = x0.x; pv[1] = x0.y; pv[2] = x0.z; pv[3] = x0.w; pv[4] = x1.x; pv[5] = x1.y; pv[6] = x1.z; pv[7] = x1.w;
       } else {
 #pragma unroll
@@ -101,8 +107,8 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
       if (bstart) { s0 = (i64)spP[bidx * 2]; s1 = (i64)spP[bidx * 2 + 1]; }
       if (sg) {
         if (full) {
-          const uint4 x0 = __ldg(reinterpret_cast<const uint4*>(Qp + q0));
-          const uint4 x1 = __ldg(reinterpret_cast<const uint4*>(Qp + q0) + 1);
+          const uint4 x0 = fin_ld4<NC>(reinterpret_cast<const uint4*>(Qp + q0));
+          const uint4 x1 = fin_ld4<NC>(reinterpret_cast<const uint4*>(Qp + q0) + 1);
           qv[0] = x0.x; qv[1] = x0.y; qv[2] = x0.z; qv[3] = x0.w; qv[4] = x1.x; qv[5] = x1.y; qv[6] = x1.z; qv[7] = x1.w;
         } else {
 #pragma unroll

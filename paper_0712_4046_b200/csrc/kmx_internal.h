@@ -82,7 +82,11 @@ struct TcsPlan {
   double cost;     // modelled SM cycles per product
 };
 bool tcs_plan(int ma, int mb, int pitch, int persist, TcsPlan& p);
-cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st);
+struct FinishArgs;
+// fin != nullptr: one CTA per pair multiplies the pair's products and runs the
+// warp-per-stream finish (K3) for it (single-tile plans only)
+cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st, const FinishArgs* fin = nullptr);
+bool launch_tcmul_finish(const MulArgs& a, const FinishArgs& fa, int batch, cudaStream_t st, cudaError_t* err);
 double measure_tc_peak(int iters);
 double measure_tc_peak_shape(int n, int iters);
 // engine choice (kmx_api.cu): the tensor cores for this shape, and whether

@@ -1207,9 +1207,15 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
   // 4-warp epilogue per CTA, 1-3 CTAs per SM, against ~8 one-shot CTAs whose
   // epilogues overlap each other's MMAs), and were never chosen
   const int pers = env_int_tc("KMX_TC_PERSIST", 0);
+  // With swizzled-window candidates in the list (they won every measured shape)
+  // only the tiled kernel's model-best tilings stay, as a cross-check; the wide
+  // tiled field is timed only where the swizzled-window kernel has no plan.
+  const bool have_swz = !out.empty();
+  const double keep = have_swz ? 1.05 : 1.6;
   for (const TcPlan& p : v)
-    if (p.cost <= 1.6 * best) {
+    if (p.cost <= keep * best) {
       out.push_back(p);
+      if (have_swz) continue;
       if (pers && tcp_ok(ma, mb, p)) {  // the persistent form of the same tiling
         TcPlan q = p;
         q.persist = 1;
@@ -1309,6 +1315,31 @@ bool tc_tuned_plan(const MulArgs& a, cudaStream_t st, TcPlan& p, bool* launched)
   return true;
 }
 }  // namespace
+
+// K2 + K3 in one launch (kmx_tcs.cu, pair CTAs): when every product is one
+// tile of a swizzled-window plan and K3 would be the warp-per-stream finish.
+// Opt-in (KMX_FUSE_FIN=1): bit-exact, but measured slower than the two
+// kernels at c2 (ks4: 118.7 us against 80.3 + 29.4; ks3: 212 against 99 + 62)
+// -- a pair CTA holds its shared memory and TMEM through the finish, so fewer
+// MMA phases overlap.  Returns true when the fused kernel ran.
+bool launch_tcmul_finish(const MulArgs& a, const FinishArgs& fa, int batch, cudaStream_t st, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (env_int_tc("KMX_FUSE_FIN", 0) == 0 || tcs_mode() == 0 || tcs_persist_mode() == 1) return false;
+  if (fa.ns < 1 || fa.ns > 4 || fa.nprod_pair < 1 || a.nprod != (long long)batch * fa.nprod_pair) return false;
+  if (!finish_use_warp(fa, batch) || finish_use_chunks(fa, batch)) return false;  // K3 = k_finish_w only
+  bool ok = false;
+  TcsPlan best;
+  for (int pitch : {32, 64, 128}) {
+    if (tcs_mode() >= 32 && tcs_mode() != pitch) continue;
+    TcsPlan sp;
+    if (!tcs_plan(a.ma, a.mb, pitch, 0, sp) || sp.ntiles != 1) continue;
+    if (!ok || sp.cost < best.cost) best = sp;
+    ok = true;
+  }
+  if (!ok) return false;
+  *err = launch_tcs(a, best, st, &fa);
+  return true;
+}
 
 cudaError_t launch_tcmul(const MulArgs& a, cudaStream_t st, const PackArgs* pk, int P) {
   TcPlan p;

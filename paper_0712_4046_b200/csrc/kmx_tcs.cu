@@ -42,6 +42,7 @@
 #include "kmx_internal.h"
 #include "kmx_common.cuh"
 #include "kmx_tcutil.cuh"
+#include "kmx_finish.cuh"
 
 namespace kmx {
 
@@ -116,6 +117,15 @@ struct TcsArgs {
 
 __device__ __forceinline__ uint64_t sdesc_lt(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t lt) {
   return sdesc(addr, lbo, sbo) | ((uint64_t)lt << 61);
+}
+
+// One lane polls the mbarrier, the warp joins at __syncwarp: every polling
+// lane's try_wait is a shared-memory access, and this kernel is bound by
+// shared-memory bandwidth (ncu: tensor-operand reads 73% + LSU 28% of the
+// pipe with all 128 threads polling).
+__device__ __forceinline__ void mbar_wait_warp(uint32_t mbar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(mbar, parity);
+  __syncwarp();
 }
 
 // The MMA is issued from WARP-UNIFORM code: every lane of the issuing warp
@@ -294,14 +304,21 @@ __device__ __forceinline__ unsigned long long tcs_limbs(uint32_t tacc, int nch, 
   return x >> 32;
 }
 
-template <int PITCH>
-__global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
+// PAIR = false: one CTA per (product, tile).
+// PAIR = true (single-tile products only): one CTA per polynomial PAIR.  It
+// multiplies the pair's nprod_pair products one after the other and then runs
+// K3 for the pair -- the warp-per-stream finish (kmx_finish.cuh: half sums /
+// differences, exact halving and shifts, digit extraction), one warp per
+// output stream, on the products it has just written (they sit in L2).  The
+// finish instructions fill issue slots the other resident CTAs' MMA phases
+// leave idle, and the separate K3 launch disappears.
+template <int PITCH, bool PAIR>
+__global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta, FinishArgs fa) {
   using G = SG<PITCH>;
   const MulArgs& a = ta.m;
   extern __shared__ __align__(1024) unsigned char ssm_raw[];
   const int tid = threadIdx.x, lane = tid & 31;
   const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);  // warp-uniform for the compiler
-  const int z = blockIdx.x / ta.ntiles, t = blockIdx.x % ta.ntiles;
   unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
   const int KS = ta.KS;
   unsigned char* abuf = ssm;                                     // swizzled a-window
@@ -311,11 +328,12 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
 
   // operand roles: a slides (longer), b goes through the table (shorter)
   const bool sw = a.mb > a.ma;
-  const uint32_t* Ag = sw ? a.B + (long long)z * a.b_stride : a.A + (long long)z * a.a_stride;
-  const uint32_t* Bg = sw ? a.A + (long long)z * a.a_stride : a.B + (long long)z * a.b_stride;
   const int mA = sw ? a.mb : a.ma, mB = sw ? a.ma : a.mb;
   const TcsDims d = tcs_dims<PITCH>(mA, mB);
   const int mp = a.ma + a.mb;
+  const int t = PAIR ? 0 : (int)(blockIdx.x % ta.ntiles);
+  const int nz = PAIR ? fa.nprod_pair : 1;
+  const long long z0 = PAIR ? (long long)blockIdx.x * fa.nprod_pair : (long long)(blockIdx.x / ta.ntiles);
   const int k0 = t * G::T;
   int slo, shi;
   tcs_tile_steps<PITCH>(d, t, slo, shi);
@@ -329,126 +347,152 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta) {
     mbar_init(smem_u32(&sh.bar_mma), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-
-  const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
   const uint32_t abase = smem_u32(abuf);
   uint32_t tmem = 0u;
   uint32_t phase = 0u;
-  bool first = true;
-  for (int sb = slo; sb < shi; sb += KS) {
-    const int se = min(shi, sb + KS);
+  bool have_tmem = false;
+  constexpr int LPT = G::LPT;
+
+  for (int zi = 0; zi < nz; zi++) {
+    const long long z = z0 + zi;
+    const uint32_t* Ag = sw ? a.B + z * a.b_stride : a.A + z * a.a_stride;
+    const uint32_t* Bg = sw ? a.A + z * a.a_stride : a.B + z * a.b_stride;
+    const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+    bool first = true;
+    for (int sb = slo; sb < shi; sb += KS) {
+      const int se = min(shi, sb + KS);
+      if (!first) {
+        // the previous chunk's MMAs still read the buffers (warp 0 polls, the
+        // others join at the barrier)
+        if (warp == 0) mbar_wait_warp(smem_u32(&sh.bar_mma), phase);
+        __syncthreads();
+        phase ^= 1u;
+      }
+      {
+        const TcsChunk<PITCH> ck(d, k0, sb, se);
+        TcsRegs R;
+        tcs_load<PITCH>(R, ck, Ag, Bg, mA, mB, a16, tid);
+        tcs_store<PITCH>(R, ck, abuf, braw, tid);
+        __syncthreads();
+        tcs_table<PITCH>(ck, d, braw, tab, tid);
+      }
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (!have_tmem) {
+        tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
+        have_tmem = true;
+      }
+      if (warp == 0) {
+        uint64_t ad = sdesc_lt(abase, 16, 8 * PITCH, G::LT);
+        uint64_t bd = sdesc(smem_u32(tab), 256, 128);
+        // K-step s accumulates into chain (s - slo) & (nch - 1): with more than
+        // 64 KB of b the u32 sums are exact only per half of the K-steps (at
+        // most 65536 byte products < 2^16 each); the epilogue adds the chains
+        const int nch = ta.nch;
+        for (int s = sb; s < se; s++) {
+          const uint32_t ch = (uint32_t)(s - slo) & (uint32_t)(nch - 1);
+          mma_i8_elect(tmem + ch * G::N, ad, bd, G::IDESC, (s - slo) >= nch ? 1u : 0u);
+          ad += 2;   // + 32 bytes
+          bd += 32;  // + 512 bytes
+        }
+        mma_commit_elect(smem_u32(&sh.bar_mma));
+      }
+      first = false;
+    }
     if (!first) {
-      // the previous chunk's MMAs still read the buffers
-      mbar_wait(smem_u32(&sh.bar_mma), phase);
+      if (warp == 0) mbar_wait_warp(smem_u32(&sh.bar_mma), phase);
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncthreads();
       phase ^= 1u;
     }
-    {
-      const TcsChunk<PITCH> ck(d, k0, sb, se);
-      TcsRegs R;
-      tcs_load<PITCH>(R, ck, Ag, Bg, mA, mB, a16, tid);
-      tcs_store<PITCH>(R, ck, abuf, braw, tid);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (!have_tmem) {  // no K-step touches this tile (cannot happen for t < ntiles; kept for safety)
       __syncthreads();
-      tcs_table<PITCH>(ck, d, braw, tab, tid);
+      tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
+      have_tmem = true;
     }
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+
+    // ---- epilogue: lane m = tid owns limbs [LPT m, LPT m + LPT) of the tile
+    uint32_t dg[LPT];
+    // (a tile with fewer K-steps than chains never wrote the later chains)
+    const unsigned long long cout =
+        tcs_limbs<PITCH>(tmem + ((uint32_t)(32 * warp) << 16), min(ta.nch, shi - slo), !first, dg);
+    unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
+    if (lane == 31) sh.s_cout[warp] = cout;
+    uint32_t ones = 0xFFFFFFFFu;
+#pragma unroll
+    for (int q = 1; q < LPT; q++) ones &= dg[q];
+    // (also orders this product's TMEM reads before the next product's MMAs)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    if (first) tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
-    if (warp == 0) {
-      uint64_t ad = sdesc_lt(abase, 16, 8 * PITCH, G::LT);
-      uint64_t bd = sdesc(smem_u32(tab), 256, 128);
-      // K-step s accumulates into chain (s - slo) & (nch - 1): with more than
-      // 64 KB of b the u32 sums are exact only per half of the K-steps (at
-      // most 65536 byte products < 2^16 each); the epilogue adds the chains
-      const int nch = ta.nch;
-      for (int s = sb; s < se; s++) {
-        const uint32_t ch = (uint32_t)(s - slo) & (uint32_t)(nch - 1);
-        mma_i8_elect(tmem + ch * G::N, ad, bd, G::IDESC, (s - slo) >= nch ? 1u : 0u);
-        ad += 2;   // + 32 bytes
-        bd += 32;  // + 512 bytes
-      }
-      mma_commit_elect(smem_u32(&sh.bar_mma));
+    if (lane == 0) xin = warp ? sh.s_cout[warp - 1] : 0ull;
+    // overflow of (digits + xin + o) past the lane's LPT limbs, o in {0,1} from the previous lane
+    const unsigned long long s0 = (unsigned long long)dg[0] + xin;
+    const bool all1 = ones == 0xFFFFFFFFu;
+    const uint32_t gg = all1 && (s0 >> 32) != 0ull;
+    const uint32_t pp = all1 && ((s0 + 1ull) >> 32) != 0ull;
+    uint32_t F = gg | (pp << 1);
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
+      if (lane >= dd) F = cm2(F, y);
     }
-    first = false;
-  }
-  if (!first) mbar_wait(smem_u32(&sh.bar_mma), phase);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  if (first) {  // no K-step touches this tile (cannot happen for t < ntiles; kept for safety)
+    if (lane == 31) sh.warp_map[warp] = F;
     __syncthreads();
-    tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
-  }
-
-  // ---- epilogue: lane m = tid owns limbs [LPT m, LPT m + LPT) of the tile
-  constexpr int LPT = G::LPT;
-  uint32_t dg[LPT];
-  // (a tile with fewer K-steps than chains never wrote the later chains)
-  const unsigned long long cout =
-      tcs_limbs<PITCH>(tmem + ((uint32_t)(32 * warp) << 16), min(ta.nch, shi - slo), !first, dg);
-  unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
-  if (lane == 31) sh.s_cout[warp] = cout;
-  uint32_t ones = 0xFFFFFFFFu;
+    uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
+    uint32_t Wm = CM2_ID;
+    for (int w = 0; w < warp; w++) Wm = cm2(sh.warp_map[w], Wm);
+    // the tile's carry-in is 0: evaluate the composed maps at 0
+    E = lane ? cm2(E, Wm) : Wm;
+    const uint32_t Fin = cm2(F, Wm);
+    unsigned long long acc = s0 + (E & 1u);
+    dg[0] = (uint32_t)acc;
 #pragma unroll
-  for (int q = 1; q < LPT; q++) ones &= dg[q];
-  __syncthreads();
-  if (lane == 0) xin = warp ? sh.s_cout[warp - 1] : 0ull;
-  // overflow of (digits + xin + o) past the lane's LPT limbs, o in {0,1} from the previous lane
-  const unsigned long long s0 = (unsigned long long)dg[0] + xin;
-  const bool all1 = ones == 0xFFFFFFFFu;
-  const uint32_t gg = all1 && (s0 >> 32) != 0ull;
-  const uint32_t pp = all1 && ((s0 + 1ull) >> 32) != 0ull;
-  uint32_t F = gg | (pp << 1);
-#pragma unroll
-  for (int dd = 1; dd < 32; dd <<= 1) {
-    const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
-    if (lane >= dd) F = cm2(F, y);
-  }
-  if (lane == 31) sh.warp_map[warp] = F;
-  __syncthreads();
-  uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
-  uint32_t Wm = CM2_ID;
-  for (int w = 0; w < warp; w++) Wm = cm2(sh.warp_map[w], Wm);
-  // the tile's carry-in is 0: evaluate the composed maps at 0
-  E = lane ? cm2(E, Wm) : Wm;
-  const uint32_t Fin = cm2(F, Wm);
-  unsigned long long acc = s0 + (E & 1u);
-  dg[0] = (uint32_t)acc;
-#pragma unroll
-  for (int q = 1; q < LPT; q++) {
-    acc = (acc >> 32) + dg[q];
-    dg[q] = (uint32_t)acc;
-  }
-  uint32_t* Pz = a.P + (long long)z * a.p_stride;
-  const int L = t * G::LIMBS + LPT * tid;
-  if (L + LPT <= mp) {
-#pragma unroll
-    for (int q = 0; q < LPT / 4; q++)
-      *reinterpret_cast<uint4*>(Pz + L + 4 * q) = make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
-  } else {
-#pragma unroll
-    for (int q = 0; q < LPT; q++)
-      if (L + q < mp) Pz[L + q] = dg[q];
-  }
-  // band spills: zero inside the tile, the tile's carry on its top band
-  {
-    const int b0 = G::BPT * t, b1 = min(a.nbands, G::BPT * (t + 1));
-    if (tid < b1 - b0 && tid != G::BPT - 1) {
-      unsigned long long* sp = a.spill + ((long long)z * a.nbands + b0 + tid) * 2;
-      sp[0] = 0ull;
-      sp[1] = 0ull;
+    for (int q = 1; q < LPT; q++) {
+      acc = (acc >> 32) + dg[q];
+      dg[q] = (uint32_t)acc;
     }
-    if (tid == 127 && b0 + G::BPT - 1 < b1) {
-      unsigned long long* sp = a.spill + ((long long)z * a.nbands + b0 + G::BPT - 1) * 2;
-      sp[0] = cout + (Fin & 1u);
-      sp[1] = 0ull;
+    uint32_t* Pz = a.P + z * a.p_stride;
+    const int L = t * G::LIMBS + LPT * tid;
+    if (L + LPT <= mp) {
+#pragma unroll
+      for (int q = 0; q < LPT / 4; q++)
+        *reinterpret_cast<uint4*>(Pz + L + 4 * q) = make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
+    } else {
+#pragma unroll
+      for (int q = 0; q < LPT; q++)
+        if (L + q < mp) Pz[L + q] = dg[q];
     }
+    // band spills: zero inside the tile, the tile's carry on its top band
+    {
+      const int b0 = G::BPT * t, b1 = min(a.nbands, G::BPT * (t + 1));
+      if (tid < b1 - b0 && tid != G::BPT - 1) {
+        unsigned long long* sp = a.spill + (z * a.nbands + b0 + tid) * 2;
+        sp[0] = 0ull;
+        sp[1] = 0ull;
+      }
+      if (tid == 127 && b0 + G::BPT - 1 < b1) {
+        unsigned long long* sp = a.spill + (z * a.nbands + b0 + G::BPT - 1) * 2;
+        sp[0] = cout + (Fin & 1u);
+        sp[1] = 0ull;
+      }
+    }
+  }
+  if (PAIR) {
+    // K3 for this pair: the products and spills above were written by this
+    // CTA (visible after the barrier; read with plain loads, not ld.global.nc)
+    __syncthreads();
+    u32* fbuf = reinterpret_cast<u32*>(abuf) + warp * (FIN_HALO + FW_CH);
+    if (warp < fa.ns)
+      finish_warp_stream<GlobalDigitSink, false>(fa, (int)blockIdx.x, warp, fbuf, GlobalDigitSink{&fa});
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   if (warp == 0)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(ta.nch * G::N)));
 }
-
 
 // ------------------------------------------------- persistent, specialized
 // The same tiles through a persistent CTA (one per SM): work items (product,
@@ -557,7 +601,7 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
     }
     while (valid) {
       const int st = (int)(sc % NS);
-      if (sc >= NS) mbar_wait(smem_u32(&sh.bar_empty[st]), (uint32_t)(((sc / NS) - 1) & 1));
+      if (sc >= NS) mbar_wait_warp(smem_u32(&sh.bar_empty[st]), (uint32_t)(((sc / NS) - 1) & 1));
       unsigned char* abuf = ssm + (size_t)st * stage_bytes;
       unsigned char* braw = abuf + tcs_abytes<PITCH>(KS);
       unsigned char* tab = braw + tcs_rawbytes<PITCH>(KS);
@@ -591,13 +635,13 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
         int slo, shi;
         tcs_tile_steps<PITCH>(d, t, slo, shi);
         const int buf = (int)(ac & 1);
-        if (ac >= 2) mbar_wait(smem_u32(&sh.bar_acc_empty[buf]), (uint32_t)(((ac >> 1) - 1) & 1));
+        if (ac >= 2) mbar_wait_warp(smem_u32(&sh.bar_acc_empty[buf]), (uint32_t)(((ac >> 1) - 1) & 1));
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t dcol = tmem + (uint32_t)(buf * ta.nch * G::N);
         const int nch = ta.nch;
         for (int sb = slo; sb < shi; sb += KS, sc++) {
           const int st = (int)(sc % NS);
-          mbar_wait(smem_u32(&sh.bar_full[st]), (uint32_t)((sc / NS) & 1));
+          mbar_wait_warp(smem_u32(&sh.bar_full[st]), (uint32_t)((sc / NS) & 1));
           asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
           const uint32_t sbase = smem_u32(ssm + (size_t)st * stage_bytes);
           uint64_t ad = sdesc_lt(sbase, 16, 8 * PITCH, G::LT);
@@ -625,7 +669,7 @@ __global__ void __launch_bounds__(288, 1) k_tcswz_p(TcsArgs ta) {
       int slo, shi;
       tcs_tile_steps<PITCH>(d, t, slo, shi);
       const int buf = (int)(ac & 1);
-      mbar_wait(smem_u32(&sh.bar_acc_full[buf]), (uint32_t)((ac >> 1) & 1));
+      mbar_wait_warp(smem_u32(&sh.bar_acc_full[buf]), (uint32_t)((ac >> 1) & 1));
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       uint32_t dg[LPT];
       const unsigned long long cout = tcs_limbs<PITCH>(
@@ -756,7 +800,7 @@ bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
 }
 
 template <int PITCH>
-cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
+cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st, const FinishArgs* fin) {
   TcsArgs ta;
   memset(&ta, 0, sizeof ta);
   ta.m = a;
@@ -799,14 +843,27 @@ cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
     k_tcswz_p<PITCH><<<(unsigned)grid, 288, p.smem, st>>>(ta);
     return cudaGetLastError();
   }
+  if (fin) {  // one CTA per pair, K3 fused (single-tile products)
+    static size_t s_set2 = 0;
+    if (p.smem > 48 * 1024 && p.smem > s_set2) {
+      cudaError_t e =
+          cudaFuncSetAttribute(k_tcswz<PITCH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+      if (e != cudaSuccess) return e;
+      s_set2 = p.smem;
+    }
+    k_tcswz<PITCH, true><<<(unsigned)(a.nprod / fin->nprod_pair), 128, p.smem, st>>>(ta, *fin);
+    return cudaGetLastError();
+  }
   static size_t s_set1 = 0;
   if (p.smem > 48 * 1024 && p.smem > s_set1) {
-    cudaError_t e = cudaFuncSetAttribute(k_tcswz<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+    cudaError_t e = cudaFuncSetAttribute(k_tcswz<PITCH, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
     if (e != cudaSuccess) return e;
     s_set1 = p.smem;
   }
   const long long grid = (long long)a.nprod * p.ntiles;
-  k_tcswz<PITCH><<<(unsigned)grid, 128, p.smem, st>>>(ta);
+  FinishArgs nofin;
+  memset(&nofin, 0, sizeof nofin);
+  k_tcswz<PITCH, false><<<(unsigned)grid, 128, p.smem, st>>>(ta, nofin);
   return cudaGetLastError();
 }
 
@@ -821,15 +878,18 @@ bool tcs_plan(int ma, int mb, int pitch, int persist, TcsPlan& p) {
   }
 }
 
-cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st) {
+cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st, const FinishArgs* fin) {
   if (a.nprod == 0) return cudaSuccess;
+  if (fin && (p.persist || p.ntiles != 1 || fin->ns > 4 || fin->nprod_pair < 1 || a.nprod % fin->nprod_pair))
+    return cudaErrorInvalidValue;
   if (tcs_env("KMX_TC_VERBOSE", 0))
-    fprintf(stderr, "kmx_tcs: ma=%d mb=%d nprod=%d -> pitch=%d KS=%d tiles=%d smem=%zu mmas=%lld%s NS=%d\n", a.ma, a.mb,
-            a.nprod, p.pitch, p.KS, p.ntiles, p.smem, p.mmas, p.persist ? " persistent" : "", p.NS);
+    fprintf(stderr, "kmx_tcs: ma=%d mb=%d nprod=%d -> pitch=%d KS=%d tiles=%d smem=%zu mmas=%lld%s%s NS=%d\n", a.ma, a.mb,
+            a.nprod, p.pitch, p.KS, p.ntiles, p.smem, p.mmas, p.persist ? " persistent" : "",
+            fin ? " pair CTAs + fused finish" : "", p.NS);
   switch (p.pitch) {
-    case 32: return launch_p<32>(a, p, st);
-    case 64: return launch_p<64>(a, p, st);
-    default: return launch_p<128>(a, p, st);
+    case 32: return launch_p<32>(a, p, st, fin);
+    case 64: return launch_p<64>(a, p, st, fin);
+    default: return launch_p<128>(a, p, st, fin);
   }
 }
 

@@ -23,6 +23,7 @@ SETTINGS = [
     {"KMX_FINISH_CHUNKS": "0", "KMX_SPLIT": "1"},  # warp-per-stream finish; every batch split over two streams
     {"KMX_TC": "0"},            # integer-pipe multiply everywhere
     {"KMX_TC": "1"},            # tensor-core multiply wherever supported (incl. tiny operands): swizzled-window kernel
+    {"KMX_TC": "1", "KMX_FUSE_FIN": "1"},  # K2 + K3 fused in pair CTAs wherever the products are single tiles
     {"KMX_TC": "1", "KMX_TCS": "0"},  # the tiled tensor-core kernel (k_tcmul) wherever supported
     {"KMX_TC": "1", "KMX_TCS": "32"},  # swizzled-window kernel, pitch 32 (N = 32), one-shot CTAs
     {"KMX_TC": "1", "KMX_TCS": "128", "KMX_TCS_KS": "24"},  # pitch 128, many short K-chunks per tile

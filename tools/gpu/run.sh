@@ -39,7 +39,7 @@ if has launches; then
     python bench.py --steps 3 --warmup 3 --quick > $O/${TAG}_launches.log 2>&1; echo "launches=$?"
 fi
 if has full; then
-  KREGEX=${KREGEX:-"regex:k_pack|k_tcmul|k_finish|k_recon|k_kara"}
+  KREGEX=${KREGEX:-"regex:k_pack|k_tcmul|k_tcswz|k_finish|k_recon|k_kara"}
   timeout 300 python bench.py --steps 3 --warmup 3 --quick > /dev/null 2>&1 && \
   timeout 1200 ncu --set full --clock-control none --import-source on -k "$KREGEX" -c ${NCU_COUNT:-6} \
     -o $O/${TAG}_full python bench.py --steps 3 --warmup 3 --quick > $O/${TAG}_full.log 2>&1; echo "full=$?"
