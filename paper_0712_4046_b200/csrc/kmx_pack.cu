@@ -42,9 +42,13 @@ bool pack_w1_ok(const PackArgs& a);
 bool pack_seg_wanted(const PackArgs& a, int batch);
 cudaError_t launch_pack_seg(const PackArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_pack_w1(const PackArgs& a, int batch, bool paired, cudaStream_t st);
+bool pack_cf_ok(const PackArgs& a, int batch);
+cudaError_t launch_pack_cf(const PackArgs& a, int batch, cudaStream_t st);
 
 cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
   static const int use_pair = getenv("KMX_PACK_PAIR") ? atoi(getenv("KMX_PACK_PAIR")) : 1;
+  // large carry-free unsigned packs (ks1 / ks2): the streaming kernel (kmx_packcf.cu)
+  if (pack_cf_ok(a, batch)) return launch_pack_cf(a, batch, st);
   // long operands, small batches: segments of every operand on separate CTAs
   if (pack_seg_wanted(a, batch)) return launch_pack_seg(a, batch, st);
   // one-word coefficients at 2N >= 32, + and - operands from one staged vector
