@@ -13,8 +13,9 @@
 // coefficient a thread meets; the operand's bit length (meta, for MulStats) is
 // a block max + one atomicMax per CTA.
 //
-// Used for large jobs (>= 2^20 packed limbs per call); the block-per-operand
-// kernels of kmx_pack.cu keep the small ones (c1) where their staged vectors win.
+// Used for large jobs (>= 2^20 packed limbs per call) and for multi-word
+// coefficients on operands of >= 256 limbs; the block-per-operand kernels of
+// kmx_pack.cu keep the rest, where their staged vectors win.
 #include <cstdlib>
 
 #include "kmx_common.cuh"
@@ -137,7 +138,9 @@ bool pack_cf_ok(const PackArgs& a, int batch) {
     if (a.op[i].meta_pair_stride != a.op[0].meta_pair_stride || a.op[i].meta < a.op[0].meta ||
         a.op[i].meta - a.op[0].meta >= a.op[0].meta_pair_stride)
       return false;
-  return force == 1 || limbs >= (1LL << 20);
+  // measured (config-5 sweep with KMX_PACK_CF=0 / 1): large calls always; small ones only with
+  // multi-word coefficients on operands of >= 256 limbs (3-10% faster; one-word or short: 3-25% slower)
+  return force == 1 || limbs >= (1LL << 20) || (a.in_words >= 2 && a.op[0].m >= 256 && a.op[0].len >= 64);
 }
 
 cudaError_t launch_pack_cf(const PackArgs& a, int batch, cudaStream_t st) {
