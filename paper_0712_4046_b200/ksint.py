@@ -16,7 +16,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import ReconstructionError, check, lib
-from .kstypes import CoeffVec, KsParams, MulConfig, MulStats, OverlapDigits
+from .kstypes import DEFAULT_MUL_CONFIG, CoeffVec, KsParams, MulConfig, MulStats, OverlapDigits
 from .words import ints_to_words, words_to_ints
 
 __all__ = ["KsParams", "OverlapDigits", "ReconstructionError", "derive_params", "ks1_mul",
@@ -37,7 +37,54 @@ def derive_params(len_f: int, len_g: int, coeff_bits: int) -> KsParams:
     return KsParams(len_f, len_g, coeff_bits, e, full, coeff_bits + (e + 1) // 2, (full + 3) // 4)
 
 
-def _ks(variant: int, f: CoeffVec, g: CoeffVec, stats: MulStats | None) -> CoeffVec:
+def _nlimbs64(x: int) -> int:
+    return (x.bit_length() + 63) // 64
+
+
+def _mul_count(x: int, y: int, config: MulConfig) -> int:
+    """The 64-bit word products ``bignat.mul(x, y, stats, config)`` counts
+    (bignat.py:323-371): the classical product of an m x n operand pair counts
+    m*n; above ``karatsuba_threshold`` the three-product recursion splits at
+    half the longer operand and counts its leaves.  Only operand LENGTHS are
+    followed here (splits and the two sums per node) -- no product is formed
+    on the host."""
+    xl, yl = _nlimbs64(x), _nlimbs64(y)
+    thr = config.karatsuba_threshold
+    if config.classical_only or xl <= thr or yl <= thr:
+        return xl * yl
+    half = (max(xl, yl) + 1) // 2
+    shift = 64 * half
+    mask = (1 << shift) - 1
+    x0, x1, y0, y1 = x & mask, x >> shift, y & mask, y >> shift
+    # (inside the recursion the reference tests only the threshold, bignat.py:346-347)
+    rec = MulConfig(karatsuba_threshold=thr, classical_only=False)
+    return _mul_count(x0, y0, rec) + _mul_count(x1, y1, rec) + _mul_count(x0 + x1, y0 + y1, rec)
+
+
+def _stats_count(variant: int, f: CoeffVec, g: CoeffVec, config: MulConfig) -> int:
+    """MulStats.limb_products of the reference's ksN_mul(f, g, config=config)
+    (ksint.py:219-348): the operands are the GPU packs (K1), the count follows
+    the reference's dispatch."""
+    from .pack import pack, pack_negated, pack_negated_reversed, pack_reversed
+    p = derive_params(len(f.coeffs), len(g.coeffs), max(f.width_bound_bits, g.width_bound_bits))
+    if variant == 4:
+        w = 2 * p.width_quarter
+        if not p.coeff_product_bound() < (1 << w) * ((1 << w) - 1):
+            variant = 1  # ksint.py:301-302
+        elif p.out_len == 1:
+            return _mul_count(f.coeffs[0], g.coeffs[0], config)
+    if variant == 1:
+        n, kinds = p.width_full, (pack,)
+    elif variant == 2:
+        n, kinds = p.width_half, (pack, pack_reversed)
+    elif variant == 3:
+        n, kinds = p.width_half, (pack, pack_negated)
+    else:
+        n, kinds = p.width_quarter, (pack, pack_negated, pack_reversed, pack_negated_reversed)
+    return sum(_mul_count(abs(fn(f, n)), abs(fn(g, n)), config) for fn in kinds)
+
+
+def _ks(variant: int, f: CoeffVec, g: CoeffVec, stats: MulStats | None, config: MulConfig | None = None) -> CoeffVec:
     b = max(f.width_bound_bits, g.width_bound_bits)
     words = (b + 31) // 32
     lf, lg = len(f.coeffs), len(g.coeffs)
@@ -52,7 +99,11 @@ def _ks(variant: int, f: CoeffVec, g: CoeffVec, stats: MulStats | None) -> Coeff
                                _lib.ptr(h), ow, 0, ctypes.byref(lp) if stats is not None else None)
     check(rc, f"ks{variant}_mul")
     if stats is not None:
-        stats.limb_products += int(lp.value)
+        cfg = config if config is not None else DEFAULT_MUL_CONFIG
+        if cfg.classical_only:
+            stats.limb_products += int(lp.value)  # counted on the device from K1's bit lengths
+        else:
+            stats.limb_products += _stats_count(variant, f, g, cfg)
     return CoeffVec(tuple(words_to_ints(h)), 2 * b + _e(lf, lg))
 
 
@@ -63,7 +114,7 @@ def _e(lf: int, lg: int) -> int:
 def ks1_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
             config: MulConfig | None = None) -> CoeffVec:
     """Standard substitution: one full-width product (ksint.py:219-226)."""
-    return _ks(1, f, g, stats)
+    return _ks(1, f, g, stats, config)
 
 
 def ks2_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
@@ -72,14 +123,14 @@ def ks2_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
     reconstruction (ksint.py:229-247).  ``parallel`` is accepted for
     signature compatibility: the sub-products always run concurrently on the
     GPU, with bit-identical results."""
-    return _ks(2, f, g, stats)
+    return _ks(2, f, g, stats, config)
 
 
 def ks3_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
             config: MulConfig | None = None, parallel: bool = False) -> CoeffVec:
     """Negated variant: products at +-2^N, half-sum / half-difference
     (ksint.py:257-279)."""
-    return _ks(3, f, g, stats)
+    return _ks(3, f, g, stats, config)
 
 
 def ks4_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
@@ -87,7 +138,7 @@ def ks4_mul(f: CoeffVec, g: CoeffVec, *, stats: MulStats | None = None,
     """Four-point variant: quarter-width products at +-2^N and +-2^-N, even/odd
     split, two overlap reconstructions; KS1 fallback when the bound is not
     certified (ksint.py:289-348)."""
-    return _ks(4, f, g, stats)
+    return _ks(4, f, g, stats, config)
 
 
 def reconstruct_overlapped(d: OverlapDigits, *, with_carries: bool = False):

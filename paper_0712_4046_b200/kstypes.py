@@ -44,9 +44,12 @@ class CoeffVec:
 
 @dataclass
 class MulStats:
-    """Counter of 64-bit word x word products (bignat.py:57-68).  The GPU path
-    reports the classical count of the normalized packed operands,
-    sum limbs64(x) * limbs64(y) over the sub-products (bignat.py:327-330)."""
+    """Counter of 64-bit word x word products (bignat.py:57-68), as the
+    reference reports it for the given MulConfig: with ``classical_only`` the
+    sum of limbs64(x) * limbs64(y) over the sub-products (bignat.py:327-330,
+    counted on the device), otherwise the leaves of the reference's Karatsuba
+    recursion (bignat.py:344-371; ksint._mul_count follows the operand
+    lengths of the GPU-packed operands)."""
 
     limb_products: int = 0
 
@@ -57,9 +60,8 @@ class MulStats:
 @dataclass(frozen=True)
 class MulConfig:
     """Dispatch policy of the reference's bignum multiply (bignat.py:71-84).
-    Accepted for signature compatibility; results never depend on it
-    (pkg/tests/test_ksint.py:93-112), and the GPU multiply kernels choose
-    their own tiling."""
+    Results never depend on it (pkg/tests/test_ksint.py:93-112) and the GPU
+    multiply kernels choose their own tiling; MulStats follows it."""
 
     karatsuba_threshold: int = 16
     classical_only: bool = False

@@ -59,3 +59,8 @@ def bivar_mod_cases():
         out.append((int(c["n"]), [[int(x) for x in r] for r in c["f"]], [[int(x) for x in r] for r in c["g"]],
                     [[int(x) for x in r] for r in c["h"]], c["missing_halve"]))
     return out
+
+
+def stats_cases():
+    """(f, g, b, {"default" | "thr2" | "classical": [ks1, ks2, ks3, ks4 counts]}) from the reference."""
+    return [(_ints(c["f"]), _ints(c["g"]), c["b"], c["counts"]) for c in _load("stats_golden.json.gz")]

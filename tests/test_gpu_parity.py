@@ -69,6 +69,23 @@ def test_dropin_stats_match_reference_counts(kmx):
     assert counts == {1: 173056, 2: 86528, 3: 86528, 4: 44100}
 
 
+def test_dropin_stats_follow_mulconfig(kmx):
+    # MulStats.limb_products for the default MulConfig (Karatsuba above 16 limbs),
+    # karatsuba_threshold=2 and classical_only, against counts the reference
+    # reported (tests/golden/make_golden_stats.py; bignat.py:323-371)
+    cfgs = {"default": None, "thr2": kmx.MulConfig(karatsuba_threshold=2),
+            "classical": kmx.MulConfig(classical_only=True)}
+    for f, g, b, counts in G.stats_cases():
+        F, Gv = kmx.CoeffVec(tuple(f), b), kmx.CoeffVec(tuple(g), b)
+        for name, cfg in cfgs.items():
+            got = []
+            for fn in (kmx.ks1_mul, kmx.ks2_mul, kmx.ks3_mul, kmx.ks4_mul):
+                st = kmx.MulStats()
+                fn(F, Gv, stats=st, config=cfg)
+                got.append(st.limb_products)
+            assert got == counts[name], (len(f), len(g), b, name)
+
+
 def test_dropin_reconstruct_golden(kmx):
     for fwd, rev, w, h in G.recon_cases():
         got = kmx.reconstruct_overlapped(kmx.OverlapDigits(tuple(fwd), tuple(rev), w))

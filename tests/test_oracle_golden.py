@@ -142,3 +142,36 @@ def test_oracle_uni_schoolbook_matches_convolution():
         assert O.uni_schoolbook(a, b) == O.convolve_exact(a, b) == O.schoolbook(a, b)
     tag, f, g, h = G.bivar_cases()[3]
     assert O.bks(4, f, g, umul=O.uni_schoolbook) == h
+
+
+def test_mul_count_follows_the_reference_recursion():
+    """ksint._mul_count (host: operand lengths of the Karatsuba recursion,
+    bignat.py:344-371) against the oracle's counted multiply on random and
+    all-ones operands, default and small thresholds."""
+    import random
+    from paper_0712_4046_b200.ksint import _mul_count
+    from paper_0712_4046_b200.kstypes import MulConfig
+    rng = random.Random(5)
+    for bits_x, bits_y in ((64, 64), (1024, 1024), (1100, 5000), (4096, 4000), (20000, 20000), (7, 30000)):
+        for x, y in ((rng.getrandbits(bits_x) | 1 << (bits_x - 1), rng.getrandbits(bits_y) | 1 << (bits_y - 1)),
+                     ((1 << bits_x) - 1, (1 << bits_y) - 1)):
+            for thr in (16, 2):
+                st = O.Counter()
+                O.mul(x, y, "karatsuba", st, threshold=thr)
+                assert _mul_count(x, y, MulConfig(karatsuba_threshold=thr)) == st.limb_products
+            st = O.Counter()
+            O.mul(x, y, "karatsuba", st, classical_only=True)
+            assert _mul_count(x, y, MulConfig(classical_only=True)) == st.limb_products
+
+
+def test_oracle_stats_golden():
+    """The oracle's counted multiply against MulStats values the reference
+    reported (default MulConfig and classical_only; tests/golden/make_golden_stats.py)."""
+    for f, g, b, counts in G.stats_cases():
+        for name, kw in (("default", {}), ("classical", {"classical_only": True})):
+            row = []
+            for v in (1, 2, 3, 4):
+                c = O.Counter()
+                O.ks_mul(v, f, g, b, stats=c, **kw)
+                row.append(c.limb_products)
+            assert row == counts[name], (len(f), len(g), b, name)
