@@ -65,6 +65,12 @@ bool use_tcj(int ma, int mb, long long nprod) {
   const int force = v && *v ? atoi(v) : -1;
   if (force == 0) return false;
   if (force < 0 && nprod >= 4LL * 148) return false;
+  // the swizzled-window kernel (kmx_tcs.cu) beats it at c1 too (ks2 / ks3 K2
+  // 16.8 -> 14.3 us, ks4 13.1 -> 12.8): chosen only where that kernel is off
+  if (force < 0) {
+    const char* ts = getenv("KMX_TCS");
+    if (!(ts && *ts && atoi(ts) == 0)) return false;
+  }
   return tcj_plan(ma, mb, nullptr, force < 0);
 }
 
