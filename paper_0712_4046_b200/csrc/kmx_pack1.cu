@@ -65,6 +65,37 @@ struct Cur1 {
   }
 };
 
+// Streaming reader of one parity stream of one-word coefficients (S >= 32,
+// b <= 32): a 64-bit accumulator holds the stream from the current limb's
+// first bit; `filled` is where the next coefficient starts.  One compare,
+// and at most one load + 64-bit shift / or, per digit -- against a window
+// extraction (two loads, two shifts, index arithmetic) per digit with the
+// cursor above.
+struct Str1 {
+  unsigned long long acc;
+  int filled, idx;
+  __device__ __forceinline__ void init(int q, int off, int S, int par, const u32* sc) {
+    const int x = 32 * q - off;  // >= -off > -S
+    const int m = x >= 0 ? x / S : -1;
+    const int t = x - m * S;     // bits into coefficient m (0 <= t < S)
+    const u32 c = m >= 0 ? sc[2 * m + par] : 0u;
+    acc = t < 32 ? (unsigned long long)(c >> t) : 0ull;
+    filled = S - t;
+    idx = 2 * (m + 1) + par;
+  }
+  __device__ __forceinline__ u32 next(int S, const u32* sc) {
+    if (filled < 32) {
+      acc |= (unsigned long long)sc[idx] << filled;
+      idx += 2;
+      filled += S;
+    }
+    const u32 d = (u32)acc;
+    acc >>= 32;
+    filled -= 32;
+    return d;
+  }
+};
+
 // {0,1}-carry map of a lane's digits: bit0 = carry out for carry-in 0,
 // bit1 = for carry-in 1 (kmx_tcutil.cuh cm2 encoding); compose(later, earlier)
 __device__ __forceinline__ u32 cmp2(u32 later, u32 earlier) {
@@ -197,20 +228,35 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
   for (int c0 = 0; c0 < m; c0 += W1_CH) {
     const int q0 = c0 + lane * W1_V;
     Cur1 ce, co;
-    ce.init(q0, 0, S);
-    co.init(q0, N, S);
+    Str1 se, so;
+    if (IW == 1) {
+      if (q0 < m) {
+        se.init(q0, 0, S, 0, sc);
+        so.init(q0, N, S, 1, sc);
+      }
+    } else {
+      ce.init(q0, 0, S);
+      co.init(q0, N, S);
+    }
     u32 dp[W1_V], dn[W1_V];
     u32 cp = 0u, cn = 0u;  // local carry (+) / borrow (-) with carry-in 0
     u32 allFp = 0xffffffffu, allZn = 0u;
 #pragma unroll
     for (int v = 0; v < W1_V; v++) {
       u32 e = 0u, ov = 0u;
-      if (q0 + v < m) {
-        e = ce.template bits<IW>(sc, 0, S, b);
-        ov = co.template bits<IW>(sc, 1, S, b);
+      if (IW == 1) {
+        if (q0 + v < m) {
+          e = se.next(S, sc);
+          ov = so.next(S, sc);
+        }
+      } else {
+        if (q0 + v < m) {
+          e = ce.template bits<IW>(sc, 0, S, b);
+          ov = co.template bits<IW>(sc, 1, S, b);
+        }
+        ce.next(S);
+        co.next(S);
       }
-      ce.next(S);
-      co.next(S);
       // + : e + o + carry
       const unsigned long long sp = (unsigned long long)e + ov + cp;
       dp[v] = (u32)sp;
