@@ -61,7 +61,12 @@ cudaError_t launch_pack(const PackArgs& a, int batch, cudaStream_t st) {
     for (int i = 0; i < a.nops; i++) mmax0 = a.op[i].m > mmax0 ? a.op[i].m : mmax0;
     static const int w1_force = getenv("KMX_PACK_W1") ? atoi(getenv("KMX_PACK_W1")) : -1;
     const bool paired = use_pair && pairable(a);
-    if (pack_w1_ok(a) && (w1_force == 1 || (paired && mmax0 <= 1024)))
+    // one-word coefficients read through the streaming accumulator (Str1): the
+    // warp kernel also wins on longer paired jobs (c2 ks3, m = 1184: pack 37.5 ->
+    // 30.1 us).  Single jobs stay on the block kernel: the warp kernel is 5-15%
+    // slower there at small n (config-5 sweep) and at m = 2367 (c2 ks1 35.0 vs 40.1)
+    const bool w1_auto = paired && mmax0 <= (a.in_words == 1 ? 2048 : 1024);
+    if (pack_w1_ok(a) && (w1_force == 1 || w1_auto))
       return launch_pack_w1(a, batch, paired, st);
   }
   int mmax = 0;
