@@ -152,6 +152,9 @@ struct KsPlan {
   int fin_chunks;  // 256-limb chunks of the longest finish stream (chunk-parallel finish maps)
 };
 
+// words per digit-stream slot, rounded to 16 bytes (the pair reconstruction loads digit pairs)
+static inline long long dslot_words(const KsPlan& p) { return ((long long)p.cnt_max * p.dwords + 3) & ~3LL; }
+
 size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 // optional per-kernel CUDA-event timing of run_plan (kmx_prof_*):
@@ -294,7 +297,7 @@ int make_plan(KsPlan& p, int variant, int batch, int lf, int lg, int b, int in_w
   p.off_prod = o; o = align256(o + (size_t)batch * p.P * p.ps * 4);
   p.off_spill = o; o = align256(o + (size_t)batch * p.P * p.nbands * 16);
   p.off_dbuf = o;
-  if (p.nrs) o = align256(o + (size_t)batch * p.dslots * p.cnt_max * p.dwords * 4);
+  if (p.nrs) o = align256(o + (size_t)batch * p.dslots * dslot_words(p) * 4);
   p.off_scr = o;
   if (p.sign) o = align256(o + (size_t)batch * (lf + lg + 2) * 8);
   {  // chunk-parallel finish: one carry-map byte per (stream, 256-limb chunk)
@@ -464,7 +467,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.spill = spill; fa.nbands = p.nbands; fa.band_cols = p.C;
   fa.meta = meta; fa.meta_per_pair = 4 * p.P; fa.mf_slot_stride = p.P;
   fa.h = h; fa.out_words = out_words; fa.h_pair_stride = (long long)p.out_len * out_words;
-  fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = (long long)p.cnt_max * p.dwords;
+  fa.dbuf = dbuf; fa.dwords = p.dwords; fa.dslot_stride = dslot_words(p);
   fa.dslots_pair = p.dslots; fa.err = err;
   fa.bias = bfix;
   fa.cmaps = (uint8_t*)(w + p.off_cmap);
@@ -495,7 +498,7 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   if (p.nrs) {
     for (int i = 0; i < p.nrs; i++) ra.s[i] = p.rs[i];
     ra.ns = p.nrs; ra.batch = p.batch; ra.W = p.W;
-    ra.dbuf = dbuf; ra.dwords = p.dwords; ra.dslot_stride = (long long)p.cnt_max * p.dwords;
+    ra.dbuf = dbuf; ra.dwords = p.dwords; ra.dslot_stride = dslot_words(p);
     ra.dslots_pair = p.dslots;
     ra.h = h; ra.out_words = out_words; ra.h_pair_stride = (long long)p.out_len * out_words;
     ra.err = err;

@@ -228,6 +228,9 @@ cudaError_t launch_mul(const MulArgs& a, cudaStream_t st);
 cudaError_t launch_conv(const ConvArgs& a, cudaStream_t st);
 cudaError_t launch_finish(const FinishArgs& a, int batch, cudaStream_t st);
 cudaError_t launch_recon(const ReconArgs& a, cudaStream_t st);
+// K4 with one CTA per pair for digits of at most 64 bits (kmx_recon2.cu)
+bool recon_pair_ok(const ReconArgs& a);
+cudaError_t launch_recon_pair(const ReconArgs& a, cudaStream_t st);
 // K3 + K4 fused for ks2 / ks4 when both apply (warp finish, staged
 // reconstruction); *used = false: nothing launched, run them separately
 cudaError_t launch_finrec(const FinishArgs& fa, const ReconArgs& ra, int batch, cudaStream_t st, bool* used);

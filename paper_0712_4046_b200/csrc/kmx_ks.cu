@@ -1340,7 +1340,10 @@ cudaError_t launch_recon(const ReconArgs& a0, cudaStream_t st) {
   static const int seq = getenv("KMX_RECON_SEQ") ? atoi(getenv("KMX_RECON_SEQ")) : 0;
   // the one-thread-per-stream kernel handles the signed correction only for
   // digits of at most 64 bits (its multiword branch stores unsigned)
-  if (!a0.carries && !a0.sequential && !(seq && a0.dwords <= 2)) return launch_recon_par(a0, st);
+  if (!a0.carries && !a0.sequential && !(seq && a0.dwords <= 2)) {
+    if (recon_pair_ok(a0)) return launch_recon_pair(a0, st);
+    return launch_recon_par(a0, st);
+  }
   ReconArgs a = a0;
   a.rch = a.dwords >= 32 ? 1 : 32 / a.dwords;  // ~32 words per stream per array per chunk
   switch (a.dwords) {

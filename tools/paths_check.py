@@ -43,7 +43,8 @@ def main():
                 bad += 1
     rng = random.Random(77)
     shapes = [(64, 1024, 1024, 32, True), (2, 4096, 4096, 128, False), (40, 16, 16, 8, False),
-              (9, 300, 17, 64, False), (5, 1000, 1000, 256, False), (3, 8192, 8192, 8, False)]
+              (9, 300, 17, 64, False), (5, 1000, 1000, 256, False), (3, 8192, 8192, 8, False),
+              (6, 700, 333, 32, True), (4, 600, 601, 30, False), (3, 2049, 2048, 20, False)]
     for B, lf, lg, b, signed in shapes:
         if signed:
             fs = [[rng.randrange(-2**31, 2**31) for _ in range(lf)] for _ in range(B)]
