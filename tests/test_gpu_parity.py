@@ -109,6 +109,44 @@ def test_dropin_reconstruct_rejects(kmx):
         kmx.reconstruct_overlapped(kmx.OverlapDigits(tuple(fwd), tuple(rev), w))
 
 
+def test_dropin_reconstruct_long_streams(kmx):
+    # streams of >= 256 digits of at most 64 bits take the one-CTA-per-pair
+    # kernel (kmx_recon2.cu): round trips at both digit word counts, with 16-byte
+    # aligned and unaligned stream slots, full and ragged last segments, the
+    # extreme values, and the rejection of an inconsistent stream (ksint.py:137-179)
+    rng = random.Random(11)
+    for w, count in ((7, 256), (32, 300), (33, 257), (38, 1024), (50, 1001), (64, 513), (64, 2049), (19, 4100)):
+        top = (1 << w) * ((1 << w) - 1)
+        for kind in ("random", "max", "zero"):
+            if kind == "random":
+                vals = [rng.randrange(top) for _ in range(count)]
+            elif kind == "max":
+                vals = [top - 1] * count
+            else:
+                vals = [0] * count
+            fv = sum(h << (i * w) for i, h in enumerate(vals))
+            rv = sum(h << ((count - 1 - i) * w) for i, h in enumerate(vals))
+            m = (1 << w) - 1
+            fwd = [(fv >> (i * w)) & m for i in range(count + 1)]
+            rev = [(rv >> (i * w)) & m for i in range(count + 1)][::-1]
+            got = kmx.reconstruct_overlapped(kmx.OverlapDigits(tuple(fwd), tuple(rev), w))
+            assert list(got.coeffs) == vals, (w, count, kind)
+            if kind == "random":
+                bad = list(fwd)
+                bad[count // 2] ^= 1
+                with pytest.raises(kmx.ReconstructionError):
+                    kmx.reconstruct_overlapped(kmx.OverlapDigits(tuple(bad), tuple(rev), w))
+        # a coefficient equal to 2^w (2^w - 1) is out of range (ksint.py:157-158)
+        vals = [rng.randrange(top) for _ in range(count)]
+        vals[count - 3] = top
+        fv = sum(h << (i * w) for i, h in enumerate(vals))
+        rv = sum(h << ((count - 1 - i) * w) for i, h in enumerate(vals))
+        fwd = [(fv >> (i * w)) & m for i in range(count + 1)]
+        rev = [(rv >> (i * w)) & m for i in range(count + 1)][::-1]
+        with pytest.raises(kmx.ReconstructionError):
+            kmx.reconstruct_overlapped(kmx.OverlapDigits(tuple(fwd), tuple(rev), w))
+
+
 def test_dropin_random_reconstruct_carries(kmx):
     rng = random.Random(5)
     for _ in range(200):
