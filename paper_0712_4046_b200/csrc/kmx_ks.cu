@@ -1276,7 +1276,9 @@ static cudaError_t launch_recon_par_t(const ReconArgs& a, int maxcount, cudaStre
   b.bias_smem = bias_smem;
   b.spec = recon_spec();
   const size_t smem = recon_stage_words(a, T, bias_smem) * sizeof(u32);
-  b.stage = smem <= 160 * 1024;
+  // dynamic + ~5 KB static within the 227 KB opt-in limit (KMX_RECON_STAGE_KB: c4 ks4, 168 KB, stages since the limit is 216)
+  static const int stage_kb = getenv("KMX_RECON_STAGE_KB") ? atoi(getenv("KMX_RECON_STAGE_KB")) : 216;
+  b.stage = smem <= (size_t)stage_kb * 1024;
   // register-capped instance (KMX_RECON_MINB=0 disables)
   static const int minb = getenv("KMX_RECON_MINB") ? atoi(getenv("KMX_RECON_MINB")) : 5;
   if constexpr (NW <= 2) {
