@@ -1338,11 +1338,17 @@ cudaError_t launch_recon_par(const ReconArgs& a, cudaStream_t st) {
   }
 }
 
+// kmx_reconcl.cu: a thread-block cluster per stream for few, long streams
+cudaError_t launch_recon_cluster(const ReconArgs& a, cudaStream_t st, bool* used);
+
 cudaError_t launch_recon(const ReconArgs& a0, cudaStream_t st) {
   static const int seq = getenv("KMX_RECON_SEQ") ? atoi(getenv("KMX_RECON_SEQ")) : 0;
   // the one-thread-per-stream kernel handles the signed correction only for
   // digits of at most 64 bits (its multiword branch stores unsigned)
   if (!a0.carries && !a0.sequential && !(seq && a0.dwords <= 2)) {
+    bool clustered = false;
+    const cudaError_t ec = launch_recon_cluster(a0, st, &clustered);
+    if (clustered || ec != cudaSuccess) return ec;
     if (recon_pair_ok(a0)) return launch_recon_pair(a0, st);
     return launch_recon_par(a0, st);
   }
