@@ -422,27 +422,39 @@ bool rc_geometry(const ReconArgs& a, RcGeom& g) {
   int maxcount = a.s[0].count;
   if (a.ns > 1 && a.s[1].count > maxcount) maxcount = a.s[1].count;
   const int nsteps = maxcount - 1;
-  // few, long streams (measured at config 4); KMX_RECON_CLUSTER=C forces clusters of C for any stream count
-  if (force < 0 && (nstreams * 2 > 148 || nsteps < 1024)) return false;
   if (nsteps < 64 || nstreams < 1) return false;
+  // What one CTA per stream (k_recon_par) would have to stage: past its 216 KB the walks read
+  // global memory step by step, and a cluster -- whose CTAs each stage a part -- wins at any
+  // stream count (config 5, n = 8192, b = 128, ks2: 494 -> 146 us).  Streams that one CTA can
+  // stage go to clusters only while there are too few of them to fill the chip (config 4).
+  // (digits of at least 4 words: with narrower ones the unstaged walks keep up -- n = 8192, b = 32 / 64, ks2:
+  // 52 / 86 us either way)
+  const bool unstageable = a.dwords >= 4 &&
+                           2 * ((size_t)(maxcount + 1) * a.dwords + (size_t)(maxcount + 1) / 8 + 1) * sizeof(u32) >
+                               (size_t)216 * 1024;
+  if (force < 0 && !unstageable && (nstreams * 2 > 148 || nsteps < 1024)) return false;
   int C = 2;
   if (force >= 2) {
     C = force > 8 ? 8 : force;
   } else {
     while (C < 8 && nstreams * (2 * C) <= 148 && nsteps / (2 * C) >= 512) C *= 2;
+    if (unstageable && C < 4) C = 4;
   }
   static const int lgv0 = getenv("KMX_RECON_CL_LGV") ? atoi(getenv("KMX_RECON_CL_LGV")) : 3;
-  for (int lgV = lgv0 < 1 ? 1 : lgv0; lgV <= 4; lgV++) {
-    const int V = 1 << lgV;
-    int T = ((nsteps + C - 1) / C + V - 1) / V;
-    T = (T + 31) & ~31;
-    if (T > RC_MAXT) continue;
-    const int spc = T * V;
-    const int nd = spc + 2;
-    const size_t smem = 2 * ((size_t)nd * a.dwords + (nd >> lgV) + 1) * sizeof(u32);
-    if (smem > 200 * 1024) continue;
-    g.C = C; g.T = T; g.lgV = lgV; g.spc = spc; g.smem = smem;
-    return true;
+  for (; C <= 8; C *= 2) {
+    for (int lgV = lgv0 < 1 ? 1 : lgv0; lgV <= 4; lgV++) {
+      const int V = 1 << lgV;
+      int T = ((nsteps + C - 1) / C + V - 1) / V;
+      T = (T + 31) & ~31;
+      if (T > RC_MAXT) continue;
+      const int spc = T * V;
+      const int nd = spc + 2;
+      const size_t smem = 2 * ((size_t)nd * a.dwords + (nd >> lgV) + 1) * sizeof(u32);
+      if (smem > 200 * 1024) continue;
+      g.C = C; g.T = T; g.lgV = lgV; g.spc = spc; g.smem = smem;
+      return true;
+    }
+    if (force >= 2) break;  // a forced cluster size is not widened
   }
   return false;
 }
