@@ -499,7 +499,7 @@ def hbm_roofline(g, cfg, v, km):
     else:
         out["finish"] = ent("finish", by["finish"], km.get("finish"), "k_finish_w / k_finish / k_finchunk")
         if "recon" in by:
-            out["recon"] = ent("recon", by["recon"], km.get("recon"), "k_recon_par")
+            out["recon"] = ent("recon", by["recon"], km.get("recon"), "k_recon_pair / k_recon_cl / k_recon_par")
     return out
 
 
