@@ -356,6 +356,25 @@ __global__ void __launch_bounds__(R2_MAXT, 1) k_recon_pair(ReconArgs a, int TS, 
 
 }  // namespace
 
+// Launch geometry: threads per stream and the shared-memory layout (transpose slots / final
+// words, whichever is larger, then the signed path's prefix sums).
+struct R2Geom { int TS, T, pf_off; size_t smem; };
+static R2Geom r2_geometry(const ReconArgs& a) {
+  int maxcount = a.s[0].count;
+  if (a.ns == 2 && a.s[1].count > maxcount) maxcount = a.s[1].count;
+  R2Geom g;
+  // 8 TS >= count: the group's threads cover the steps, and 8 T the pair's coefficients
+  g.TS = ((maxcount + R2_V - 1) / R2_V + 31) & ~31;
+  g.T = g.TS * a.ns;
+  const int klen = a.ns == 1 ? a.s[0].count : a.s[0].count + a.s[1].count;
+  const size_t tbytes = (size_t)(a.ns * (8 * (g.TS + 1) + 4)) * 16;
+  const size_t fbytes = ((size_t)klen * a.out_words + 8) * 4;
+  g.smem = ((tbytes > fbytes ? tbytes : fbytes) + 15) & ~(size_t)15;
+  g.pf_off = (int)g.smem;
+  if (a.bias.enabled) g.smem += ((size_t)(a.bias.lf + a.bias.lg + 2) * 8 + 15) & ~(size_t)15;
+  return g;
+}
+
 // One CTA per pair: digits of at most two words, no carry report, streams
 // short enough for 8 steps per thread.  KMX_RECON_PAIR=0 disables, 2 forces it for short streams too.
 bool recon_pair_ok(const ReconArgs& a) {
@@ -376,31 +395,20 @@ bool recon_pair_ok(const ReconArgs& a) {
   // measured over config 5 (KMX_RECON_PAIR=2 forces): streams of fewer than 256 digits leave the
   // pair's CTA at one or two warps and k_recon_par is 8-10% faster there
   if (en != 2 && maxcount < 256) return false;
-  // 8 TS >= count: the group's threads cover the steps, and 8 T the pair's coefficients
-  int TS = ((maxcount + R2_V - 1) / R2_V + 31) & ~31;
-  return TS * a.ns <= R2_MAXT;
+  const R2Geom g = r2_geometry(a);
+  return g.T <= R2_MAXT && g.smem <= 200 * 1024;  // (a caller's wide out_words can outgrow the final-word buffer)
 }
 
 cudaError_t launch_recon_pair(const ReconArgs& a, cudaStream_t st) {
-  int maxcount = a.s[0].count;
-  if (a.ns == 2 && a.s[1].count > maxcount) maxcount = a.s[1].count;
-  const int TS = ((maxcount + R2_V - 1) / R2_V + 31) & ~31;
-  const int T = TS * a.ns;
-  const int klen = a.ns == 1 ? a.s[0].count : a.s[0].count + a.s[1].count;
-  // transpose slots (16 B) and the final words (+ phase), whichever is larger
-  const size_t tbytes = (size_t)(a.ns * (8 * (TS + 1) + 4)) * 16;
-  const size_t fbytes = ((size_t)klen * a.out_words + 8) * 4;
-  size_t smem = ((tbytes > fbytes ? tbytes : fbytes) + 15) & ~(size_t)15;
-  const int pf_off = (int)smem;  // prefix sums of the signed path behind the transpose / final words
-  if (a.bias.enabled) smem += ((size_t)(a.bias.lf + a.bias.lg + 2) * 8 + 15) & ~(size_t)15;
-  if (smem > 200 * 1024) return cudaErrorInvalidValue;
+  const R2Geom g = r2_geometry(a);
+  if (g.T > R2_MAXT || g.smem > 200 * 1024) return cudaErrorInvalidValue;
   const int aligned = (reinterpret_cast<uintptr_t>(a.h) & 3) == 0 ? 1 : 0;
   auto kern = a.dwords == 1 ? k_recon_pair<1> : k_recon_pair<2>;
-  if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (g.smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.smem);
     if (e != cudaSuccess) return e;
   }
-  kern<<<a.batch, T, smem, st>>>(a, TS, aligned, pf_off);
+  kern<<<a.batch, g.T, g.smem, st>>>(a, g.TS, aligned, g.pf_off);
   return cudaGetLastError();
 }
 

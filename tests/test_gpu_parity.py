@@ -207,6 +207,31 @@ def test_config2_signed(kmx, variant):
     _check_batch(kmx, variant, fs, gs, 32, want, signed=True)
 
 
+@pytest.mark.parametrize("signed", [False, True])
+def test_wider_output_records(kmx, signed):
+    # a caller may ask for more words per coefficient than the minimum: the upper words are the
+    # zero / sign extension (the coefficient writers of every finish / reconstruction kernel)
+    rng = random.Random(303)
+    B, lf, lg, b = 3, 700, 640, 32 if signed else 27
+    if signed:
+        fs = [[rng.randrange(-2**31, 2**31) for _ in range(lf)] for _ in range(B)]
+        gs = [[rng.randrange(-2**31, 2**31) for _ in range(lg)] for _ in range(B)]
+    else:
+        fs = [[rng.randrange(1 << b) for _ in range(lf)] for _ in range(B)]
+        gs = [[rng.randrange(1 << b) for _ in range(lg)] for _ in range(B)]
+    words = 1
+    fd, gd = _dev_words(fs, words, signed), _dev_words(gs, words, signed)
+    for v in (1, 2, 3, 4):
+        kb = kmx.KsBatch(v, B, lf, lg, b, signed=signed)
+        base = _host_ints(kb(fd, gd), signed=signed)
+        kb.status()
+        kw = kmx.KsBatch(v, B, lf, lg, b, signed=signed)
+        kw.out_words += 3
+        wide = _host_ints(kw(fd, gd), signed=signed)
+        kw.status()
+        assert wide == base, (v, signed)
+
+
 def test_signed_golden(kmx):
     for f, g, h in G.signed_cases():
         for v in (1, 2, 3, 4):
