@@ -46,6 +46,10 @@ int cur_dev() {
 // integer pipe, KMX_TC=1 the tensor cores wherever supported.
 }  // namespace
 namespace kmx {
+// kmx_recon2.cu: in-place signed correction of coefficient records
+cudaError_t launch_bias_apply(const BiasFix& bf, uint32_t* h, int out_words, int klen, long long h_pair_stride, int batch,
+                              cudaStream_t st);
+
 // chunked single-tile tensor-core multiply (kmx_tcj.cu)
 bool tcj_plan(int ma, int mb, double* cost, bool short_only);
 bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]);
@@ -472,6 +476,11 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
   fa.bias = bfix;
   fa.cmaps = (uint8_t*)(w + p.off_cmap);
   fa.nchunks = p.fin_chunks;
+  // ks1 / ks3 with signed inputs: the finish writes the lifted product's coefficients and a
+  // streaming pass corrects them in place (kmx_recon2.cu; KMX_BIAS_FUSED=1: inside the finish)
+  static const int bias_fused = getenv_int("KMX_BIAS_FUSED", 0);
+  const bool bias_pass = p.sign && !p.nrs && !bias_fused && p.batch <= 65535;
+  if (bias_pass) fa.bias.enabled = 0;
   bool finished = false;  // K3 already ran inside K2
   prof_begin(1, st);
   if (p.kara) {
@@ -518,6 +527,14 @@ int run_plan(const KsPlan& p, const uint32_t* f, const uint32_t* g, uint32_t* h,
     prof_begin(2, st);
     if ((e = launch_finish(fa, p.batch, st)) != cudaSuccess) return KMX_ECUDA;
     prof_end(2, st);
+    g_launches++;
+  }
+  if (bias_pass) {
+    prof_begin(4, st);
+    if ((e = launch_bias_apply(bfix, h, out_words, p.out_len, (long long)p.out_len * out_words, p.batch, st)) !=
+        cudaSuccess)
+      return KMX_ECUDA;
+    prof_end(4, st);
     g_launches++;
   }
 

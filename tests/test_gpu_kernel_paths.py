@@ -32,6 +32,7 @@ SETTINGS = [
     {"KMX_TC": "1", "KMX_TCJ": "1", "KMX_PACK_PAIR": "2"},  # chunked single-tile tensor-core kernel; paired packs at every batch size
     {"KMX_RECON_PAIR": "2"},    # one-CTA-per-pair reconstruction (kmx_recon2.cu) for every digit width <= 64, short streams too
     {"KMX_RECON_PAIR": "0", "KMX_RECON_BIAS_SMEM": "0", "KMX_RECON_WARP": "1"},  # k_recon_par family: signed prefix sums from L2; warp-per-stream recon
+    {"KMX_BIAS_FUSED": "1"},    # ks1 / ks3 signed correction inside the finish's coefficient stores (default: streaming pass)
     {"KMX_RECON_CLUSTER": "2"},  # a cluster of 2 CTAs per reconstruction stream (kmx_reconcl.cu) for every unsigned shape
     {"KMX_RECON_CLUSTER": "8", "KMX_RECON_CL_LGV": "2"},  # clusters of 8, 4 steps per thread
     {"KMX_RECON_PAIR": "0", "KMX_RECON_CLUSTER": "0", "KMX_RECON_SPEC": "1", "KMX_RECON_MINB": "0"},  # k_recon_par only (long streams unstaged): speculative stores from round 1; uncapped registers
