@@ -424,7 +424,7 @@ def mul_roofline(g, cfg, cfg_name, v, mul_ms, clocks):
     info = {}
     if g.L.kmx_mul_plan(v, B, cfg["n"], cfg["n"], cfg["b"], flags, plan) == 0:
         info = {"engine": ["imad", "tensor tiled", "tensor chunked", "karatsuba",
-                           "tensor swizzled-window"][min(4, int(plan[0]))],
+                           "tensor swizzled-window", "tensor swizzled-window M=64"][min(5, int(plan[0]))],
                 "H": int(plan[1]), "NW": int(plan[2]), "KC": int(plan[3]), "TPC": int(plan[4]),
                 "mmas_per_product": int(plan[5]), "smem_bytes_per_product": int(plan[6]),
                 "issued_byte_macs_per_product": int(plan[7])}
@@ -436,7 +436,7 @@ def mul_roofline(g, cfg, cfg_name, v, mul_ms, clocks):
         tops = 2.0 * 16.0 * lps / 1e12
         tpk = 2.0 * g.tensor / 1e12
         kname = ("k_tcswz (tcgen05.mma kind::i8 byte convolution: swizzled sliding windows x phase table, TMEM s32)"
-                 if info.get("engine") == "tensor swizzled-window"
+                 if str(info.get("engine", "")).startswith("tensor swizzled-window")
                  else "k_tcmul (tcgen05.mma kind::i8 byte convolution, TMEM s32)")
         r = {"bound": "tensor", "kernel": kname,
              "achieved": tops, "peak": tpk, "unit": "TOPS (int8, 2 ops per MAC)", "frac": tops / tpk,
@@ -445,19 +445,22 @@ def mul_roofline(g, cfg, cfg_name, v, mul_ms, clocks):
              "traffic": g.traffic(cfg_name, v, "tcmul_dram_bytes"),
              "same_kernel_in_imad_units": {"achieved": lps / 1e9, "unit": "G limb-products/s",
                                            "frac_of_imad_peak": lps / g.imad}}
-        if info.get("engine") in ("tensor tiled", "tensor swizzled-window") and info.get("H"):
+        m64 = info.get("engine") == "tensor swizzled-window M=64"
+        if info.get("engine") in ("tensor tiled", "tensor swizzled-window", "tensor swizzled-window M=64") and info.get("H"):
             n_mma = 16 * info["H"]
             sp = g.tc_shape_peak(n_mma)
             nprod_ = B * PCOUNT[ks_geometry(cfg, v)["variant"]]
             issued = info["issued_byte_macs_per_product"] * nprod_ / (mul_ms * 1e-3) if info.get(
                 "issued_byte_macs_per_product") else None
             r["same_shape_ceiling"] = {
-                "mma_shape": f"M=128 N={n_mma} K=32 (SS, u8)", "peak": 2.0 * sp / 1e12, "unit": "TOPS",
+                "mma_shape": (f"M=64 N={n_mma} K=32 issued (two 64-row windows); ceiling measured at M=128 N={n_mma}"
+                              if m64 else f"M=128 N={n_mma} K=32 (SS, u8)"), "peak": 2.0 * sp / 1e12, "unit": "TOPS",
                 "frac_algorithmic": 2.0 * 16.0 * lps / (2.0 * sp) if sp > 0 else None,
                 "frac_issued": issued / sp if (issued and sp > 0) else None,
                 "note": "kmx_tc_peak_n(): the dense rate of the MMA shape K2 issues; frac_issued counts every MAC "
                         "the tiles issue (incl. the Toeplitz zero padding), frac_algorithmic only the product's"}
-        if info.get("engine") in ("tensor tiled", "tensor swizzled-window") and info.get("smem_bytes_per_product"):
+        if info.get("engine") in ("tensor tiled", "tensor swizzled-window", "tensor swizzled-window M=64") and info.get(
+                "smem_bytes_per_product"):
             nprod = B * PCOUNT[ks_geometry(cfg, v)["variant"]]
             clk = (clocks or {}).get("sm_mhz") or 1965.0
             smem_peak = 148 * 128 * clk * 1e6 / 1e9

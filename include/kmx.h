@@ -222,9 +222,10 @@ int kmx_mul_karatsuba_levels(int variant, int batch, int len_f, int len_g, int c
  * aside: for `batch` products per launch): out8 = {engine (0 integer pipe,
  * 1 tiled tensor-core kernel, 2 chunked single-tile kernel, 3 Karatsuba levels
  * over the engines with out8[1] = levels, 4 swizzled-window tensor-core
- * kernel), H (MMA N = 16 H), NW, KC (K-steps per stage / chunk), tiles
- * per CTA, MMAs per product, shared-memory operand bytes per product, issued
- * byte MACs per product}; fields 1-7 are filled for engines 1 and 4. */
+ * kernel, 5 its M = 64 two-window form), H (MMA N = 16 H), NW, KC (K-steps
+ * per stage / chunk), tiles per CTA, MMAs per product, shared-memory operand
+ * bytes per product, issued byte MACs per product}; fields 1-7 are filled
+ * for engines 1, 4 and 5. */
 int kmx_mul_plan(int variant, int batch, int len_f, int len_g, int coeff_bits, unsigned flags, int64_t* out8);
 
 /* Measured dense u8 x u8 -> s32 tcgen05.mma throughput on the current

@@ -886,8 +886,9 @@ int tcs_mode() {
   const char* v = getenv("KMX_TCS");
   return v && *v ? atoi(v) : -1;
 }
-// KMX_TCS_PERSIST: -1 (default) both forms are tuner candidates; 0 one-shot
-// CTAs only; 1 the persistent form only (wherever its plan exists).
+// KMX_TCS_PERSIST: -1 (default) all forms are tuner candidates; 0 one-shot
+// CTAs only; 1 the persistent form only (wherever its plan exists); 2 the
+// M = 64 two-window form only (wherever the product fits it).
 int tcs_persist_mode() {
   const char* v = getenv("KMX_TCS_PERSIST");
   return v && *v ? atoi(v) : -1;
@@ -901,6 +902,12 @@ bool tcs_best(int ma, int mb, TcPlan& out) {
     if (mode >= 32 && mode != pitch) continue;
     TcsPlan sp;
     if (!(tcs_persist_mode() == 1 && tcs_plan(ma, mb, pitch, 1, sp)) && !tcs_plan(ma, mb, pitch, 0, sp)) continue;
+    {  // the M = 64 two-window form where the product fits it (KMX_TCS_PERSIST=2 forces, 0 / 1 exclude)
+      TcsPlan s64;
+      if ((tcs_persist_mode() < 0 || tcs_persist_mode() == 2) && tcs_plan(ma, mb, pitch, 2, s64) &&
+          (tcs_persist_mode() == 2 || s64.cost < sp.cost))
+        sp = s64;
+    }
     if (!ok || sp.cost < out.sp.cost) {
       out = TcPlan();
       out.swz = pitch;
@@ -1189,7 +1196,7 @@ std::vector<TcPlan> tc_candidates(int ma, int mb, long long nprod) {
   }
   std::vector<TcPlan> out;
   if (tcs_mode() != 0)
-    for (int form = 0; form < 2; form++)
+    for (int form = 0; form < 3; form++)  // one-shot, persistent, M = 64 windows
     for (int pitch : {32, 64, 128}) {
       if (tcs_mode() >= 32 && tcs_mode() != pitch) continue;
       if (tcs_persist_mode() >= 0 && tcs_persist_mode() != form) continue;
@@ -1505,6 +1512,14 @@ bool tc_plan_info(int ma, int mb, long long nprod, long long out[8]) {
     std::lock_guard<std::mutex> lk(g_tune_mu);
     auto it = g_tune.find(TuneKey{current_device(), ma, mb, nprod});
     if (it != g_tune.end()) p = it->second;
+  }
+  if (p.swz && p.sp.persist == 2) {  // M = 64 two-window form: A tile 64 x 32 B per MMA, rows up to 79 staged
+    out[0] = 5; out[1] = p.H; out[2] = 4; out[3] = p.KC; out[4] = 1;
+    out[5] = p.sp.mmas;
+    out[6] = p.sp.mmas * (2048LL + 32LL * p.swz) + (16LL * 4 * (ma < mb ? ma : mb) + 79LL * p.swz + 4LL * (ma < mb ? ma : mb)) +
+             2LL * 2 * (p.swz / 4) * 64 * 8;  // + the limb sums through shared memory (written, read)
+    out[7] = 64LL * p.swz * 32 * p.sp.mmas;
+    return true;
   }
   if (p.swz) {
     out[0] = 4; out[1] = p.H; out[2] = 4; out[3] = p.KC; out[4] = 1;

@@ -95,6 +95,9 @@ __host__ __device__ inline size_t r128(size_t x) { return (x + 127) & ~(size_t)1
 __host__ __device__ inline size_t r1024(size_t x) { return (x + 1023) & ~(size_t)1023; }
 template <int PITCH>
 __host__ __device__ inline size_t tcs_abytes(int KS) { return r1024((size_t)SG<PITCH>::AMAX + 32 * KS + 64); }
+// M = 64 form: rows up to R0 + 63 <= 79 are read
+template <int PITCH>
+__host__ __device__ inline size_t tcs_abytes64(int KS) { return r1024((size_t)79 * PITCH + 32 * KS + 64); }
 template <int PITCH>
 __host__ __device__ inline int tcs_rawbytes(int KS) { return (int)r128((size_t)32 * KS + PITCH + 96); }
 template <int PITCH>
@@ -102,6 +105,11 @@ __host__ __device__ inline int tcs_entries(int KS) { return 4 * KS + PITCH / 8 +
 template <int PITCH>
 __host__ __device__ inline size_t tcs_smem(int KS) {
   return 1024 + r128(sizeof(TcsShared)) + tcs_abytes<PITCH>(KS) + tcs_rawbytes<PITCH>(KS) +
+         (size_t)tcs_entries<PITCH>(KS) * 128;
+}
+template <int PITCH>
+__host__ __device__ inline size_t tcs_smem64(int KS) {
+  return 1024 + r128(sizeof(TcsShared)) + tcs_abytes64<PITCH>(KS) + tcs_rawbytes<PITCH>(KS) +
          (size_t)tcs_entries<PITCH>(KS) * 128;
 }
 
@@ -113,6 +121,7 @@ struct TcsArgs {
   int nch;     // accumulation chains per tile (K-step s -> chain (s - slo) % nch): 2 past 64 KB of b
   int NS;      // persistent kernel: operand stages in the ring
   unsigned char order[TCS_MAXT];  // persistent kernel: tiles by descending K-steps
+  int smid, r0;  // M = 64 form: K-steps < smid read rows [r0, r0 + 64), the rest rows [0, 64)
 };
 
 __device__ __forceinline__ uint64_t sdesc_lt(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t lt) {
@@ -169,11 +178,11 @@ struct TcsRegs {
 template <int PITCH>
 struct TcsChunk {  // geometry of one chunk (all warp-uniform)
   int aw0, nq, x0, nx, jb, nw;
-  __device__ __forceinline__ TcsChunk(const TcsDims& d, int k0, int sb, int se) {
+  __device__ __forceinline__ TcsChunk(const TcsDims& d, int k0, int sb, int se, int amax = SG<PITCH>::AMAX) {
     using G = SG<PITCH>;
     const int cc = G::N - 8 - d.ulo;  // T[x][r][i] = b[r + cc - 8x - i]
     aw0 = k0 + d.ulo + 32 * sb;       // region byte o is a[aw0 + o]; a multiple of 32
-    nq = (G::AMAX + 32 * (se - sb) + 15) / 16;
+    nq = (amax + 32 * (se - sb) + 15) / 16;  // amax: offset of the last A row that is read
     x0 = 4 * sb;
     nx = 4 * (se - sb) + G::N / 8 - 2;  // entries x0 .. x0 + nx - 1 are read
     const int jlo = cc - 8 * (x0 + nx - 1) - 15;  // lowest index r + cc - 8x - i
@@ -494,6 +503,201 @@ __global__ void __launch_bounds__(128) k_tcswz(TcsArgs ta, FinishArgs fa) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(ta.nch * G::N)));
 }
 
+// ------------------------------------------------------------------------
+// M = 64 form for products of at most 64 + R0 rows of PITCH bytes (c2 ks4: 77
+// rows of 64).  In a 128-row tile of such a product only ~39 rows are live at
+// any K-step -- the rows whose A window holds bytes of a -- and the live band
+// slides down by half a row per step.  An M = 128 instruction reads all 128
+// rows of A from shared memory every step; here the K-steps are issued as
+// M = 64 instructions over TWO row windows: the early steps (live rows high)
+// read rows [R0, R0 + 64) into a second accumulator, the late steps rows
+// [0, 64) into the first.  A step then reads 2 + 2 KB instead of 4 + 2 KB of
+// shared memory (measured 36.6 against 62 SM cycles per step at N = 64, 3 CTAs
+// per SM: tools/microbench/tc_m64.cu).  An M = 64 accumulator keeps tile row r
+// in TMEM lane (r % 16) + 32 (r / 16) (same microbenchmark), so the epilogue
+// passes the lanes' limb sums through shared memory into row order, adds the
+// two windows where they overlap, and continues as k_tcswz does.
+// ------------------------------------------------------------------------
+template <int PITCH>
+__global__ void __launch_bounds__(128) k_tcswz_m64(TcsArgs ta) {
+  using G = SG<PITCH>;
+  constexpr int LPT = G::LPT;
+  constexpr uint32_t IDESC64 = (2u << 4) | ((uint32_t)(G::N >> 3) << 17) | (4u << 24);
+  const MulArgs& a = ta.m;
+  extern __shared__ __align__(1024) unsigned char ssm_raw[];
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+  unsigned char* ssm = ssm_raw + ((1024u - (smem_u32(ssm_raw) & 1023u)) & 1023u);
+  const int KS = ta.KS;
+  unsigned char* abuf = ssm;
+  unsigned char* braw = abuf + tcs_abytes64<PITCH>(KS);
+  unsigned char* tab = braw + tcs_rawbytes<PITCH>(KS);
+  TcsShared& sh = *reinterpret_cast<TcsShared*>(tab + (size_t)tcs_entries<PITCH>(KS) * 128);
+
+  const bool sw = a.mb > a.ma;
+  const int mA = sw ? a.mb : a.ma, mB = sw ? a.ma : a.mb;
+  const TcsDims d = tcs_dims<PITCH>(mA, mB);
+  const int mp = a.ma + a.mb;
+  const long long z = blockIdx.x;
+  int slo, shi;
+  tcs_tile_steps<PITCH>(d, 0, slo, shi);
+  const int R0 = ta.r0, smid = ta.smid;
+
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&sh.tmem_base)),
+                 "r"((uint32_t)(2 * G::N)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  if (tid == 0) {
+    mbar_init(smem_u32(&sh.bar_mma), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  const uint32_t abase = smem_u32(abuf);
+  const uint32_t* Ag = sw ? a.B + z * a.b_stride : a.A + z * a.a_stride;
+  const uint32_t* Bg = sw ? a.A + z * a.a_stride : a.B + z * a.b_stride;
+  const bool a16 = (reinterpret_cast<uintptr_t>(Ag) & 15) == 0;
+  {
+    // one chunk: the whole K span; rows up to R0 + 63 are read
+    const TcsChunk<PITCH> ck(d, 0, slo, shi, (R0 + 63) * PITCH);
+    TcsRegs R;
+    tcs_load<PITCH>(R, ck, Ag, Bg, mA, mB, a16, tid);
+    tcs_store<PITCH>(R, ck, abuf, braw, tid);
+    __syncthreads();
+    tcs_table<PITCH>(ck, d, braw, tab, tid);
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = __shfl_sync(0xffffffffu, sh.tmem_base, 0);
+  if (warp == 0) {
+    uint64_t ad0 = sdesc_lt(abase, 16, 8 * PITCH, G::LT);                              // rows [0, 64)
+    uint64_t ad1 = sdesc_lt(abase + (uint32_t)(R0 * PITCH), 16, 8 * PITCH, G::LT);     // rows [R0, R0 + 64)
+    uint64_t bd = sdesc(smem_u32(tab), 256, 128);
+    for (int s = slo; s < shi; s++) {
+      const bool hi = s < smid;
+      mma_i8_elect(tmem + (hi ? (uint32_t)G::N : 0u), hi ? ad1 : ad0, bd, IDESC64,
+                   (s == slo || s == smid) ? 0u : 1u);
+      ad0 += 2; ad1 += 2;  // + 32 bytes
+      bd += 32;            // + 512 bytes
+    }
+    mma_commit_elect(smem_u32(&sh.bar_mma));
+    mbar_wait_warp(smem_u32(&sh.bar_mma), 0u);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+
+  // ---- limb sums of the two accumulators into row order (the table's shared memory is free now):
+  // S[w][q][r] = sum of limb q of tile row r of window w, u64
+  unsigned long long* S0 = reinterpret_cast<unsigned long long*>(tab);
+  unsigned long long* S1 = S0 + LPT * 64;
+  {
+    // (tcgen05.ld is warp-wide: every lane loads, the lower half-warp holds the rows)
+    const int tr = 16 * warp + (lane & 15);  // tile row held by TMEM lane 32 warp + lane, lane < 16
+    const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
+#pragma unroll
+    for (int w = 0; w < 2; w++) {
+      const bool have = w == 0 ? shi > smid && shi > slo : smid > slo;
+      unsigned long long* Sw = w == 0 ? S0 : S1;
+#pragma unroll
+      for (int c = 0; c < G::N / 16; c++) {
+        unsigned long long ls[4] = {0ull, 0ull, 0ull, 0ull};
+        if (have) {  // warp-uniform
+          uint32_t v[16];
+          tmem_ld16(tl + (uint32_t)(w * G::N + G::N - 16 - 16 * c), v);
+#pragma unroll
+          for (int q = 0; q < 4; q++) {
+            const int o = q < 2 ? 8 + 4 * q : 4 * (q - 2);
+            ls[q] = (unsigned long long)v[o] + ((unsigned long long)v[o + 1] << 8) +
+                    ((unsigned long long)v[o + 2] << 16) + ((unsigned long long)v[o + 3] << 24);
+          }
+        }
+        if (lane < 16) {
+#pragma unroll
+          for (int q = 0; q < 4; q++) Sw[(4 * c + q) * 64 + tr] = ls[q];
+        }
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+
+  // ---- epilogue as k_tcswz: thread tid owns limbs [LPT tid, LPT tid + LPT) = row tid
+  uint32_t dg[LPT];
+  unsigned long long x = 0ull;
+  {
+    const int r = tid;
+#pragma unroll
+    for (int q = 0; q < LPT; q++) {
+      unsigned long long lsq = 0ull;
+      if (r < 64) lsq = S0[q * 64 + r];
+      if (r >= R0 && r < R0 + 64) lsq += S1[q * 64 + r - R0];
+      x = (x >> 32) + lsq;
+      dg[q] = (uint32_t)x;
+    }
+  }
+  const unsigned long long cout = x >> 32;
+  unsigned long long xin = __shfl_up_sync(0xffffffffu, cout, 1);
+  if (lane == 31) sh.s_cout[warp] = cout;
+  uint32_t ones = 0xFFFFFFFFu;
+#pragma unroll
+  for (int q = 1; q < LPT; q++) ones &= dg[q];
+  __syncthreads();
+  if (lane == 0) xin = warp ? sh.s_cout[warp - 1] : 0ull;
+  const unsigned long long s0 = (unsigned long long)dg[0] + xin;
+  const bool all1 = ones == 0xFFFFFFFFu;
+  const uint32_t gg = all1 && (s0 >> 32) != 0ull;
+  const uint32_t pp = all1 && ((s0 + 1ull) >> 32) != 0ull;
+  uint32_t F = gg | (pp << 1);
+#pragma unroll
+  for (int dd = 1; dd < 32; dd <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, F, dd);
+    if (lane >= dd) F = cm2(F, y);
+  }
+  if (lane == 31) sh.warp_map[warp] = F;
+  __syncthreads();
+  uint32_t E = __shfl_up_sync(0xffffffffu, F, 1);
+  uint32_t Wm = CM2_ID;
+  for (int w = 0; w < warp; w++) Wm = cm2(sh.warp_map[w], Wm);
+  E = lane ? cm2(E, Wm) : Wm;
+  const uint32_t Fin = cm2(F, Wm);
+  unsigned long long acc = s0 + (E & 1u);
+  dg[0] = (uint32_t)acc;
+#pragma unroll
+  for (int q = 1; q < LPT; q++) {
+    acc = (acc >> 32) + dg[q];
+    dg[q] = (uint32_t)acc;
+  }
+  uint32_t* Pz = a.P + z * a.p_stride;
+  const int L = LPT * tid;
+  if (L + LPT <= mp) {
+#pragma unroll
+    for (int q = 0; q < LPT / 4; q++)
+      *reinterpret_cast<uint4*>(Pz + L + 4 * q) = make_uint4(dg[4 * q], dg[4 * q + 1], dg[4 * q + 2], dg[4 * q + 3]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < LPT; q++)
+      if (L + q < mp) Pz[L + q] = dg[q];
+  }
+  {
+    const int b1 = min(a.nbands, G::BPT);
+    if (tid < b1 && tid != G::BPT - 1) {
+      unsigned long long* sp = a.spill + (z * a.nbands + tid) * 2;
+      sp[0] = 0ull;
+      sp[1] = 0ull;
+    }
+    if (tid == 127 && G::BPT - 1 < b1) {
+      unsigned long long* sp = a.spill + (z * a.nbands + G::BPT - 1) * 2;
+      sp[0] = cout + (Fin & 1u);
+      sp[1] = 0ull;
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)(2 * G::N)));
+}
+
 // ------------------------------------------------- persistent, specialized
 // The same tiles through a persistent CTA (one per SM): work items (product,
 // tile) in a static round-robin, heaviest tile class first, with the warps
@@ -753,6 +957,32 @@ int tcs_num_sms() {
   return n;
 }
 
+// M = 64 form: the second window's first row R0 and the K-step smid from which every live row
+// lies in [0, 64); false when the product does not fit the two windows
+template <int PITCH>
+bool tcs_m64_geom(const TcsDims& d, int* r0, int* smid) {
+  using G = SG<PITCH>;
+  if (d.ntiles != 1) return false;
+  const int rows = (d.La + d.Lb - 1 + PITCH - 1) / PITCH;
+  if (rows > 80) return false;
+  const int R0 = rows > 64 ? 16 : 0;
+  int slo, shi;
+  tcs_tile_steps<PITCH>(d, 0, slo, shi);
+  // live rows of K-step s: those whose 32-byte A window [PITCH m + o, +32), o = ulo + 32 s, meets [0, La)
+  auto mlo = [&](int s) { const int o = d.ulo + 32 * s; const int t = -o - 31; return t <= 0 ? 0 : (t + PITCH - 1) / PITCH; };
+  auto mhi = [&](int s) { const int o = d.ulo + 32 * s; const int t = d.La - 1 - o; return t < 0 ? -1 : t / PITCH; };
+  int sm = slo;
+  while (sm < shi && mhi(sm) > 63) sm++;
+  for (int s = slo; s < sm; s++)
+    if (mlo(s) < R0 || mhi(s) > R0 + 63) return false;
+  for (int s = sm; s < shi; s++)
+    if (mhi(s) > 63) return false;
+  (void)G::N;
+  *r0 = R0;
+  *smid = sm;
+  return true;
+}
+
 template <int PITCH>
 bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   const int mA = ma > mb ? ma : mb, mB = ma > mb ? mb : ma;
@@ -767,7 +997,7 @@ bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   if (ksmax > TCS_KSMAX) ksmax = TCS_KSMAX;
   p.persist = persist;
   p.NS = 0;
-  if (persist) {
+  if (persist == 1) {
     if (d.ntiles > TCS_MAXT) return false;
     // three stages of the largest chunk that fits (two when one chunk is the whole K span)
     int NS = tcs_env("KMX_TCS_NS", 3);
@@ -783,7 +1013,7 @@ bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   p.pitch = PITCH;
   p.KS = KS;
   p.ntiles = d.ntiles;
-  p.smem = persist ? tcsp_smem<PITCH>(KS, p.NS) : tcs_smem<PITCH>(KS);
+  p.smem = persist == 1 ? tcsp_smem<PITCH>(KS, p.NS) : persist == 2 ? tcs_smem64<PITCH>(KS) : tcs_smem<PITCH>(KS);
   long long mmas = 0;
   for (int t = 0; t < d.ntiles; t++) {
     int slo, shi;
@@ -793,8 +1023,15 @@ bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   p.mmas = mmas;
   // modelled SM cycles per product: shared-memory operand reads at ~110 B/clk,
   // never below the tensor floor
-  const double per = (4096.0 + 32.0 * PITCH) / 110.0;
+  double per = (4096.0 + 32.0 * PITCH) / 110.0;
   const double fl = 128.0 * PITCH * 32 / 8192.0;
+  if (persist == 2) {
+    // M = 64 form: one chunk, no accumulation chains, the row-order buffers inside the table's memory
+    int r0, smid;
+    if (PITCH == 128 || p.nch != 1 || KS < d.S || !tcs_m64_geom<PITCH>(d, &r0, &smid)) return false;
+    if ((size_t)tcs_entries<PITCH>(KS) * 128 < (size_t)2 * SG<PITCH>::LPT * 64 * 8) return false;
+    per = (2048.0 + 32.0 * PITCH) / 110.0;
+  }
   p.cost = (double)mmas * (per > fl ? per : fl);
   return p.smem <= 200 * 1024;
 }
@@ -808,6 +1045,23 @@ cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st, const 
   ta.ntiles = p.ntiles;
   ta.NS = p.NS;
   ta.nch = p.nch;
+  if (p.persist == 2) {  // M = 64 form (one CTA per product)
+    if constexpr (PITCH == 128) {
+      return cudaErrorInvalidValue;
+    } else {
+      const int mA = a.ma > a.mb ? a.ma : a.mb, mB = a.ma > a.mb ? a.mb : a.ma;
+      const TcsDims d = tcs_dims<PITCH>(mA, mB);
+      if (fin || !tcs_m64_geom<PITCH>(d, &ta.r0, &ta.smid)) return cudaErrorInvalidValue;
+      static size_t s_set3 = 0;
+      if (p.smem > 48 * 1024 && p.smem > s_set3) {
+        cudaError_t e = cudaFuncSetAttribute(k_tcswz_m64<PITCH>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)p.smem);
+        if (e != cudaSuccess) return e;
+        s_set3 = p.smem;
+      }
+      k_tcswz_m64<PITCH><<<(unsigned)a.nprod, 128, p.smem, st>>>(ta);
+      return cudaGetLastError();
+    }
+  }
   if (p.persist) {
     static size_t s_set = 0;
     if (p.smem > 48 * 1024 && p.smem > s_set) {
@@ -880,11 +1134,11 @@ bool tcs_plan(int ma, int mb, int pitch, int persist, TcsPlan& p) {
 
 cudaError_t launch_tcs(const MulArgs& a, const TcsPlan& p, cudaStream_t st, const FinishArgs* fin) {
   if (a.nprod == 0) return cudaSuccess;
-  if (fin && (p.persist || p.ntiles != 1 || fin->ns > 4 || fin->nprod_pair < 1 || a.nprod % fin->nprod_pair))
+  if (fin && (p.persist != 0 || p.ntiles != 1 || fin->ns > 4 || fin->nprod_pair < 1 || a.nprod % fin->nprod_pair))
     return cudaErrorInvalidValue;
   if (tcs_env("KMX_TC_VERBOSE", 0))
     fprintf(stderr, "kmx_tcs: ma=%d mb=%d nprod=%d -> pitch=%d KS=%d tiles=%d smem=%zu mmas=%lld%s%s NS=%d\n", a.ma, a.mb,
-            a.nprod, p.pitch, p.KS, p.ntiles, p.smem, p.mmas, p.persist ? " persistent" : "",
+            a.nprod, p.pitch, p.KS, p.ntiles, p.smem, p.mmas, p.persist == 2 ? " M=64 windows" : p.persist ? " persistent" : "",
             fin ? " pair CTAs + fused finish" : "", p.NS);
   switch (p.pitch) {
     case 32: return launch_p<32>(a, p, st, fin);
