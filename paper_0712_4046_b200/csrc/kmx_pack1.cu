@@ -110,7 +110,7 @@ struct StreamAcc {  // the running top nonzero digit of one output stream
 };
 
 template <int IW>
-__global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int paired, int njobs) {
+__global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int paired, int njobs, int psplit) {
   extern __shared__ u32 w1_sm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int job = blockIdx.x * (blockDim.x >> 5) + warp;
@@ -182,16 +182,33 @@ __global__ void __launch_bounds__(32 * W1_WARPS, 8) k_pack_w1(PackArgs A, int pa
   if (PP) {  // coalesced: 32 consecutive entries per step, warp scan + running total
     unsigned long long* out = PP->prefix + (long long)pair * PP->prefix_pair_stride;
     unsigned long long run = 0ull;
-    if (lane == 0) out[0] = 0ull;
-    for (int i0 = 0; i0 < L; i0 += 32) {
+    // psplit: the polynomial's forward job writes the entries of [0, h), its reversed job (which has
+    // staged the same coefficients) those of [h, L) on top of the sum of the first h -- the scan is
+    // ~1300 instructions on the jobs that carry it, so the two jobs of a polynomial share it
+    int ibeg = 0, iend = L;
+    if (psplit) {
+      const int h = ((L >> 1) + 31) & ~31;
+      if (rev) {
+        ibeg = h;
+        unsigned long long t = 0ull;
+        for (int i = lane; i < h; i += 32) t += sc[(L - 1 - i) * IW];
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+        run = t;
+      } else {
+        iend = h < L ? h : L;
+      }
+    }
+    if (lane == 0 && ibeg == 0) out[0] = 0ull;
+    for (int i0 = ibeg; i0 < iend; i0 += 32) {
       const int i = i0 + lane;
-      unsigned long long inc = i < L ? sc[(rev ? L - 1 - i : i) * IW] : 0ull;  // signed: IW == 1
+      unsigned long long inc = i < iend ? sc[(rev ? L - 1 - i : i) * IW] : 0ull;  // signed: IW == 1
 #pragma unroll
       for (int d = 1; d < 32; d <<= 1) {
         const unsigned long long y = __shfl_up_sync(0xffffffffu, inc, d);
         if (lane >= d) inc += y;
       }
-      if (i < L) out[i + 1] = run + inc;
+      if (i < iend) out[i + 1] = run + inc;
       run += __shfl_sync(0xffffffffu, inc, 31);
     }
   }
@@ -367,7 +384,28 @@ bool pack_w1_ok(const PackArgs& a) {
 }
 
 template <int IW>
-cudaError_t launch_w1(const PackArgs& a, int njobs, bool paired, cudaStream_t st) {
+cudaError_t launch_w1(const PackArgs& a0, int njobs, bool paired, cudaStream_t st) {
+  // signed inputs: hand the second half of each polynomial's prefix sums to its reversed job
+  // (ks2 / ks4: ops [f: P][g: P], kind 0 carries the prefix pointer, kind 2 is the reversed pack)
+  PackArgs a = a0;
+  int psplit = 0;
+  static const int en_split = getenv("KMX_PACK_PSPLIT") ? atoi(getenv("KMX_PACK_PSPLIT")) : 1;
+  if (en_split && a.bias && (a.nops & 1) == 0 && a.op[0].len >= 64) {
+    const int half = a.nops / 2;
+    int src[2] = {-1, -1}, dst[2] = {-1, -1};
+    for (int g = 0; g < 2; g++)
+      for (int i = g * half; i < (g + 1) * half; i++) {
+        if (a.op[i].prefix && a.op[i].kind == 0) src[g] = i;
+        if (!a.op[i].prefix && a.op[i].kind == 2) dst[g] = i;
+      }
+    if (src[0] >= 0 && dst[0] >= 0 && src[1] >= 0 && dst[1] >= 0) {
+      for (int g = 0; g < 2; g++) {
+        a.op[dst[g]].prefix = a.op[src[g]].prefix;
+        a.op[dst[g]].prefix_pair_stride = a.op[src[g]].prefix_pair_stride;
+      }
+      psplit = 1;
+    }
+  }
   // small batches (config 1: 256 jobs): one warp per CTA, spread over more SMs
   const int wpc = njobs < 148 * 2 * W1_WARPS ? 1 : W1_WARPS;
   const size_t smem = (size_t)wpc * (a.op[0].len + W1_PAD) * IW * 4;
@@ -377,7 +415,7 @@ cudaError_t launch_w1(const PackArgs& a, int njobs, bool paired, cudaStream_t st
     if (e != cudaSuccess) return e;
     s_set = smem;
   }
-  k_pack_w1<IW><<<(njobs + wpc - 1) / wpc, 32 * wpc, smem, st>>>(a, paired ? 1 : 0, njobs);
+  k_pack_w1<IW><<<(njobs + wpc - 1) / wpc, 32 * wpc, smem, st>>>(a, paired ? 1 : 0, njobs, psplit);
   return cudaGetLastError();
 }
 
