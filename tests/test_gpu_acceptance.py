@@ -120,3 +120,44 @@ def test_bivariate_equivalence_1000(kmx):
         for fn in (kmx.bks_negated, kmx.bks_four):
             with pytest.raises(kmx.MissingHalveError):
                 fn(p, p, kmx.ring_zmod(2 ** k))
+
+
+def test_random_medium_lengths(kmx):
+    # beyond the reference's leg (lengths <= 512): lengths 300..3000, mostly unequal, widths
+    # on both sides of the one- and two-word digit boundaries, signed and unsigned, small
+    # batches -- the shapes on which the kernel selection changes (pair / cluster / per-stream
+    # reconstruction, one- and two-window tensor-core tiles, warp / block / streaming packs);
+    # the first and the last pair of every batch against an exact product, all variants equal
+    from paper_0712_4046_b200.words import ints_to_words, words_to_ints
+    rng = random.Random(20260)
+    for case in range(48):
+        signed = case % 4 == 0
+        b = 32 if signed else rng.choice((5, 16, 27, 32, 33, 47, 64, 65, 96, 130))
+        lf = rng.randrange(300, 3000)
+        lg = lf if case % 5 == 0 else rng.randrange(300, 3000)
+        B = rng.choice((1, 2, 3, 5))
+        lo, hi = (-(1 << 31), 1 << 31) if signed else (0, 1 << b)
+        fs = [[rng.randrange(lo, hi) for _ in range(lf)] for _ in range(B)]
+        gs = [[rng.randrange(lo, hi) for _ in range(lg)] for _ in range(B)]
+        if case % 7 == 0:  # extremes in one pair
+            fs[-1] = [hi - 1] * lf
+            gs[-1] = [lo if signed else hi - 1] * lg
+        words = 1 if signed else (b + 31) // 32
+        fd = torch.from_numpy(np.stack([ints_to_words(f, words, signed=signed) for f in fs]).view(np.int32)).cuda()
+        gd = torch.from_numpy(np.stack([ints_to_words(g, words, signed=signed) for g in gs]).view(np.int32)).cuda()
+        want = {}
+        for p in {0, B - 1}:
+            want[p] = (O.ks_mul_signed(1, fs[p], gs[p], b, mode="native") if signed
+                       else O.ks_mul(1, fs[p], gs[p], b, mode="native"))
+        first = None
+        for v in (1, 2, 3, 4):
+            kb = kmx.KsBatch(v, B, lf, lg, b, signed=signed)
+            h = kb(fd, gd)
+            kb.status()
+            a = h.cpu().numpy().view(np.uint32)
+            for p, w in want.items():
+                assert words_to_ints(a[p], signed=signed) == w, (case, v, lf, lg, b, signed, p)
+            if first is None:
+                first = a
+            else:
+                assert np.array_equal(first, a), (case, v, lf, lg, b, signed)
