@@ -13,6 +13,8 @@
 #             over tools/sanitize_suite.py (reduced suite); NOTE: the round-2
 #             GPU pool refuses compute-sanitizer (exit 86, "closed on this
 #             pool"), so this mode only runs where the tool is allowed
+# After a `tests,bench,launches` run (TAG) and a `KMX_TC_AUTOTUNE=0 ... full` run (FULLTAG),
+# `python tools/collect_evidence.py TAG FULLTAG` copies the tracked evidence set into profiles/rNN/.
 # Each step runs only after the previous one of the same mode exited 0
 # (profilers never run on a command that has not already passed without them).
 set -u
