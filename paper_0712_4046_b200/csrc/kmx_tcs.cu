@@ -1028,7 +1028,7 @@ bool tcs_plan_p(int ma, int mb, int persist, TcsPlan& p) {
   if (persist == 2) {
     // M = 64 form: one chunk, no accumulation chains, the row-order buffers inside the table's memory
     int r0, smid;
-    if (PITCH == 128 || p.nch != 1 || KS < d.S || !tcs_m64_geom<PITCH>(d, &r0, &smid)) return false;
+    if (p.nch != 1 || KS < d.S || !tcs_m64_geom<PITCH>(d, &r0, &smid)) return false;
     if ((size_t)tcs_entries<PITCH>(KS) * 128 < (size_t)2 * SG<PITCH>::LPT * 64 * 8) return false;
     per = (2048.0 + 32.0 * PITCH) / 110.0;
   }
@@ -1046,9 +1046,7 @@ cudaError_t launch_p(const MulArgs& a, const TcsPlan& p, cudaStream_t st, const 
   ta.NS = p.NS;
   ta.nch = p.nch;
   if (p.persist == 2) {  // M = 64 form (one CTA per product)
-    if constexpr (PITCH == 128) {
-      return cudaErrorInvalidValue;
-    } else {
+    {
       const int mA = a.ma > a.mb ? a.ma : a.mb, mB = a.ma > a.mb ? a.mb : a.ma;
       const TcsDims d = tcs_dims<PITCH>(mA, mB);
       if (fin || !tcs_m64_geom<PITCH>(d, &ta.r0, &ta.smid)) return cudaErrorInvalidValue;

@@ -31,6 +31,7 @@ SETTINGS = [
     {"KMX_TC": "1", "KMX_TCS": "128", "KMX_TCS_PERSIST": "1", "KMX_TCS_KS": "40", "KMX_TCS_NS": "2"},  # persistent, pitch 128, short chunks, 2 stages
     {"KMX_TC": "1", "KMX_TCS": "64", "KMX_TCS_PERSIST": "2"},  # M = 64 two-window form (k_tcswz_m64), pitch 64, wherever the product fits it
     {"KMX_TC": "1", "KMX_TCS": "32", "KMX_TCS_PERSIST": "2"},  # the same at pitch 32
+    {"KMX_TC": "1", "KMX_TCS": "128", "KMX_TCS_PERSIST": "2"},  # and at pitch 128 (products of up to 80 rows of 128 bytes in one K-chunk)
     {"KMX_TC": "1", "KMX_TCJ": "1", "KMX_PACK_PAIR": "2"},  # chunked single-tile tensor-core kernel; paired packs at every batch size
     {"KMX_RECON_PAIR": "2"},    # one-CTA-per-pair reconstruction (kmx_recon2.cu) for every digit width <= 64, short streams too
     {"KMX_RECON_PAIR": "0", "KMX_RECON_BIAS_SMEM": "0", "KMX_RECON_WARP": "1"},  # k_recon_par family: signed prefix sums from L2; warp-per-stream recon
