@@ -86,6 +86,7 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
   buf[lane] = 0u;  // halo (FIN_HALO == 32)
   i64 cin_chunk = 0;  // carry + hi of the previous chunk's top limb
   bool bad = false;
+  long long jl_next = 0;
   for (int q00 = 0; q00 < Qd; q00 += FW_CH) {
     const int q0 = q00 + lane * FW_V;
     u32 lo[FW_V];
@@ -143,17 +144,25 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
       any |= d[v];
     }
     const int f1 = allF == 0xffffffffu ? 1 : 0, z1 = any == 0u ? 1 : 0;
-    // carry map: cin -1 -> c - all0, 0 -> c, +1 -> c + allF  (6-bit cm_ encoding)
-    u32 inc = (u32)(c - z1 + 1) | ((u32)(c + 1) << 2) | ((u32)(c + f1 + 1) << 4);
+    // carry map: cin -1 -> c - all0, 0 -> c, +1 -> c + allF, entry i = cout + 1 for cin = i - 1.
+    // Held in two forms so that a composition is one PRMT: bytes (the table that is indexed)
+    // and nibbles (the selector); x -> later(earlier(x)) = PRMT(later bytes, earlier nibbles).
+    const u32 e0 = (u32)(c - z1 + 1), e1 = (u32)(c + 1), e2 = (u32)(c + f1 + 1);
+    u32 incB = e0 | (e1 << 8) | (e2 << 16);
+    u32 incN = e0 | (e1 << 4) | (e2 << 8);
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-      const u32 pm = __shfl_up_sync(0xffffffffu, inc, o);
-      if (lane >= o) inc = cm_compose(pm, inc);
+      const u32 pmN = __shfl_up_sync(0xffffffffu, incN, o);
+      const u32 nb = __byte_perm(incB, 0u, pmN);  // byte i = incB[pmN nibble i] (byte 3 unused)
+      if (lane >= o) {
+        incB = nb;
+        incN = (nb & 0x3u) | ((nb >> 4) & 0x30u) | ((nb >> 8) & 0x300u);
+      }
     }
-    u32 exc = __shfl_up_sync(0xffffffffu, inc, 1);
-    if (lane == 0) exc = CM_IDENT;
-    const u32 tot = __shfl_sync(0xffffffffu, inc, 31);
-    int k = cm_apply(exc, 0);
+    u32 excB = __shfl_up_sync(0xffffffffu, incB, 1);
+    if (lane == 0) excB = 0x020100u;  // identity
+    const u32 totB = __shfl_sync(0xffffffffu, incB, 31);
+    int k = (int)((excB >> 8) & 0xffu) - 1;  // the preceding lanes' map at carry-in 0
     if (k) {  // ripple the carry-in through this lane's digits
 #pragma unroll
       for (int v = 0; v < FW_V; v++) {
@@ -162,7 +171,7 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
         k = k > 0 ? (d[v] == 0u ? 1 : 0) : (k < 0 && old == 0u ? -1 : 0);
       }
     }
-    cin_chunk = (i64)cm_apply(tot, 0) + hlast;
+    cin_chunk = (i64)((int)((totB >> 8) & 0xffu) - 1) + hlast;
     // exactness checks (bits below off, bits at or above E), chunk-uniform branch
     if (32LL * q00 < off || 32LL * (q00 + FW_CH) > E) {
 #pragma unroll
@@ -185,15 +194,16 @@ __device__ __forceinline__ void finish_warp_stream(const FinishArgs& a, int pair
     b4[1] = make_uint4(d[4], d[5], d[6], d[7]);
     __syncwarp();
     // digits whose top bit falls inside this chunk
-    const long long clo = 32LL * q00, chi = 32LL * (q00 + FW_CH);
+    const long long chi = 32LL * (q00 + FW_CH);
     // stream bit positions stay below 2^31 (products of < 2^26 limbs), so
     // 32-bit divisions
-    const int t = (int)(clo - off + 1);
-    long long jl = t <= 0 ? 0 : (t + W - 1) / W - 1;
-    if (jl < 0) jl = 0;
+    // jl: first digit whose top bit lies at or above clo = the previous chunk's jh
+    // (ceil((u + 1) / W) - 1 = floor(u / W) for u > 0), so one division per chunk
+    const long long jl = jl_next;
     const int u = (int)(chi - off);
     long long jh = u <= 0 ? 0 : u / W;
     if (jh > S.cnt) jh = S.cnt;
+    jl_next = jh;
     const long long base = off - 32LL * (q00 - FIN_HALO);
     if (W <= 32 * FIN_HALO) {
       // lean extraction: every digit handled here starts inside the halo or
