@@ -34,7 +34,10 @@ struct CfCur {
   int i, t;       // window start: bit t of coefficient i, 0 <= t < N
 };
 
-template <int IW, bool SMALLN>  // IW = 0: any in_words; SMALLN: N < 32 (several coefficients per limb)
+// BIAS (signed inputs, one word per coefficient): every loaded word is range-checked as a signed
+// b-bit value and lifted by 2^(b-1) (the bias lift of the signed path); the prefix sums the
+// correction needs are written by k_prefix_cf below.
+template <int IW, bool SMALLN, bool BIAS = false>  // IW = 0: any in_words; SMALLN: N < 32 (several coefficients per limb)
 __global__ void __launch_bounds__(CF_T) k_pack_cf(PackArgs A) {
   // grid: x = (pair, op), y = chunk of 4 * CF_T limbs
   const int job = blockIdx.x;
@@ -46,8 +49,18 @@ __global__ void __launch_bounds__(CF_T) k_pack_cf(PackArgs A) {
   const bool rev = (P.kind & 2) != 0;
   const int step = rev ? -iw : iw;
   const u32* cf = P.coeffs + (long long)pair * P.coeff_pair_stride;
-  const int topsh = (P.validate && (A.b & 31)) ? (A.b & 31) : 0;  // bits >= b of the top word must be zero
+  const int topsh = (!BIAS && P.validate && (A.b & 31)) ? (A.b & 31) : 0;  // bits >= b of the top word must be zero
   bool bad = false;
+  const u32 biasw = 1u << ((A.b - 1) & 31), bmask = A.b >= 32 ? 0xffffffffu : ((1u << A.b) - 1u);
+  const bool vchk = BIAS && P.validate && A.b < 32;
+  auto lift = [&](u32 raw) -> u32 {  // BIAS: signed range check + bias lift
+    if (!BIAS) return raw;
+    if (vchk) {
+      const int v = (int)raw;
+      bad |= v < -(1 << (A.b - 1)) || v >= (1 << (A.b - 1));
+    }
+    return (raw + biasw) & bmask;
+  };
   const int q0 = 4 * (blockIdx.y * CF_T + threadIdx.x);
   u32 d[4] = {0u, 0u, 0u, 0u};
   if (q0 < mq) {
@@ -64,7 +77,7 @@ __global__ void __launch_bounds__(CF_T) k_pack_cf(PackArgs A) {
       if (i < L) {
         const int w = t >> 5;
         if (IW == 1) {
-          const u32 lo = t < 32 ? __ldg(p) : 0u;
+          const u32 lo = t < 32 ? lift(__ldg(p)) : 0u;
           if (topsh && t < 32) bad |= (lo >> topsh) != 0u;
           x = lo >> (t & 31);
         } else if (w < iw) {
@@ -79,12 +92,12 @@ __global__ void __launch_bounds__(CF_T) k_pack_cf(PackArgs A) {
           const u32* pn = p;
           for (int k = 1, s2 = sh; s2 < 32 && i + k < L; k++, s2 += N) {
             pn += step;
-            const u32 lo = __ldg(pn);
+            const u32 lo = IW == 1 ? lift(__ldg(pn)) : __ldg(pn);
             if (topsh) bad |= (lo >> topsh) != 0u;
             x |= lo << s2;
           }
         } else if (sh < 32 && i + 1 < L) {
-          const u32 lo = __ldg(p + step);
+          const u32 lo = IW == 1 ? lift(__ldg(p + step)) : __ldg(p + step);
           if (topsh && iw == 1) bad |= (lo >> topsh) != 0u;
           x |= lo << sh;
         }
@@ -117,17 +130,31 @@ __global__ void __launch_bounds__(CF_T) k_pack_cf(PackArgs A) {
   }
 }
 
+// Prefix sums of the lifted coefficients of one operand vector per CTA (signed path):
+// out[0] = 0, out[i + 1] = sum_{k <= i} ((c_k + 2^(b-1)) mod 2^b).
+__global__ void __launch_bounds__(256) k_prefix_cf(const u32* coeffs, long long coeff_pair_stride, int len, int b,
+                                                   unsigned long long* prefix, long long prefix_pair_stride) {
+  const long long pair = blockIdx.x;
+  const u32 biasw = 1u << ((b - 1) & 31), bmask = b >= 32 ? 0xffffffffu : ((1u << b) - 1u);
+  block_prefix_u64(coeffs + pair * coeff_pair_stride, len, biasw, bmask, prefix + pair * prefix_pair_stride);
+}
+
 }  // namespace
 
-// Carry-free, unsigned, every output row padded to 4 limbs and 16-byte aligned.
+// Carry-free, every output row padded to 4 limbs and 16-byte aligned; unsigned inputs, or signed
+// one-word inputs (bias lift in the kernel, prefix sums by k_prefix_cf).
 bool pack_cf_ok(const PackArgs& a, int batch) {
   static const int force = getenv("KMX_PACK_CF") ? atoi(getenv("KMX_PACK_CF")) : -1;
   if (force == 0) return false;
-  if (a.N < a.b || a.bias || a.nops < 1 || batch < 1) return false;
+  // signed inputs: opt-in (KMX_PACK_CF_SIGNED=1).  Measured at c2: the streaming pack plus its two
+  // prefix-sum launches take 42.8 / 44.7 us (ks1 / ks2) against 35.4 / 39.2 us for the block kernel
+  static const int cf_signed = getenv("KMX_PACK_CF_SIGNED") ? atoi(getenv("KMX_PACK_CF_SIGNED")) : 0;
+  if (a.N < a.b || a.nops < 1 || batch < 1) return false;
+  if (a.bias && (!cf_signed || a.in_words != 1 || a.b < 1 || a.b > 32)) return false;
   long long limbs = 0;
   for (int i = 0; i < a.nops; i++) {
     const PackOp& p = a.op[i];
-    if ((p.kind & 1) || p.prefix) return false;
+    if ((p.kind & 1) || (p.prefix && !a.bias)) return false;
     if ((reinterpret_cast<uintptr_t>(p.out) & 15) || (p.out_pair_stride & 3)) return false;
     if (p.out_pair_stride < ((p.m + 3) & ~3)) return false;  // room for the rounding limbs
     if ((long long)p.len * a.N + 64 >= (1LL << 31) || p.m > 65535LL * 4 * CF_T) return false;
@@ -140,6 +167,7 @@ bool pack_cf_ok(const PackArgs& a, int batch) {
       return false;
   // measured (config-5 sweep with KMX_PACK_CF=0 / 1): large calls always; small ones only with
   // multi-word coefficients on operands of >= 256 limbs (3-10% faster; one-word or short: 3-25% slower)
+  if (a.bias) return force == 1 || limbs >= (1LL << 19);
   return force == 1 || limbs >= (1LL << 20) || (a.in_words >= 2 && a.op[0].m >= 256 && a.op[0].len >= 64);
 }
 
@@ -153,6 +181,17 @@ cudaError_t launch_pack_cf(const PackArgs& a, int batch, cudaStream_t st) {
   // (f and g operands may differ in m: the grid covers the larger, each CTA bounds by its own)
   dim3 grid(batch * a.nops, (mq / 4 + CF_T - 1) / CF_T);
   if (grid.y > 65535) return cudaErrorInvalidValue;
+  if (a.bias) {
+    if (a.N < 32) k_pack_cf<1, true, true><<<grid, CF_T, 0, st>>>(a);
+    else k_pack_cf<1, false, true><<<grid, CF_T, 0, st>>>(a);
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    for (int i = 0; i < a.nops; i++) {
+      const PackOp& p = a.op[i];
+      if (!p.prefix) continue;
+      k_prefix_cf<<<batch, 256, 0, st>>>(p.coeffs, p.coeff_pair_stride, p.len, a.b, p.prefix, p.prefix_pair_stride);
+    }
+    return cudaGetLastError();
+  }
   if (a.N < 32) {
     if (a.in_words == 1) k_pack_cf<1, true><<<grid, CF_T, 0, st>>>(a);
     else k_pack_cf<0, true><<<grid, CF_T, 0, st>>>(a);

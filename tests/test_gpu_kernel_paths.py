@@ -47,6 +47,7 @@ SETTINGS = [
     {"KMX_WIDE": "1"},          # wide-digit finish + multiword reconstruction for every unsigned shape
     {"KMX_PACK_W1": "0", "KMX_PACK_CF": "0"},  # block-per-job pack everywhere (no warp-per-job, no streaming kernel)
     {"KMX_PACK_CF": "1"},       # streaming carry-free pack (kmx_packcf.cu) for every unsigned ks1 / ks2 shape
+    {"KMX_PACK_CF": "1", "KMX_PACK_CF_SIGNED": "1"},  # and for signed ones (bias lift in the kernel, prefix sums by k_prefix_cf)
     {"KMX_PACK_W1": "1"},       # warp-per-job pack for every one- and two-word shape (single and paired jobs)
     {"KMX_PACK_W1": "1", "KMX_PACK_PSPLIT": "0"},  # the same with the signed prefix sums by the forward job alone
     {"KMX_PACK_SEG": "1", "KMX_BKS_UNI": "0", "KMX_BEVAL_STAGED": "0"},  # segmented pack; bivariate: IMAD products, unstaged evaluation
